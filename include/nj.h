@@ -1,0 +1,265 @@
+/*
+ * nj.h — C ABI of libnj: batched speculative-decoding verification on B200 (sm_100a)
+ * and the Nightjar speculative-length bandit that drives it.
+ *
+ * Citation keys: P:n = PAPER.md line n (arXiv 2512.22420, LaTeX source);
+ * S:n = SPEC.md line n; BJ = BASELINE.json north_star; "Leviathan" = the
+ * speculative-sampling algorithm the paper cites at P:23 (leviathan2023fast).
+ * DESIGN.md "Readings" R1..R14 resolve every place the paper is silent.
+ *
+ * ------------------------------------------------------------------------
+ * Packed ragged batch (P:73 continuous batching; BJ "per-request variable-γ").
+ *   B requests, request b carries gamma_b ∈ [0, gamma_max] drafts.
+ *   N  = Σ_b (gamma_b + 1)  rows (verified positions),  G = Σ_b gamma_b drafts.
+ *   row_off[b]   = Σ_{b'<b} (gamma_b' + 1)   (host exclusive scan, done inside)
+ *   draft_off[b] = Σ_{b'<b} gamma_b'
+ *   Row row_off[b]+j (j = 0..gamma_b) holds the target's final hidden state
+ *   whose LM-head logits give p_j, the target distribution for position j;
+ *   row j = gamma_b is the bonus position.  Draft i (i < gamma_b) of request b
+ *   is draft_tokens[draft_off[b]+i] ~ q_i, with q_i = draft_probs row
+ *   draft_off[b]+i.  Uniform slot row_off[b]+i (i < gamma_b) is the i-th
+ *   acceptance test, slot row_off[b]+gamma_b is the final draw (R3).
+ *
+ * What nj_verify computes, per request b (Leviathan; BJ steps 1-3; R1):
+ *   l_j(x)  = Σ_k W[x,k]·h_j[k]                (LM head, fp32 accumulate)
+ *   p_j(x)  = exp(l_j(x) − lse_j), lse_j = log Σ_x exp l_j(x)  (online softmax)
+ *   n_b     = first i < gamma_b with NOT(u_i·q_i(x_i) < p_i(x_i)), else gamma_b (R2)
+ *   w(x)    = max(0, p_n(x) − q_n(x))  if n_b < gamma_b   (residual)
+ *           = p_gamma(x)               otherwise          (bonus)
+ *   W_b     = Σ_x w(x);  if W_b == 0 use w = p_n (R6)
+ *   t_b     = min{x : Σ_{y≤x} w(y) > u_gamma·W_b}  ascending id (R5);
+ *             on rounding overshoot the last x with w(x) > 0.
+ *   accept_len[b] = n_b,  next_token[b] = t_b.
+ * Decisions are certified: any acceptance test or draw whose fp32 margin is
+ * inside the kernel's error bound is recomputed in fp64 on the GPU (R11/R12,
+ * DESIGN.md "certified fallback"), so outputs equal the fp64 definition.
+ *
+ * Conventions (all functions):
+ *   - The caller owns every I/O buffer; nj_ctx owns its device workspace,
+ *     sized at nj_create for max_batch and gamma_max.
+ *   - Device functions are asynchronous on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream); outputs are valid after the stream
+ *     synchronises.  No device->host synchronisation happens inside nj_verify
+ *     (gamma_per_req is a HOST array so every shape is known on the host), so
+ *     it is CUDA-graph capturable.
+ *   - One nj_ctx per stream; a ctx is not thread-safe.  The bandit is
+ *     single-threaded.
+ *   - Host-side shape and pointer checks return NJ_EINVAL / NJ_ESHAPE before
+ *     any launch.  CUDA / NCCL failures return NJ_ECUDA / NJ_ENCCL; the
+ *     message is available from nj_last_error.  Element values are not
+ *     validated (u must be in [0,1), tokens in [0,V), q_i(x_i) > 0 expected).
+ *   - bf16 tensors are passed as uint16_t bit patterns (IEEE bfloat16).
+ *   - There is no CPU fallback: without a visible sm_100 device nj_create
+ *     fails with NJ_ECUDA.
+ */
+#ifndef NJ_H
+#define NJ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NJ_OK = 0,
+    NJ_EINVAL = 1,        /* bad argument (NULL pointer, value out of range) */
+    NJ_ESHAPE = 2,        /* inconsistent sizes / alignment */
+    NJ_ECUDA = 3,         /* CUDA runtime / driver error */
+    NJ_ENCCL = 4,         /* NCCL error */
+    NJ_ENOMEM = 5,        /* allocation failed */
+    NJ_EUNSUPPORTED = 6   /* configuration not supported by this build */
+} nj_status;
+
+typedef struct nj_ctx nj_ctx;
+typedef struct nj_bandit nj_bandit;
+
+/* ---------------------------------------------------------------- verify */
+
+typedef struct {
+    int32_t d;          /* hidden size; d % 8 == 0 (16-byte TMA row pitch)        */
+    int32_t V;          /* GLOBAL vocabulary size, V >= 1                          */
+    int32_t max_batch;  /* B_max, 1..4096                                   */
+    int32_t gamma_max;  /* Γ_max, 0..15                                     */
+    int32_t device;     /* CUDA device ordinal                                     */
+    void*   nccl_comm;  /* NULL: unsharded.  Else an ncclComm_t: vocab-sharded LM  */
+                        /* head (BJ config 5); this rank owns W rows [v_begin,v_end) */
+    int32_t v_begin;    /* shard start (global id); unsharded: 0                   */
+    int32_t v_end;      /* shard end (exclusive);   unsharded: V                   */
+} nj_config;
+
+/* Optional per-call debug outputs (device buffers; any member may be NULL). */
+typedef struct {
+    float*   lse;      /* [N]  lse_j; NaN for rows the chosen path never evaluates  */
+                       /*      (two-pass path: bonus row of a rejected request)     */
+    float*   p_draft;  /* [G]  p_i(x_i), fp32                                       */
+    double*  mass;     /* [B]  W_b of the distribution actually drawn from          */
+    int32_t* flags;    /* [B]  NJ_FLAG_* bits                                       */
+} nj_debug;
+
+#define NJ_FLAG_FALLBACK  1  /* request recomputed by the fp64 certified fallback   */
+#define NJ_FLAG_ZERO_MASS 2  /* residual mass 0 -> drew from p_n (R6)              */
+#define NJ_FLAG_CLAMP     4  /* inverse-CDF overshoot -> clamped (R5)              */
+
+/* Create a context on cfg->device.  Allocates the workspace for max_batch /
+ * gamma_max.  Fails with NJ_ECUDA if the device is not sm_100. */
+nj_status nj_create(const nj_config* cfg, nj_ctx** out);
+void      nj_destroy(nj_ctx* ctx);
+/* Last error message of ctx (static storage inside ctx; "" if none).  With
+ * ctx == NULL returns the last nj_create failure message of this thread. */
+const char* nj_last_error(const nj_ctx* ctx);
+
+/* Verify one packed batch (see header comment).  Device pointers:
+ *   hidden       [N, d]      bf16 row-major
+ *   W_lm         [v_end - v_begin, d] bf16 row-major (nn.Linear weight layout)
+ *   draft_tokens [G]         int32 global token ids
+ *   draft_probs  [G, ldq]    fp32 full draft distributions q_i (ldq >= V,
+ *                            ldq % 4 == 0); sharded ranks read cols [v_begin,v_end)
+ *   uniforms     [N]         fp32 in [0,1)
+ *   accept_len   [B]         int32 out
+ *   next_token   [B]         int32 out
+ * Host pointer: gamma_per_req [B], each in [0, gamma_max].
+ * B in [1, max_batch].  dbg may be NULL. */
+nj_status nj_verify(nj_ctx* ctx, void* stream,
+                    const uint16_t* hidden, const uint16_t* W_lm,
+                    const int32_t* draft_tokens,
+                    const float* draft_probs, int64_t ldq,
+                    const int32_t* gamma_per_req, const float* uniforms,
+                    int32_t B, int32_t* accept_len, int32_t* next_token,
+                    const nj_debug* dbg);
+
+/* End-to-end variant: every per-step input and output is a HOST pointer
+ * (pinned memory recommended); W_lm stays a resident device pointer (model
+ * weight).  Copies the inputs into ctx staging buffers on `stream`, runs
+ * nj_verify, copies accept_len / next_token back and synchronises `stream`
+ * before returning.  ldq as above (host row pitch). */
+nj_status nj_verify_host(nj_ctx* ctx, void* stream,
+                         const uint16_t* hidden_h, const uint16_t* W_lm,
+                         const int32_t* draft_tokens_h,
+                         const float* draft_probs_h, int64_t ldq,
+                         const int32_t* gamma_per_req, const float* uniforms_h,
+                         int32_t B, int32_t* accept_len_h, int32_t* next_token_h);
+
+/* Execution path of nj_verify. */
+typedef enum {
+    NJ_PATH_AUTO = 0,    /* pick by size            */
+    NJ_PATH_FUSED = 1,   /* one persistent kernel, logits resident in TMEM       */
+    NJ_PATH_TWOPASS = 2  /* stats GEMM over drafts, accept, sample-row GEMM,     */
+                         /* sampler kernels                                      */
+} nj_path;
+
+typedef enum {
+    NJ_OPT_PATH = 1,          /* value: nj_path                                  */
+    NJ_OPT_CERTIFY = 2,       /* 1 (default): certified fp64 fallback on; 0 off  */
+    NJ_OPT_FORCE_FALLBACK = 3,/* 1: recompute EVERY request in fp64 (tests)      */
+    NJ_OPT_PROFILE = 4        /* 1: bracket the dominant kernel of every nj_verify */
+                              /*    with CUDA events (see nj_kernel_time)           */
+} nj_option;
+
+nj_status nj_set_option(nj_ctx* ctx, nj_option opt, int64_t value);
+
+/* Device time of the dominant kernel (fused verify kernel, or the stats GEMM
+ * of the two-pass path) accumulated since the last reset, measured with CUDA
+ * events recorded on the launch stream (NJ_OPT_PROFILE must be on).
+ * Synchronises those events.  reset != 0 clears the accumulator. */
+nj_status nj_kernel_time(nj_ctx* ctx, double* ms_total, int64_t* launches, int32_t reset);
+
+/* Which path nj_verify would take for this batch and how many kernels it
+ * launches (for bench accounting).  Host only. */
+nj_status nj_plan(nj_ctx* ctx, const int32_t* gamma_per_req, int32_t B,
+                  int32_t* path_out, int32_t* launches_out);
+
+/* ---- test-only stage exports (used by tests/ for stage-isolated parity) ---- */
+
+/* LM-head GEMM probe: logits[r, x] = Σ_k W[x,k]·hidden[rows[r],k] for
+ * x in [0, v_end-v_begin), written fp32 row-major with pitch ld_out (>= V_local).
+ * Same tcgen05 mainloop as nj_verify.  rows: device int32 [n_rows]. */
+nj_status nj_lmhead_logits(nj_ctx* ctx, void* stream,
+                           const uint16_t* hidden, const uint16_t* W_lm,
+                           const int32_t* rows, int32_t n_rows,
+                           float* logits, int64_t ld_out);
+
+/* Accuracy probe (test-only): same GEMM with the TMEM accumulator restarted
+ * every ks MMA steps (K=16 each) and the partials summed in fp64; writes the
+ * fp64 sums.  n_rows <= 32.  Used to characterise tensor-core accumulation
+ * error. */
+nj_status nj_lmhead_logits_ks(nj_ctx* ctx, void* stream,
+                              const uint16_t* hidden, const uint16_t* W_lm,
+                              const int32_t* rows, int32_t n_rows,
+                              double* logits, int64_t ld_out, int32_t ks);
+
+/* TMA streaming microbenchmark (test-only): every CTA
+ * pulls its vocab share of W through a TMA ring of nstages stages of `group`
+ * 64x128 boxes (mode 0/1; mode 2 = pre-tiled W), optionally with an H box of
+ * hrows rows per k-block.  No compute. */
+nj_status nj_stream_test(nj_ctx* ctx, void* stream, const uint16_t* W, int32_t mode, int32_t group,
+                         int32_t nstages, const uint16_t* H, int32_t hrows);
+
+/* Sampler stage (BJ step 3, residual / bonus draw) on given fp32 logits:
+ *   logits   [B, ld_l] fp32 device, one row per request over the full vocab V
+ *   residual [B] int32 device: 1 -> w = max(0, p − q_row), 0 -> w = p
+ *   q        [B, ldq] fp32 device (read only for residual rows)
+ *   u        [B] fp32 device final-draw uniforms
+ *   out: next_token [B] int32, mass [B] double (W_b, may be NULL).
+ * lse of each row is computed from the given logits.  Unsharded ctx only. */
+nj_status nj_sample_from_logits(nj_ctx* ctx, void* stream,
+                                const float* logits, int64_t ld_l,
+                                const int32_t* residual,
+                                const float* q, int64_t ldq,
+                                const float* u, int32_t B,
+                                int32_t* next_token, double* mass);
+
+/* ---------------------------------------------------------------- bandit */
+/* Nightjar arm selection (Algorithm 1) with the
+ * c_prefill lookup (Table 1).  Host-only, no device code.
+ * RNG: SplitMix64 over (seed, draw counter), draws consumed in the order
+ * bin-type draw, then uniform-arm draw (R14). */
+
+/* gamma_max >= 1, batch_max >= 1.  len_buckets[n_len],
+ * batch_buckets[n_batch] strictly increasing; cost_ms[n_len*n_batch]
+ * row-major by length bucket (NULL → c_prefill ≡ 0). */
+nj_status nj_bandit_create(int32_t gamma_max, int32_t batch_max, uint64_t seed,
+                           const int32_t* len_buckets, int32_t n_len,
+                           const int32_t* batch_buckets, int32_t n_batch,
+                           const double* cost_ms, nj_bandit** out);
+void nj_bandit_destroy(nj_bandit* b);
+
+/* γ_t for the current step (Algorithm 1).  batch_size in
+ * 1..batch_max, l_max >= 0 the effective skip length.  Returns
+ * γ >= 0, or -NJ_EINVAL on bad arguments. */
+int32_t nj_select_gamma(nj_bandit* b, int32_t batch_size, int32_t l_max);
+
+/* Reward feedback (Algorithm 1 line 190 + counters 191-200).  reward is the
+ * realised goodput in tokens/s, >= 0. */
+nj_status nj_observe(nj_bandit* b, int32_t batch_size, int32_t gamma,
+                     double reward_tok_per_s);
+
+/* Eq. 3 score of one candidate: 1/g̃ + 1(γ_prev=0 ∧ γ>0)·c_prefill/γ,
+ * c_prefill in seconds.  Returns NaN for an unvisited arm. */
+double nj_exploitation_score(const nj_bandit* b, int32_t batch_size,
+                             int32_t gamma_prev, int32_t gamma, int32_t l_max);
+
+/* c_prefill(L_max, B) in milliseconds: ceiling bucket with clamp; 0 if
+ * L_max == 0. */
+double nj_prefill_cost_ms(const nj_bandit* b, int32_t l_max, int32_t batch_size);
+
+/* Inspection for tests: hierarchy counters of batch size B
+ * (j_B, H_B, b_B, τ_B, bin type: -1 unset, 0 exploit, 1 explore) and
+ * arm statistics (g̃_{B,γ}, visit count). */
+nj_status nj_bandit_state(const nj_bandit* b, int32_t batch_size,
+                          int32_t* j, int64_t* H, int64_t* bin, int64_t* tau,
+                          int32_t* bin_type);
+nj_status nj_bandit_arm(const nj_bandit* b, int32_t batch_size, int32_t gamma,
+                        double* mean, int64_t* count);
+int32_t   nj_bandit_last_gamma(const nj_bandit* b);
+
+/* JSON snapshot.  Writes at most cap bytes (NUL-terminated),
+ * *needed = full length + 1.  NJ_ESHAPE if cap is too small. */
+nj_status nj_bandit_snapshot_json(const nj_bandit* b, char* buf, size_t cap,
+                                  size_t* needed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NJ_H */

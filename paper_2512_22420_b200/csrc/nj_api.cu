@@ -1,0 +1,744 @@
+// nj_api.cu — host side of libnj: the C ABI of include/nj.h.
+//
+// Validation, workspace ownership, TMA tensor-map encoding, path planning and
+// launch sequencing for nj_verify (BJ steps 1-3), plus the
+// test-only stage exports.  No device->host synchronisation happens inside
+// nj_verify: gamma_per_req is a host array, so every shape (N, G, row offsets)
+// is known here and passed to the kernels by value (graph capturable).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "nj.h"
+#include "nj_gemm.cuh"
+#include "nj_sampler.cuh"
+#include "nj_probe_ks.cuh"
+#include "nj_stream_test.cuh"
+
+using namespace nj;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 K-major tensor [rows, d], box {64, box_rows}, SWIZZLE_128B.
+bool encode_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t d, int box_rows) {
+    EncodeTiledFn fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline int round16(int x) { return (x + 15) & ~15; }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// device smem carve-up mirrors (must match nj_gemm.cuh / nj_fused.cuh)
+size_t gemm_rows_tail(int R, bool stats, bool capture, int S) {
+    size_t t = 4 * 256 * sizeof(float2);
+    if (stats) t += (size_t)R * sizeof(float2);
+    if (capture) t += (size_t)R * sizeof(int32_t);
+    t = align_up(t, 8);
+    t += (size_t)(2 * S + 4) * 8 + 8;
+    return t;
+}
+size_t fused_tail(int NPAD, int S) {
+    const int kMaxT = 16;
+    size_t t = 0;
+    t += 4 * NPAD * sizeof(float2);
+    t += NPAD * sizeof(double);
+    t += NPAD * sizeof(ReqInfo);
+    t += (size_t)NPAD * kMaxT * 4 * sizeof(float);
+    t += (size_t)NPAD * (kMaxT + 1) * sizeof(double);
+    t += NPAD * sizeof(double);
+    t += 3 * NPAD * sizeof(int32_t) + 4 * sizeof(int32_t);
+    t = align_up(t, 8);
+    t += (size_t)(2 * S + 16) * 8 + 8;
+    return t;
+}
+
+struct Dev {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace
+
+struct nj_ctx {
+    nj_config cfg{};
+    int V_local = 0;
+    int num_sms = 0;
+    int grid = 0;       // persistent grid (CTAs)
+    int U = 0;          // 16-row vocab units
+    int max_tiles = 0;  // max 128-row tiles per CTA
+    int nchunks = 0;    // sampler chunks
+    int Nmax = 0, Gmax = 0;
+    // options
+    int path_opt = NJ_PATH_AUTO;
+    int certify = 1;
+    int force_fb = 0;
+    int profile = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // recorded, not yet harvested
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;
+    double prof_ms = 0.0;
+    int64_t prof_n = 0;
+    // certificate margins: fused path logits err <= 6e-7 (ln p);
+    // two-pass path (plain tcgen05 accumulation) err <= 8e-5 (lse)
+    float eps_acc_fused = 2e-6f, eps_draw_fused = 0.f;
+    float eps_acc = 2e-4f;
+    float eps_draw = 1.5e-5f;
+    std::string err;
+    // workspace
+    std::vector<void*> allocs;
+    float *part_m = nullptr, *part_s = nullptr, *part2_m = nullptr, *part2_s = nullptr;
+    double* dl = nullptr;
+    double *wpart = nullptr, *s_lse = nullptr, *cmass = nullptr, *fb_logits = nullptr, *lse_tmp = nullptr;
+    uint16_t *hd = nullptr, *hs = nullptr;
+    float* logits_s = nullptr;
+    int32_t *s_resid = nullptr, *s_qrow = nullptr;
+    int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
+    uint32_t* bar = nullptr;       // count, gen
+    int32_t* scratch_i = nullptr;  // [MB]
+    // host-API staging (lazy)
+    uint16_t* st_hidden = nullptr;
+    int32_t* st_tok = nullptr;
+    float *st_q = nullptr, *st_u = nullptr;
+    int32_t *st_acc = nullptr, *st_next = nullptr;
+    int64_t st_ldq = 0;
+    // W tensor-map cache
+    const void* w_cached = nullptr;
+    CUtensorMap tmW128{}, tmW16{};
+
+    int32_t* fb_count() { return fb_block; }
+    int32_t* fb_list() { return fb_block + 1; }
+    int32_t* req_flags() { return fb_block + 1 + cfg.max_batch; }
+};
+
+namespace {
+
+nj_status set_err(nj_ctx* c, nj_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf; else g_create_error = buf;
+    return st;
+}
+
+// NJ_TRACE=1: synchronise after every launch and report it on stderr (debug).
+bool trace_on() {
+    static int on = -1;
+    if (on < 0) { const char* e = getenv("NJ_TRACE"); on = (e && *e == '1') ? 1 : 0; }
+    return on == 1;
+}
+cudaError_t trace(const char* what, cudaStream_t st) {
+    cudaError_t e = cudaGetLastError();
+    if (!trace_on() || e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(st);
+    fprintf(stderr, "[nj] %s -> %s\n", what, cudaGetErrorString(e));
+    return e;
+}
+#define NJ_LAUNCHED(ctx, name, st) NJ_CUDA(ctx, trace(name, st))
+
+#define NJ_CUDA(ctx, call)                                                                          \
+    do {                                                                                            \
+        cudaError_t e_ = (call);                                                                    \
+        if (e_ != cudaSuccess)                                                                      \
+            return set_err(ctx, NJ_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),   \
+                           __FILE__, __LINE__);                                                     \
+    } while (0)
+
+template <typename T>
+nj_status alloc(nj_ctx* c, T** p, size_t n) {
+    void* q = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+    if (e != cudaSuccess) return set_err(c, NJ_ENOMEM, "cudaMalloc(%zu) failed: %s", n * sizeof(T), cudaGetErrorString(e));
+    c->allocs.push_back(q);
+    *p = reinterpret_cast<T*>(q);
+    return NJ_OK;
+}
+
+template <typename K>
+cudaError_t set_smem_attr(K kernel) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+}
+
+nj_status ensure_w_maps(nj_ctx* c, const uint16_t* W) {
+    if (c->w_cached == W) return NJ_OK;
+    if (!encode_2d(&c->tmW128, W, c->V_local, c->cfg.d, 128) || !encode_2d(&c->tmW16, W, c->V_local, c->cfg.d, 16))
+        return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed for W_lm");
+    c->w_cached = W;
+    return NJ_OK;
+}
+
+struct Plan {
+    int B, N, G;
+    int path;
+    int npad;
+    std::vector<int32_t> row_off;
+};
+
+nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
+    if (!gamma) return set_err(c, NJ_EINVAL, "gamma_per_req is NULL");
+    if (B < 1 || B > c->cfg.max_batch) return set_err(c, NJ_ESHAPE, "B=%d outside [1, max_batch=%d]", B, c->cfg.max_batch);
+    pl.B = B;
+    pl.row_off.assign((size_t)B + 1, 0);
+    for (int b = 0; b < B; ++b) {
+        if (gamma[b] < 0 || gamma[b] > c->cfg.gamma_max)
+            return set_err(c, NJ_EINVAL, "gamma_per_req[%d]=%d outside [0, gamma_max=%d]", b, gamma[b], c->cfg.gamma_max);
+        pl.row_off[b + 1] = pl.row_off[b] + gamma[b] + 1;
+    }
+    pl.N = pl.row_off[B];
+    pl.G = pl.N - B;
+    pl.npad = round16(pl.N);
+    const bool fused_ok = pl.N <= kFusedMaxN && c->max_tiles <= 16 && (c->max_tiles + 1) * pl.npad <= 512 &&
+                          c->cfg.nccl_comm == nullptr;
+    int path = c->path_opt;
+    if (path == NJ_PATH_AUTO) path = fused_ok ? NJ_PATH_FUSED : NJ_PATH_TWOPASS;
+    if (path == NJ_PATH_FUSED && !fused_ok)
+        return set_err(c, NJ_EUNSUPPORTED, "fused path needs N <= %d and TMEM room (N=%d)", kFusedMaxN, pl.N);
+    pl.path = path;
+    return NJ_OK;
+}
+
+ReqMeta make_meta(const Plan& pl) {
+    ReqMeta m;
+    m.B = pl.B;
+    for (int b = 0; b <= pl.B; ++b) m.row_off[b] = pl.row_off[b];
+    return m;
+}
+
+// dominant-kernel event bracket (NJ_OPT_PROFILE)
+nj_status prof_begin(nj_ctx* c, cudaStream_t st, std::pair<cudaEvent_t, cudaEvent_t>& e) {
+    if (!c->profile) return NJ_OK;
+    if (c->ev_free.empty()) {
+        cudaEvent_t a, b;
+        NJ_CUDA(c, cudaEventCreate(&a));
+        NJ_CUDA(c, cudaEventCreate(&b));
+        c->ev_free.push_back({a, b});
+    }
+    e = c->ev_free.back();
+    c->ev_free.pop_back();
+    NJ_CUDA(c, cudaEventRecord(e.first, st));
+    return NJ_OK;
+}
+nj_status prof_end(nj_ctx* c, cudaStream_t st, std::pair<cudaEvent_t, cudaEvent_t>& e) {
+    if (!c->profile) return NJ_OK;
+    NJ_CUDA(c, cudaEventRecord(e.second, st));
+    c->ev.push_back(e);
+    return NJ_OK;
+}
+
+template <int NPAD>
+nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtensorMap& tmH, FusedParams& fp) {
+    // ring stages of GK k-blocks: one barrier round trip per 4 x 16 KB of W keeps
+    // the TMA stream at HBM speed (scripts/stream_test.py: 16-KB stages reach
+    // 4.75 TB/s, 64-KB stages 6.6 TB/s on B200)
+    int GK = 4;
+    if (const char* e = getenv("NJ_KGROUP")) GK = std::max(1, atoi(e));
+    const size_t stage = (size_t)GK * (kTileBytesA + NPAD * 128);
+    int S = (int)std::min<size_t>(8, (kSmemLimit - fused_tail(NPAD, 8) - 1024) / stage);
+    if (S < 2) { GK = 2; }
+    const size_t stage2 = (size_t)GK * (kTileBytesA + NPAD * 128);
+    S = (int)std::min<size_t>(8, (kSmemLimit - fused_tail(NPAD, 8) - 1024) / stage2);
+    fp.nstages = S;
+    fp.kgroup = GK;
+    fp.scratch_col = c->max_tiles * NPAD;
+    fp.nbuf = std::min(8, (512 - fp.scratch_col) / NPAD);
+    fp.kpd = 1;
+    fp.f32drain = 0;
+    if (const char* e = getenv("NJ_NBUF")) fp.nbuf = std::max(1, std::min(fp.nbuf, atoi(e)));   // tuning knobs
+    if (const char* e = getenv("NJ_KPD")) fp.kpd = std::max(1, atoi(e));
+    if (const char* e = getenv("NJ_F32DRAIN")) fp.f32drain = atoi(e);
+    const size_t smem = (size_t)S * stage2 + fused_tail(NPAD, S);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->grid);
+    cfg.blockDim = dim3(kFusedThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    nj_status ps = prof_begin(c, st, ev);
+    if (ps != NJ_OK) return ps;
+    NJ_CUDA(c, cudaLaunchKernelEx(&cfg, k_fused_verify<NPAD>, c->tmW128, c->tmW16, tmH, fp));
+    NJ_LAUNCHED(c, "k_fused_verify", st);
+    return prof_end(c, st, ev);
+    return NJ_OK;
+}
+
+// k_gemm_rows launcher (rows contiguous in `h`, R rows)
+template <bool WRITE, bool STATS, bool CAPTURE>
+nj_status launch_gemm_rows(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, GemmRowsParams gp) {
+    if (R <= 0) return NJ_OK;
+    const int box = std::min(256, round16(R));
+    CUtensorMap tmH;
+    if (!encode_2d(&tmH, h, R, c->cfg.d, box)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
+    gp.R = R;
+    gp.box_rows = box;
+    gp.nchunks = (R + box - 1) / box;
+    gp.V_local = c->V_local;
+    gp.U = c->U;
+    gp.num_kb = (c->cfg.d + kBK - 1) / kBK;
+    gp.v_begin = c->cfg.v_begin;
+    gp.part_ld = c->grid;
+    const size_t stage = kTileBytesA + (size_t)box * 128;
+    int S = (int)std::min<size_t>(8, (kSmemLimit - gemm_rows_tail(R, STATS, CAPTURE, 8) - 1024) / stage);
+    if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_rows: not enough shared memory (R=%d)", R);
+    gp.nstages = S;
+    const size_t smem = (size_t)S * stage + gemm_rows_tail(R, STATS, CAPTURE, S);
+    k_gemm_rows<WRITE, STATS, CAPTURE><<<c->grid, kThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
+    NJ_LAUNCHED(c, "k_gemm_rows", st);
+    return NJ_OK;
+}
+
+FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const int32_t* tok, const float* q,
+                   int64_t ldq, const float* u, int32_t* acc, int32_t* nxt, const nj_debug* dbg) {
+    FbParams f{};
+    f.hidden = hidden;
+    f.W = W;
+    f.d = c->cfg.d;
+    f.V_local = c->V_local;
+    f.v_begin = c->cfg.v_begin;
+    f.fb_count = c->fb_count();
+    f.fb_list = c->fb_list();
+    f.req_flags = c->req_flags();
+    f.fb_logits = c->fb_logits;
+    f.draft_tokens = tok;
+    f.q = q;
+    f.ldq = ldq;
+    f.u = u;
+    f.accept_len = acc;
+    f.next_token = nxt;
+    f.dbg_mass = dbg ? dbg->mass : nullptr;
+    f.dbg_flags = dbg ? dbg->flags : nullptr;
+    return f;
+}
+
+nj_status launch_fallback(nj_ctx* c, cudaStream_t st, const FbParams& f, const ReqMeta& m) {
+    k_fb_logits<<<c->num_sms * 2, 256, 0, st>>>(f, m);
+    NJ_LAUNCHED(c, "k_fb_logits", st);
+    k_fb_decide<<<std::min(c->cfg.max_batch, c->num_sms), 256, 0, st>>>(f, m);
+    NJ_LAUNCHED(c, "k_fb_decide", st);
+    return NJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
+    if (!cfg || !out) return set_err(nullptr, NJ_EINVAL, "NULL argument");
+    *out = nullptr;
+    if (cfg->d < 8 || cfg->d % 8 != 0) return set_err(nullptr, NJ_ESHAPE, "d=%d must be a positive multiple of 8", cfg->d);
+    if (cfg->V < 1) return set_err(nullptr, NJ_ESHAPE, "V=%d", cfg->V);
+    if (cfg->max_batch < 1 || cfg->max_batch > kMaxB)
+        return set_err(nullptr, NJ_ESHAPE, "max_batch=%d outside [1, %d]", cfg->max_batch, kMaxB);
+    if (cfg->gamma_max < 0 || cfg->gamma_max > 15) return set_err(nullptr, NJ_ESHAPE, "gamma_max=%d outside [0,15]", cfg->gamma_max);
+    if (cfg->v_begin < 0 || cfg->v_end > cfg->V || cfg->v_begin >= cfg->v_end)
+        return set_err(nullptr, NJ_ESHAPE, "bad shard [%d,%d) of V=%d", cfg->v_begin, cfg->v_end, cfg->V);
+    if (cfg->nccl_comm) return set_err(nullptr, NJ_EUNSUPPORTED, "vocab-sharded mode is not built in this round");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_err(nullptr, NJ_ECUDA, "no CUDA device visible (libnj has no CPU fallback)");
+    if (cfg->device < 0 || cfg->device >= ndev) return set_err(nullptr, NJ_EINVAL, "device %d of %d", cfg->device, ndev);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess) return set_err(nullptr, NJ_ECUDA, "cudaGetDeviceProperties failed");
+    if (prop.major != 10 || prop.minor != 0)
+        return set_err(nullptr, NJ_ECUDA, "device %d is sm_%d%d; libnj is built for sm_100a only", cfg->device, prop.major, prop.minor);
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return set_err(nullptr, NJ_ECUDA, "cudaSetDevice failed");
+    if (!get_encode_fn()) return set_err(nullptr, NJ_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+
+    nj_ctx* c = new nj_ctx();
+    c->cfg = *cfg;
+    c->V_local = cfg->v_end - cfg->v_begin;
+    c->num_sms = prop.multiProcessorCount;
+    c->U = (c->V_local + kUnit - 1) / kUnit;
+    c->grid = std::min(c->num_sms, c->U);
+    const int upc = (c->U + c->grid - 1) / c->grid;
+    c->max_tiles = (upc * kUnit + kTileV - 1) / kTileV;
+    c->nchunks = (c->V_local + kChunk - 1) / kChunk;
+    const int MB = cfg->max_batch, GM = cfg->gamma_max;
+    c->Nmax = MB * (GM + 1);
+    c->Gmax = std::max(1, MB * GM);
+    nj_status s = NJ_OK;
+    const size_t g = (size_t)c->grid;
+#define A(ptr, n) if ((s = alloc(c, &c->ptr, (n))) != NJ_OK) { nj_destroy(c); return s; }
+    A(part_m, (size_t)c->Nmax * g);
+    A(part_s, (size_t)c->Nmax * g);
+    A(part2_m, (size_t)MB * g);
+    A(part2_s, (size_t)MB * g);
+    A(dl, (size_t)c->Gmax);
+    A(wpart, (size_t)MB * g);
+    A(s_lse, (size_t)MB);
+    A(lse_tmp, (size_t)MB);
+    A(cmass, (size_t)MB * c->nchunks);
+    A(fb_logits, (size_t)c->Nmax * c->V_local);
+    A(hd, (size_t)c->Gmax * cfg->d);
+    A(hs, (size_t)MB * cfg->d);
+    A(logits_s, (size_t)MB * c->V_local);
+    A(s_resid, (size_t)MB);
+    A(s_qrow, (size_t)MB);
+    A(fb_block, (size_t)1 + 2 * MB);
+    A(bar, 2);
+    A(scratch_i, (size_t)MB);
+#undef A
+    if (cudaMemset(c->bar, 0, 2 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMemset(c->fb_block, 0, (1 + 2 * MB) * sizeof(int32_t)) != cudaSuccess) {
+        nj_destroy(c);
+        return set_err(nullptr, NJ_ECUDA, "cudaMemset failed");
+    }
+    cudaError_t e = cudaSuccess;
+    e = e ? e : set_smem_attr(k_fused_verify<16>);
+    e = e ? e : set_smem_attr(k_fused_verify<32>);
+    e = e ? e : set_smem_attr(k_fused_verify<48>);
+    e = e ? e : set_smem_attr(k_gemm_rows<true, false, false>);
+    e = e ? e : set_smem_attr(k_gemm_rows<false, true, true>);
+    e = e ? e : set_smem_attr(k_gemm_rows<true, true, false>);
+    if (e != cudaSuccess) {
+        nj_destroy(c);
+        return set_err(nullptr, NJ_ECUDA, "cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
+    }
+    *out = c;
+    return NJ_OK;
+}
+
+void nj_destroy(nj_ctx* c) {
+    if (!c) return;
+    for (auto& e : c->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    for (auto& e : c->ev_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    for (void* p : c->allocs) cudaFree(p);
+    delete c;
+}
+
+const char* nj_last_error(const nj_ctx* c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+nj_status nj_set_option(nj_ctx* c, nj_option opt, int64_t v) {
+    if (!c) return NJ_EINVAL;
+    switch (opt) {
+        case NJ_OPT_PATH:
+            if (v < NJ_PATH_AUTO || v > NJ_PATH_TWOPASS) return set_err(c, NJ_EINVAL, "bad path %lld", (long long)v);
+            c->path_opt = (int)v;
+            return NJ_OK;
+        case NJ_OPT_CERTIFY: c->certify = v != 0; return NJ_OK;
+        case NJ_OPT_FORCE_FALLBACK: c->force_fb = v != 0; return NJ_OK;
+        case NJ_OPT_PROFILE: c->profile = v != 0; return NJ_OK;
+    }
+    return set_err(c, NJ_EINVAL, "unknown option %d", (int)opt);
+}
+
+nj_status nj_kernel_time(nj_ctx* c, double* ms_total, int64_t* launches, int32_t reset) {
+    if (!c) return NJ_EINVAL;
+    for (auto& e : c->ev) {
+        NJ_CUDA(c, cudaEventSynchronize(e.second));
+        float ms = 0.f;
+        NJ_CUDA(c, cudaEventElapsedTime(&ms, e.first, e.second));
+        c->prof_ms += ms;
+        c->prof_n += 1;
+        c->ev_free.push_back(e);
+    }
+    c->ev.clear();
+    if (ms_total) *ms_total = c->prof_ms;
+    if (launches) *launches = c->prof_n;
+    if (reset) { c->prof_ms = 0.0; c->prof_n = 0; }
+    return NJ_OK;
+}
+
+nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out, int32_t* launches_out) {
+    if (!c) return NJ_EINVAL;
+    Plan pl;
+    nj_status s = make_plan(c, gamma, B, pl);
+    if (s != NJ_OK) return s;
+    int n = 0;
+    if (pl.path == NJ_PATH_FUSED) n = 1;
+    else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) : 0) + 4;   // gather+KA, KB, KC, KD1, KD2
+    if (c->certify) n += 2;
+    if (path_out) *path_out = pl.path;
+    if (launches_out) *launches_out = n;
+    return NJ_OK;
+}
+
+nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
+                    const int32_t* draft_tokens, const float* draft_probs, int64_t ldq,
+                    const int32_t* gamma_per_req, const float* uniforms, int32_t B,
+                    int32_t* accept_len, int32_t* next_token, const nj_debug* dbg) {
+    if (!c) return NJ_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    Plan pl;
+    nj_status s = make_plan(c, gamma_per_req, B, pl);
+    if (s != NJ_OK) return s;
+    if (!hidden || !W_lm || !uniforms || !accept_len || !next_token)
+        return set_err(c, NJ_EINVAL, "NULL device pointer");
+    if (pl.G > 0 && (!draft_tokens || !draft_probs)) return set_err(c, NJ_EINVAL, "NULL draft buffers with G=%d", pl.G);
+    if (ldq < c->cfg.V || ldq % 4 != 0) return set_err(c, NJ_ESHAPE, "ldq=%lld must be >= V and a multiple of 4", (long long)ldq);
+    if ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(W_lm)) & 15)
+        return set_err(c, NJ_ESHAPE, "hidden / W_lm must be 16-byte aligned");
+    if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
+    const ReqMeta meta = make_meta(pl);
+    const int certify = c->certify || c->force_fb;
+
+    if (pl.path == NJ_PATH_FUSED) {
+        CUtensorMap tmH;
+        if (!encode_2d(&tmH, hidden, pl.N, c->cfg.d, pl.npad))
+            return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (hidden)");
+        FusedParams fp{};
+        fp.B = pl.B; fp.N = pl.N; fp.G = pl.G;
+        fp.V_local = c->V_local; fp.v_begin = c->cfg.v_begin; fp.U = c->U;
+        fp.num_kb = (c->cfg.d + kBK - 1) / kBK;
+        fp.draft_tokens = draft_tokens; fp.q = draft_probs; fp.ldq = ldq; fp.u = uniforms;
+        fp.accept_len = accept_len; fp.next_token = next_token;
+        fp.part_m = c->part_m; fp.part_s = c->part_s; fp.dl = c->dl; fp.wpart = c->wpart;
+        fp.bar_count = c->bar; fp.bar_gen = c->bar + 1;
+        fp.fb_count = c->fb_count(); fp.fb_list = c->fb_list(); fp.req_flags = c->req_flags();
+        fp.dbg_lse = dbg ? dbg->lse : nullptr; fp.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
+        fp.dbg_mass = dbg ? dbg->mass : nullptr; fp.dbg_flags = dbg ? dbg->flags : nullptr;
+        fp.certify = certify; fp.force_fallback = c->force_fb;
+        fp.eps_acc = c->eps_acc_fused; fp.eps_draw = c->eps_draw_fused;
+        for (int b = 0; b <= pl.B; ++b) fp.row_off[b] = pl.row_off[b];
+        if (pl.npad == 16) s = launch_fused<16>(c, st, pl, tmH, fp);
+        else if (pl.npad == 32) s = launch_fused<32>(c, st, pl, tmH, fp);
+        else s = launch_fused<48>(c, st, pl, tmH, fp);
+        if (s != NJ_OK) return s;
+    } else {
+        NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
+        if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
+        // K-A: stats GEMM over the draft rows (gathered contiguous), draft-logit capture
+        if (pl.G > 0) {
+            k_gather_drafts<<<pl.G, 128, 0, st>>>(hidden, c->cfg.d, meta, c->hd);
+            NJ_LAUNCHED(c, "k_gather_drafts", st);
+            for (int r0 = 0; r0 < pl.G; r0 += kMaxStatRows) {
+                const int R = std::min(kMaxStatRows, pl.G - r0);
+                GemmRowsParams gp{};
+                gp.part_m = c->part_m + (size_t)r0 * c->grid;
+                gp.part_s = c->part_s + (size_t)r0 * c->grid;
+                gp.tok = draft_tokens + r0;
+                gp.dl = c->dl + r0;
+                std::pair<cudaEvent_t, cudaEvent_t> ev;
+                if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
+                if ((s = launch_gemm_rows<false, true, true>(c, st, c->hd + (size_t)r0 * c->cfg.d, R, gp)) != NJ_OK)
+                    return s;
+                if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
+            }
+        }
+        // K-B: acceptance, first rejection, sample-row gather
+        AcceptParams ap{};
+        ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = c->grid; ap.dl = c->dl;
+        ap.draft_tokens = draft_tokens; ap.q = draft_probs; ap.ldq = ldq; ap.u = uniforms;
+        ap.hidden = hidden; ap.d = c->cfg.d; ap.hs = c->hs;
+        ap.accept_len = accept_len; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
+        ap.fb_count = c->fb_count(); ap.fb_list = c->fb_list(); ap.req_flags = c->req_flags();
+        ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
+        ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc;
+        k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
+        NJ_LAUNCHED(c, "k_accept", st);
+        // K-C: sample-row GEMM -> fp32 logits [B, V_local] + stats (bonus-row lse)
+        {
+            GemmRowsParams gp{};
+            gp.logits = c->logits_s; gp.ld_out = c->V_local;
+            gp.part_m = c->part2_m; gp.part_s = c->part2_s;
+            if ((s = launch_gemm_rows<true, true, false>(c, st, c->hs, pl.B, gp)) != NJ_OK) return s;
+        }
+        // K-D: residual / bonus masses and the inverse-CDF draw
+        MassParams mp{};
+        mp.logits = c->logits_s; mp.ld = c->V_local; mp.V_local = c->V_local; mp.v_begin = c->cfg.v_begin;
+        mp.nchunks = c->nchunks; mp.s_resid = c->s_resid; mp.s_qrow = c->s_qrow; mp.s_lse = c->s_lse;
+        mp.part2_m = c->part2_m; mp.part2_s = c->part2_s; mp.grid2 = c->grid;
+        mp.q = draft_probs; mp.ldq = ldq; mp.u = uniforms; mp.stage_mode = 0; mp.cmass = c->cmass;
+        mp.accept_len = accept_len; mp.next_token = next_token;
+        mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
+        mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
+        mp.dbg_lse = dbg ? dbg->lse : nullptr;
+        mp.certify = certify; mp.eps_draw = c->eps_draw;
+        k_mass<<<dim3(c->nchunks, pl.B), kSampThreads, 0, st>>>(mp);
+        NJ_LAUNCHED(c, "k_mass", st);
+        k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
+        NJ_LAUNCHED(c, "k_locate", st);
+    }
+    if (certify) {
+        FbParams f = fb_params(c, hidden, W_lm, draft_tokens, draft_probs, ldq, uniforms, accept_len, next_token, dbg);
+        if ((s = launch_fallback(c, st, f, meta)) != NJ_OK) return s;
+    }
+    return NJ_OK;
+}
+
+nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, const uint16_t* W_lm,
+                         const int32_t* tok_h, const float* q_h, int64_t ldq, const int32_t* gamma,
+                         const float* u_h, int32_t B, int32_t* acc_h, int32_t* next_h) {
+    if (!c) return NJ_EINVAL;
+    Plan pl;
+    nj_status s = make_plan(c, gamma, B, pl);
+    if (s != NJ_OK) return s;
+    if (!hidden_h || !u_h || !acc_h || !next_h || (pl.G > 0 && (!tok_h || !q_h)))
+        return set_err(c, NJ_EINVAL, "NULL host pointer");
+    if (ldq < c->cfg.V || ldq % 4 != 0) return set_err(c, NJ_ESHAPE, "ldq=%lld", (long long)ldq);
+    if (!c->st_hidden || c->st_ldq < ldq) {
+        if (c->st_q) { cudaFree(c->st_q); c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void*)c->st_q)); }
+        if (!c->st_hidden) {
+            if ((s = alloc(c, &c->st_hidden, (size_t)c->Nmax * c->cfg.d)) != NJ_OK) return s;
+            if ((s = alloc(c, &c->st_tok, (size_t)c->Gmax)) != NJ_OK) return s;
+            if ((s = alloc(c, &c->st_u, (size_t)c->Nmax)) != NJ_OK) return s;
+            if ((s = alloc(c, &c->st_acc, (size_t)c->cfg.max_batch)) != NJ_OK) return s;
+            if ((s = alloc(c, &c->st_next, (size_t)c->cfg.max_batch)) != NJ_OK) return s;
+        }
+        if ((s = alloc(c, &c->st_q, (size_t)c->Gmax * ldq)) != NJ_OK) return s;
+        c->st_ldq = ldq;
+    }
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    NJ_CUDA(c, cudaMemcpyAsync(c->st_hidden, hidden_h, (size_t)pl.N * c->cfg.d * 2, cudaMemcpyHostToDevice, st));
+    NJ_CUDA(c, cudaMemcpyAsync(c->st_u, u_h, (size_t)pl.N * 4, cudaMemcpyHostToDevice, st));
+    if (pl.G > 0) {
+        NJ_CUDA(c, cudaMemcpyAsync(c->st_tok, tok_h, (size_t)pl.G * 4, cudaMemcpyHostToDevice, st));
+        NJ_CUDA(c, cudaMemcpyAsync(c->st_q, q_h, (size_t)pl.G * ldq * 4, cudaMemcpyHostToDevice, st));
+    }
+    s = nj_verify(c, stream, c->st_hidden, W_lm, c->st_tok, c->st_q, ldq, gamma, c->st_u, B, c->st_acc,
+                  c->st_next, nullptr);
+    if (s != NJ_OK) return s;
+    NJ_CUDA(c, cudaMemcpyAsync(acc_h, c->st_acc, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
+    NJ_CUDA(c, cudaMemcpyAsync(next_h, c->st_next, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
+    NJ_CUDA(c, cudaStreamSynchronize(st));
+    return NJ_OK;
+}
+
+nj_status nj_lmhead_logits(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
+                           const int32_t* rows, int32_t n_rows, float* logits, int64_t ld_out) {
+    if (!c) return NJ_EINVAL;
+    if (!hidden || !W_lm || !rows || !logits) return set_err(c, NJ_EINVAL, "NULL device pointer");
+    if (n_rows < 1 || n_rows > c->Gmax) return set_err(c, NJ_ESHAPE, "n_rows=%d outside [1, %d]", n_rows, c->Gmax);
+    if (ld_out < c->V_local) return set_err(c, NJ_ESHAPE, "ld_out=%lld < V_local", (long long)ld_out);
+    nj_status s;
+    if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    k_gather_rows<<<n_rows, 128, 0, st>>>(hidden, c->cfg.d, rows, c->hd);
+    NJ_LAUNCHED(c, "k_gather_rows", st);
+    GemmRowsParams gp{};
+    gp.logits = logits;
+    gp.ld_out = ld_out;
+    return launch_gemm_rows<true, false, false>(c, st, c->hd, n_rows, gp);
+}
+
+nj_status nj_lmhead_logits_ks(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
+                              const int32_t* rows, int32_t n_rows, double* logits, int64_t ld_out, int32_t ks) {
+    if (!c) return NJ_EINVAL;
+    if (!hidden || !W_lm || !rows || !logits) return set_err(c, NJ_EINVAL, "NULL device pointer");
+    if (n_rows < 1 || n_rows > 32 || n_rows > c->Gmax) return set_err(c, NJ_ESHAPE, "n_rows=%d outside [1, 32]", n_rows);
+    if (ks < 1) return set_err(c, NJ_EINVAL, "ks=%d", ks);
+    nj_status s;
+    if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    k_gather_rows<<<n_rows, 128, 0, st>>>(hidden, c->cfg.d, rows, c->hd);
+    NJ_LAUNCHED(c, "k_gather_rows", st);
+    CUtensorMap tmH;
+    if (!encode_2d(&tmH, c->hd, n_rows, c->cfg.d, 32)) return set_err(c, NJ_ECUDA, "tensor map (H)");
+    ProbeKsParams pp{};
+    pp.R = n_rows; pp.V_local = c->V_local; pp.U = c->U; pp.num_kb = (c->cfg.d + kBK - 1) / kBK;
+    pp.nstages = 8; pp.ks = ks; pp.logits = logits; pp.ld_out = ld_out;
+    const size_t smem = (size_t)8 * (kTileBytesA + 32 * 128) + (2 * 8 + 2 * kProbeBufs) * 8 + 16;
+    static bool attr = false;
+    if (!attr) { NJ_CUDA(c, set_smem_attr(k_probe_ks)); attr = true; }
+    k_probe_ks<<<c->grid, kThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, pp);
+    NJ_LAUNCHED(c, "k_probe_ks", st);
+    return NJ_OK;
+}
+
+nj_status nj_stream_test(nj_ctx* c, void* stream, const uint16_t* W, int32_t mode, int32_t group, int32_t nstages,
+                         const uint16_t* H, int32_t hrows) {
+    if (!c || !W) return NJ_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    StreamTestParams sp{};
+    sp.V_local = c->V_local; sp.U = c->U; sp.num_kb = (c->cfg.d + kBK - 1) / kBK; sp.nstages = nstages;
+    sp.mode = mode; sp.group = group; sp.ntiles_total = c->V_local / kTileV;
+    CUtensorMap m128, m16;
+    if (mode == 2) {
+        if (!encode_2d(&m128, W, (int64_t)sp.ntiles_total * sp.num_kb * kTileV, kBK, 128)) return set_err(c, NJ_ECUDA, "map");
+        m16 = m128;
+    } else {
+        if (!encode_2d(&m128, W, c->V_local, c->cfg.d, 128) || !encode_2d(&m16, W, c->V_local, c->cfg.d, 16))
+            return set_err(c, NJ_ECUDA, "map");
+    }
+    sp.hrows = H ? hrows : 0;
+    CUtensorMap mh = m128;
+    if (H && !encode_2d(&mh, H, hrows, c->cfg.d, hrows)) return set_err(c, NJ_ECUDA, "map H");
+    const size_t smem = (size_t)nstages * group * (kTileBytesA + sp.hrows * 128) + 2 * nstages * 8 + 16;
+    if (smem > (size_t)kSmemLimit) return set_err(c, NJ_ESHAPE, "smem %zu", smem);
+    NJ_CUDA(c, set_smem_attr(k_stream_test));
+    k_stream_test<<<c->grid, 128, smem, st>>>(m128, m16, mh, sp);
+    NJ_LAUNCHED(c, "k_stream_test", st);
+    return NJ_OK;
+}
+
+nj_status nj_sample_from_logits(nj_ctx* c, void* stream, const float* logits, int64_t ld_l, const int32_t* residual,
+                                const float* q, int64_t ldq, const float* u, int32_t B, int32_t* next_token,
+                                double* mass) {
+    if (!c) return NJ_EINVAL;
+    if (!logits || !residual || !q || !u || !next_token) return set_err(c, NJ_EINVAL, "NULL device pointer");
+    if (B < 1 || B > c->cfg.max_batch) return set_err(c, NJ_ESHAPE, "B=%d", B);
+    if (c->V_local != c->cfg.V) return set_err(c, NJ_EUNSUPPORTED, "stage export is unsharded only");
+    if (ld_l < c->V_local || ldq < c->V_local) return set_err(c, NJ_ESHAPE, "pitch < V");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
+    k_row_lse<<<B, 256, 0, st>>>(logits, ld_l, c->V_local, c->lse_tmp);
+    NJ_LAUNCHED(c, "k_row_lse", st);
+    k_iota<<<(B + 255) / 256, 256, 0, st>>>(c->scratch_i, B);
+    NJ_LAUNCHED(c, "k_iota", st);
+    MassParams mp{};
+    mp.logits = logits; mp.ld = ld_l; mp.V_local = c->V_local; mp.v_begin = 0; mp.nchunks = c->nchunks;
+    mp.s_resid = residual; mp.s_qrow = c->scratch_i; mp.s_lse = c->lse_tmp;
+    mp.q = q; mp.ldq = ldq; mp.u = u; mp.stage_mode = 1; mp.cmass = c->cmass;
+    mp.next_token = next_token;
+    mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
+    mp.dbg_mass = mass;
+    mp.certify = c->certify; mp.eps_draw = 4e-6f;
+    ReqMeta meta;
+    meta.B = B;
+    k_mass<<<dim3(c->nchunks, B), kSampThreads, 0, st>>>(mp);
+    NJ_LAUNCHED(c, "k_mass", st);
+    k_locate<<<B, kSampThreads, 0, st>>>(mp, meta);
+    NJ_LAUNCHED(c, "k_locate", st);
+    if (c->certify) {
+        FbParams f{};
+        f.V_local = c->V_local;
+        f.fb_count = c->fb_count(); f.fb_list = c->fb_list(); f.req_flags = c->req_flags();
+        f.q = q; f.ldq = ldq; f.u = u; f.next_token = next_token; f.dbg_mass = mass;
+        f.st_logits = logits; f.st_ld = ld_l; f.st_resid = residual; f.stage_mode = 1;
+        k_fb_decide<<<std::min(B, c->num_sms), 256, 0, st>>>(f, meta);
+        NJ_LAUNCHED(c, "k_fb_decide", st);
+    }
+    return NJ_OK;
+}
+
+}  // extern "C"

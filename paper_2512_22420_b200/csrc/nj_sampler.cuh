@@ -1,0 +1,584 @@
+// nj_sampler.cuh — acceptance / residual-resampling kernels of the two-pass
+// path, and the fp64 certified fallback shared by both paths.
+//
+// BJ step (3) (Leviathan): accept draft i iff u_i q_i(x_i) <
+// p_i(x_i) (R2), first rejection n, resample from norm(max(0, p_n - q_n)),
+// bonus from p_gamma on full acceptance, inverse CDF in ascending token id (R5).
+//
+// Sampler arithmetic is bandwidth-bound: rows are streamed with coalesced
+// loads (consecutive threads = consecutive vocab ids), masses are built from
+// warp inclusive scans with fp64 cross-warp / cross-chunk prefixes, and the
+// located token's interval boundaries are taken from the SAME fp32 scan values
+// (E(x) = I(x-1)) so the intervals tile [0, W) exactly.
+#pragma once
+#include "nj_gemm.cuh"
+
+namespace nj {
+
+struct ReqMeta {
+    int32_t B;
+    int32_t row_off[kMaxB + 1];
+};
+
+__device__ __forceinline__ int req_of_row(const ReqMeta& m, int j) {
+    int lo = 0, hi = m.B - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (m.row_off[mid] <= j) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+__device__ __forceinline__ int req_of_draft(const ReqMeta& m, int g) {   // draft_off[b] = row_off[b] - b
+    int lo = 0, hi = m.B - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (m.row_off[mid] - mid <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// copy one bf16 row of d elements (d % 8 == 0) with 16-B vector loads
+__device__ __forceinline__ void copy_row(uint16_t* dst, const uint16_t* src, int d, int t, int nt) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int i = t; i < d / 8; i += nt) d4[i] = __ldg(&s4[i]);
+}
+
+// gather the draft rows of hidden into a contiguous [G, d] buffer (block per row)
+__global__ void k_gather_drafts(const uint16_t* __restrict__ hidden, int d, const ReqMeta m,
+                                uint16_t* __restrict__ out) {
+    const int g = blockIdx.x;
+    const int b = req_of_draft(m, g);
+    const int row = m.row_off[b] + (g - (m.row_off[b] - b));
+    copy_row(out + (int64_t)g * d, hidden + (int64_t)row * d, d, threadIdx.x, blockDim.x);
+}
+
+// gather rows by a device row list (test-only GEMM probe)
+__global__ void k_gather_rows(const uint16_t* __restrict__ hidden, int d, const int32_t* __restrict__ rows,
+                              uint16_t* __restrict__ out) {
+    copy_row(out + (int64_t)blockIdx.x * d, hidden + (int64_t)rows[blockIdx.x] * d, d, threadIdx.x, blockDim.x);
+}
+
+__global__ void k_iota(int32_t* out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = i;
+}
+
+// lse of row j from per-CTA partials (warp-cooperative, fixed order)
+__device__ __forceinline__ double warp_lse(const float* pm, const float* ps, int ld, int j, int grid) {
+    const int lane = (int)lane_id();
+    float mx = -INFINITY;
+    for (int c = lane; c < grid; c += 32) mx = fmaxf(mx, __ldcg(&pm[(int64_t)j * ld + c]));
+    mx = warp_max(mx);
+    double sacc = 0.0;
+    for (int c = lane; c < grid; c += 32) {
+        const float mc = __ldcg(&pm[(int64_t)j * ld + c]);
+        const float sc = __ldcg(&ps[(int64_t)j * ld + c]);
+        if (mc != -INFINITY) sacc += (double)sc * (double)__expf(mc - mx);
+    }
+    sacc = warp_sum_d(sacc);
+    return (double)mx + log(sacc);
+}
+
+struct AcceptParams {
+    const float* part_m;   // [G][grid] stats of draft rows (K-A)
+    const float* part_s;
+    int32_t grid;
+    const double* dl;      // [G] draft logits
+    const int32_t* draft_tokens;
+    const float* q;
+    int64_t ldq;
+    const float* u;
+    const uint16_t* hidden;
+    int32_t d;
+    uint16_t* hs;          // [B, d] gathered sample rows
+    int32_t* accept_len;
+    int32_t* s_resid;      // [B]
+    int32_t* s_qrow;       // [B]
+    double* s_lse;         // [B] lse of the sample row if residual (else NaN)
+    int32_t* fb_count;
+    int32_t* fb_list;
+    int32_t* req_flags;
+    float* dbg_lse;
+    float* dbg_pdraft;
+    int32_t certify, force_fallback;
+    float eps_acc;
+};
+
+// K-B: warp per request — lse of its draft rows, acceptance tests, first
+// rejection, sample-row bookkeeping, and the copy of the sample hidden row.
+__global__ void k_accept(const AcceptParams p, const ReqMeta m) {
+    const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
+    if (b >= m.B) return;
+    const int lane = (int)lane_id();
+    const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
+    int n = gam, flag = 0;
+    double lse_n = __longlong_as_double(0x7ff8000000000000ll);
+    for (int i = 0; i < gam; ++i) {
+        const int g = g0 + i;
+        const double lse = warp_lse(p.part_m, p.part_s, p.grid, g, p.grid);
+        const double pd = exp(__ldcg(&p.dl[g]) - lse);
+        const double qx = (double)p.q[(int64_t)g * p.ldq + p.draft_tokens[g]];
+        const double uq = (double)p.u[ro + i] * qx;
+        if (lane == 0) {
+            if (p.dbg_lse) p.dbg_lse[ro + i] = (float)lse;
+            if (p.dbg_pdraft) p.dbg_pdraft[g] = (float)pd;
+        }
+        if (fabs(uq - pd) <= (double)p.eps_acc * pd) flag = 1;
+        if (!(uq < pd)) { n = i; lse_n = lse; break; }
+    }
+    // remaining drafts (untested) still get debug values
+    for (int i = n + 1; i < gam && p.dbg_pdraft; ++i) {
+        const int g = g0 + i;
+        const double lse = warp_lse(p.part_m, p.part_s, p.grid, g, p.grid);
+        if (lane == 0) {
+            if (p.dbg_lse) p.dbg_lse[ro + i] = (float)lse;
+            p.dbg_pdraft[g] = (float)exp(__ldcg(&p.dl[g]) - lse);
+        }
+    }
+    copy_row(p.hs + (int64_t)b * p.d, p.hidden + (int64_t)(ro + n) * p.d, p.d, lane, 32);
+    if (lane == 0) {
+        p.accept_len[b] = n;
+        p.s_resid[b] = n < gam;
+        p.s_qrow[b] = g0 + n;
+        p.s_lse[b] = lse_n;
+        if (p.certify && (flag || p.force_fallback)) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
+    }
+}
+
+// lse of each request's logits row [B, ld] (stage-isolated sampler), fp64 merge
+__global__ void k_row_lse(const float* __restrict__ logits, int64_t ld, int V, double* __restrict__ lse) {
+    const int b = blockIdx.x;
+    const float* row = logits + (int64_t)b * ld;
+    float m = -INFINITY, s = 0.f;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+        const float v = row[x];
+        const float d = v - m;
+        const float e = __expf(-fabsf(d));
+        if (d <= 0.f) s += e; else { s = s * e + 1.f; m = v; }
+    }
+    warp_ms_merge(m, s);
+    __shared__ float2 red[32];
+    if (lane_id() == 0) red[warp_id()] = make_float2(m, s);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float M = -INFINITY;
+        for (int w = 0; w < (int)(blockDim.x / 32); ++w) M = fmaxf(M, red[w].x);
+        double S = 0.0;
+        for (int w = 0; w < (int)(blockDim.x / 32); ++w)
+            if (red[w].x != -INFINITY) S += (double)red[w].y * (double)__expf(red[w].x - M);
+        lse[b] = (double)M + log(S);
+    }
+}
+
+constexpr int kSampThreads = 256;
+constexpr int kSubTiles = 16;                         // chunk = 16 sub-tiles of 256
+constexpr int kChunk = kSampThreads * kSubTiles;      // 4096 vocab ids per chunk
+
+struct MassParams {
+    const float* logits;   // [B][ld] local vocab
+    int64_t ld;
+    int32_t V_local, v_begin, nchunks;
+    const int32_t* s_resid;
+    const int32_t* s_qrow;
+    const double* s_lse;   // residual rows: lse from K-B; NaN -> merge part2 (bonus rows)
+    const float* part2_m;  // [B][grid2] (K-C stats)
+    const float* part2_s;
+    int32_t grid2;
+    const float* q;
+    int64_t ldq;
+    const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
+    int32_t stage_mode;    // 1: u indexed by b
+    double* cmass;         // [B][nchunks]
+    int32_t* accept_len;
+    int32_t* next_token;
+    int32_t* fb_count;
+    int32_t* fb_list;
+    int32_t* req_flags;
+    double* dbg_mass;
+    int32_t* dbg_flags;
+    float* dbg_lse;
+    int32_t certify;
+    float eps_draw;
+};
+
+__device__ __forceinline__ double sample_lse(const MassParams& p, int b) {
+    __shared__ double s_l;
+    double l = p.s_lse[b];
+    if (isnan(l)) {
+        if (warp_id() == 0) {
+            const double v = warp_lse(p.part2_m, p.part2_s, p.grid2, b, p.grid2);
+            if (lane_id() == 0) s_l = v;
+        }
+        __syncthreads();
+        l = s_l;
+    }
+    return l;
+}
+
+// weights of sub-tile s of chunk c for this thread (one element per thread)
+__device__ __forceinline__ float chunk_weight(const MassParams& p, int b, int c, int s, float lsef, bool resid,
+                                              const float* qrow) {
+    const int x = c * kChunk + s * kSampThreads + (int)threadIdx.x;
+    if (x >= p.V_local) return 0.f;
+    const float pe = __expf(__ldcg(&p.logits[(int64_t)b * p.ld + x]) - lsef);
+    return resid ? fmaxf(pe - __ldg(&qrow[x]), 0.f) : pe;
+}
+
+// sub-tile total in fixed order: warp inclusive scans (fp32), warps summed
+// left-associatively in fp64.  wt[8] gets the warp totals.
+__device__ __forceinline__ void subtile_scan(float w, float& inc, float* wt_sh) {
+    inc = warp_incl_scan(w);
+    if (lane_id() == 31) wt_sh[warp_id()] = inc;
+}
+
+// K-D1: grid (nchunks, B).  Chunk masses.
+__global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p) {
+    const int c = blockIdx.x, b = blockIdx.y;
+    const double lse = sample_lse(p, b);
+    const float lsef = (float)lse;
+    const bool resid = p.s_resid[b] != 0;
+    const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
+    __shared__ float wt[kSubTiles][8];
+    float w[kSubTiles];
+#pragma unroll
+    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, b, c, s, lsef, resid, qrow);
+#pragma unroll
+    for (int s = 0; s < kSubTiles; ++s) {
+        float inc;
+        subtile_scan(w[s], inc, wt[s]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        for (int s = 0; s < kSubTiles; ++s) {
+            double st = 0.0;
+            for (int k = 0; k < 8; ++k) st = st + (double)wt[s][k];
+            acc = acc + st;
+        }
+        p.cmass[(int64_t)b * p.nchunks + c] = acc;
+    }
+}
+
+// K-D2: block per request.  Locate chunk -> sub-tile -> token.
+__global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, const ReqMeta m) {
+    const int b = blockIdx.x;
+    const double lse = sample_lse(p, b);
+    const float lsef = (float)lse;
+    const bool resid = p.s_resid[b] != 0;
+    const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
+    __shared__ double sh[4];
+    __shared__ int shi[4];
+    __shared__ float wt[kSubTiles][8];
+    const int gam = p.stage_mode ? 0 : m.row_off[b + 1] - m.row_off[b] - 1;
+    const float uf = p.stage_mode ? p.u[b] : p.u[m.row_off[b] + gam];
+    if (threadIdx.x == 0) {
+        double P = 0.0, Pc = 0.0;
+        int csel = -1, lastpos = -1;
+        double W = 0.0;
+        for (int c = 0; c < p.nchunks; ++c) W = W + p.cmass[(int64_t)b * p.nchunks + c];
+        const double T = (double)uf * W;
+        for (int c = 0; c < p.nchunks; ++c) {
+            const double wc = p.cmass[(int64_t)b * p.nchunks + c];
+            if (wc > 0.0) lastpos = c;
+            if (csel < 0 && T < P + wc) { csel = c; Pc = P; }
+            P = P + wc;
+        }
+        int clamp = 0;
+        if (!(W > 0.0)) clamp = 2;                         // zero mass (R6) -> fallback
+        else if (csel < 0) { clamp = 1; csel = lastpos; Pc = 0.0; }
+        sh[0] = T - Pc;
+        sh[1] = W;
+        shi[0] = csel;
+        shi[1] = clamp;
+        if (!p.stage_mode && p.dbg_lse && !resid) p.dbg_lse[m.row_off[b] + gam] = (float)lse;
+    }
+    __syncthreads();
+    const int clamp = shi[1];
+    if (clamp == 2) {
+        if (threadIdx.x == 0) {
+            p.next_token[b] = 0;
+            if (p.dbg_mass) p.dbg_mass[b] = 0.0;
+            if (p.dbg_flags) p.dbg_flags[b] = 2;
+            if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 2);
+        }
+        return;
+    }
+    const int c = shi[0];
+    const double tp = sh[0];
+    float w[kSubTiles], inc[kSubTiles];
+#pragma unroll
+    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, b, c, s, lsef, resid, qrow);
+#pragma unroll
+    for (int s = 0; s < kSubTiles; ++s) subtile_scan(w[s], inc[s], wt[s]);
+    __syncthreads();
+    __shared__ double spre[kSubTiles + 1];
+    __shared__ int ssel;
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        int sel = -1, lastpos = -1;
+        for (int s = 0; s < kSubTiles; ++s) {
+            spre[s] = acc;
+            double st = 0.0;
+            for (int k = 0; k < 8; ++k) st = st + (double)wt[s][k];
+            if (st > 0.0) lastpos = s;
+            acc = acc + st;
+            if (sel < 0 && tp < acc) sel = s;
+        }
+        spre[kSubTiles] = acc;
+        if (clamp || sel < 0) sel = -1 - lastpos;          // clamp marker
+        ssel = sel;
+    }
+    __syncthreads();
+    int s = ssel;
+    const bool clamped = s < 0;
+    if (clamped) s = -1 - s;
+    float ws = 0.f, is = 0.f;
+#pragma unroll
+    for (int k = 0; k < kSubTiles; ++k)
+        if (k == s) { ws = w[k]; is = inc[k]; }
+    float ex = __shfl_up_sync(0xffffffffu, is, 1);
+    if (lane_id() == 0) ex = 0.f;
+    double Sq = 0.0;
+    for (int k = 0; k < (int)warp_id(); ++k) Sq = Sq + (double)wt[s][k];
+    const double lo = spre[s] + (Sq + (double)ex);
+    const double hi = spre[s] + (Sq + (double)is);
+    const int x = c * kChunk + s * kSampThreads + (int)threadIdx.x;
+    if (clamped) {
+        const unsigned mpos = __ballot_sync(0xffffffffu, ws > 0.f);
+        __shared__ int wpick[8];
+        if (lane_id() == 0) wpick[warp_id()] = mpos ? (31 - __clz((int)mpos)) : -1;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int pick = -1;
+            for (int k = 7; k >= 0 && pick < 0; --k)
+                if (wpick[k] >= 0) pick = k * 32 + wpick[k];
+            p.next_token[b] = c * kChunk + s * kSampThreads + (pick < 0 ? 0 : pick) + p.v_begin;
+            if (p.dbg_mass) p.dbg_mass[b] = sh[1];
+            if (p.dbg_flags) p.dbg_flags[b] = 4;
+            if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 4);
+        }
+        return;
+    }
+    if (ws > 0.f && lo <= tp && tp < hi) {
+        p.next_token[b] = x + p.v_begin;
+        if (p.dbg_mass) p.dbg_mass[b] = sh[1];
+        if (p.dbg_flags) p.dbg_flags[b] = 0;
+        const double margin = fmin(tp - lo, hi - tp);
+        if (p.certify && margin <= (double)p.eps_draw) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Certified fallback (fp64 on CUDA cores): every queued request is recomputed
+// from the bf16 inputs with fp64 accumulation -- the plain definition of
+// include/nj.h -- and its outputs overwritten.  Launched unconditionally; an
+// empty queue costs one tiny launch each.
+// ---------------------------------------------------------------------------
+struct FbParams {
+    const uint16_t* hidden;
+    const uint16_t* W;
+    int32_t d, V_local, v_begin;
+    const int32_t* fb_count;
+    const int32_t* fb_list;
+    int32_t* req_flags;
+    double* fb_logits;     // [N][V_local] (row index = packed row of the request)
+    const int32_t* draft_tokens;
+    const float* q;
+    int64_t ldq;
+    const float* u;
+    int32_t* accept_len;
+    int32_t* next_token;
+    double* dbg_mass;
+    int32_t* dbg_flags;
+    // stage mode (nj_sample_from_logits): one fp32 logits row per request
+    const float* st_logits;
+    int64_t st_ld;
+    const int32_t* st_resid;
+    int32_t stage_mode;
+};
+
+__device__ __forceinline__ float bf16f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
+
+// FB-A: fp64 logits of every row of every queued request (warp per vocab id).
+__global__ void __launch_bounds__(256) k_fb_logits(const FbParams p, const ReqMeta m) {
+    const int nfb = __ldcg(p.fb_count);
+    if (nfb == 0) return;
+    const int lane = (int)lane_id();
+    const int gw = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
+    const int nw = gridDim.x * (blockDim.x / 32);
+    const int nvec = p.d / 8;
+    for (int x = gw; x < p.V_local; x += nw) {
+        const uint4* wr = reinterpret_cast<const uint4*>(p.W + (int64_t)x * p.d);
+        for (int k = 0; k < nfb; ++k) {
+            const int b = __ldcg(&p.fb_list[k]);
+            for (int j = m.row_off[b]; j < m.row_off[b + 1]; ++j) {
+                const uint4* hr = reinterpret_cast<const uint4*>(p.hidden + (int64_t)j * p.d);
+                double acc = 0.0;
+                for (int i = lane; i < nvec; i += 32) {
+                    const uint4 wv = __ldg(&wr[i]);
+                    const uint4 hv = __ldg(&hr[i]);
+                    const uint16_t* w16 = reinterpret_cast<const uint16_t*>(&wv);
+                    const uint16_t* h16 = reinterpret_cast<const uint16_t*>(&hv);
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) acc = fma((double)bf16f(w16[e]), (double)bf16f(h16[e]), acc);
+                }
+                acc = warp_sum_d(acc);
+                if (lane == 0) p.fb_logits[(int64_t)j * p.V_local + x] = acc;
+            }
+        }
+    }
+}
+
+template <typename T>
+__device__ double block_max_d(T v, double* sh) {
+    double x = (double)v;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane_id() == 0) sh[warp_id()] = x;
+    __syncthreads();
+    double r = -INFINITY;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) r = fmax(r, sh[w]);
+    __syncthreads();
+    return r;
+}
+__device__ double block_sum_d(double v, double* sh) {
+    v = warp_sum_d(v);
+    if (lane_id() == 0) sh[warp_id()] = v;
+    __syncthreads();
+    double r = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) r = r + sh[w];
+    __syncthreads();
+    return r;
+}
+
+template <typename LT>
+__device__ double row_lse_d(const LT* row, int V, double* sh) {
+    double mx = -INFINITY;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) mx = fmax(mx, (double)row[x]);
+    mx = block_max_d(mx, sh);
+    double s = 0.0;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) s += exp((double)row[x] - mx);
+    s = block_sum_d(s, sh);
+    return mx + log(s);
+}
+
+// FB-B: block per queued request.  fp64 lse, acceptance, residual / bonus,
+// inverse CDF (block scan, ascending id) -- the plain definition.
+__global__ void __launch_bounds__(256) k_fb_decide(const FbParams p, const ReqMeta m) {
+    const int nfb = __ldcg(p.fb_count);
+    __shared__ double sh[32];
+    __shared__ double lse[32];
+    __shared__ int sn, st;
+    __shared__ double sbase;
+    const int V = p.V_local;
+    for (int k = blockIdx.x; k < nfb; k += gridDim.x) {
+        const int b = __ldcg(&p.fb_list[k]);
+        int gam, ro;
+        const double* L = nullptr;
+        const float* Ls = nullptr;
+        if (p.stage_mode) {
+            gam = 0; ro = b;
+            Ls = p.st_logits + (int64_t)b * p.st_ld;
+            const double l = row_lse_d(Ls, V, sh);
+            if (threadIdx.x == 0) { lse[0] = l; sn = p.st_resid[b] ? -1 : 0; }
+        } else {
+            ro = m.row_off[b];
+            gam = m.row_off[b + 1] - ro - 1;
+            L = p.fb_logits + (int64_t)ro * V;
+            for (int j = 0; j <= gam; ++j) {
+                const double l = row_lse_d(L + (int64_t)j * V, V, sh);
+                if (threadIdx.x == 0) lse[j] = l;
+            }
+            if (threadIdx.x == 0) {
+                const int g0 = ro - b;
+                int n = gam;
+                for (int i = 0; i < gam; ++i) {
+                    const int x = p.draft_tokens[g0 + i] - p.v_begin;
+                    const double pd = exp(L[(int64_t)i * V + x] - lse[i]);
+                    const double qx = (double)p.q[(int64_t)(g0 + i) * p.ldq + p.draft_tokens[g0 + i]];
+                    if (!((double)p.u[ro + i] * qx < pd)) { n = i; break; }
+                }
+                sn = n;
+            }
+        }
+        __syncthreads();
+        int n = sn;
+        bool resid;
+        const float* qrow;
+        if (p.stage_mode) {
+            resid = (n < 0);
+            n = 0;
+            qrow = p.q + (int64_t)b * p.ldq + p.v_begin;
+        } else {
+            resid = n < gam;
+            qrow = p.q + (int64_t)(ro - b + n) * p.ldq + p.v_begin;
+        }
+        const double ln = lse[n];
+        auto logit = [&](int x) -> double {
+            return p.stage_mode ? (double)Ls[x] : L[(int64_t)n * V + x];
+        };
+        auto weight = [&](int x, bool res) -> double {
+            const double pe = exp(logit(x) - ln);
+            if (!res) return pe;
+            const double d = pe - (double)qrow[x];
+            return d > 0.0 ? d : 0.0;
+        };
+        double Wl = 0.0;
+        for (int x = threadIdx.x; x < V; x += blockDim.x) Wl += weight(x, resid);
+        double W = block_sum_d(Wl, sh);
+        int zero = 0;
+        if (W == 0.0) {   // R6
+            zero = 2;
+            resid = false;
+            Wl = 0.0;
+            for (int x = threadIdx.x; x < V; x += blockDim.x) Wl += weight(x, false);
+            W = block_sum_d(Wl, sh);
+        }
+        const float uf = p.stage_mode ? p.u[b] : p.u[ro + gam];
+        const double T = (double)uf * W;
+        if (threadIdx.x == 0) { sbase = 0.0; st = 0x7fffffff; }
+        __syncthreads();
+        for (int x0 = 0; x0 < V; x0 += blockDim.x) {
+            const int x = x0 + threadIdx.x;
+            const double w = x < V ? weight(x, resid) : 0.0;
+            const double inc = warp_incl_scan_d(w);
+            double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+            if (lane_id() == 0) exc = 0.0;
+            if (lane_id() == 31) sh[warp_id()] = inc;
+            __syncthreads();
+            double off = sbase;
+            for (int k2 = 0; k2 < (int)warp_id(); ++k2) off += sh[k2];
+            const double hi = off + inc;
+            const double lo = off + exc;
+            double tot = sbase;
+            for (int k2 = 0; k2 < (int)(blockDim.x / 32); ++k2) tot += sh[k2];
+            __syncthreads();
+            if (w > 0.0 && lo <= T && T < hi) atomicMin(&st, x);   // first crossing (ties: smallest id)
+            if (threadIdx.x == 0) sbase = tot;
+            __syncthreads();
+            if (st != 0x7fffffff) break;
+        }
+        int clampf = 0;
+        if (st == 0x7fffffff) {   // overshoot (R5): last positive weight
+            clampf = 4;
+            if (threadIdx.x == 0) {
+                int last = 0;
+                for (int x = V - 1; x >= 0; --x)
+                    if (weight(x, resid) > 0.0) { last = x; break; }
+                st = last;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            if (!p.stage_mode) p.accept_len[b] = n;
+            p.next_token[b] = st + p.v_begin;
+            if (p.dbg_mass) p.dbg_mass[b] = W;
+            if (p.dbg_flags) p.dbg_flags[b] = 1 | zero | clampf;
+            p.req_flags[b] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace nj

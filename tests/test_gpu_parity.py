@@ -1,0 +1,230 @@
+"""GPU parity: libnj (CUDA, sm_100a, through the C ABI) vs the fp64 oracle on
+identical seeded inputs.
+
+Bar (BASELINE.json north_star; R11/R12):
+  * accept_len / next_token bit-exact, except requests whose oracle margin
+    |a_i - u_i| or |F - u| is <= 1e-6 (counted, reported, excused);
+  * probabilities: |ln p_gpu - ln p_oracle| <= 2e-3 (bf16 GEMM inputs), and the
+    tighter regression bound this build actually meets;
+  * sampler stage on given fp32 logits: W_b within 1e-5 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import bruteforce
+from paper_2512_22420_b200 import (NJ_FLAG_FALLBACK, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PATH,
+                                   NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_TWOPASS, NJError, Verifier)
+from synth.inputs import dyadic_rows, make_batch, make_sampler_case, make_weight
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
+QV, QD = 152064, 3584
+_W = {}
+
+
+def w_full():
+    if "W" not in _W:
+        _W["W"] = make_weight(QV, QD, 0, DEV)
+    return _W["W"]
+
+
+def run(b, path=NJ_PATH_AUTO, certify=True, force_fb=False, max_batch=None, gamma_max=5):
+    B = b.B
+    v = Verifier(b.hidden.shape[1], b.W.shape[0], max_batch=max_batch or B, gamma_max=gamma_max)
+    v.set_option(NJ_OPT_PATH, path)
+    v.set_option(NJ_OPT_CERTIFY, int(certify))
+    v.set_option(NJ_OPT_FORCE_FALLBACK, int(force_fb))
+    acc = torch.full((B,), -7, dtype=torch.int32, device=DEV)
+    nxt = torch.full((B,), -7, dtype=torch.int32, device=DEV)
+    dd = {"lse": torch.full((b.N,), float("nan"), device=DEV), "p_draft": torch.zeros(max(b.G, 1), device=DEV),
+          "mass": torch.zeros(B, dtype=torch.float64, device=DEV), "flags": torch.zeros(B, dtype=torch.int32, device=DEV)}
+    v.verify(b.hidden, b.W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt, debug=dd)
+    torch.cuda.synchronize()
+    return acc.cpu().numpy(), nxt.cpu().numpy(), {k: t.cpu().numpy() for k, t in dd.items()}, v
+
+
+def check(b, acc, nxt, dd, lnp_tol=2e-3, lse_tol=None):
+    n = b.to_numpy()
+    r = oracle.verify(n["hidden_bits"], n["W_bits"], n["draft_tokens"], n["draft_probs"], n["gamma"], n["uniforms"])
+    ok = ~r["tie"]
+    bad_a = np.nonzero((acc != r["accept_len"]) & ok)[0]
+    bad_t = np.nonzero((nxt != r["next_token"]) & ok)[0]
+    assert bad_a.size == 0, (bad_a, acc[bad_a], r["accept_len"][bad_a])
+    assert bad_t.size == 0, (bad_t, nxt[bad_t], r["next_token"][bad_t])
+    assert ((acc >= 0) & (acc <= n["gamma"])).all()
+    if b.G:
+        m = r["p_draft"] > 1e-20
+        lnp = np.abs(np.log(np.maximum(dd["p_draft"][:b.G][m], 1e-38)) - np.log(r["p_draft"][m]))
+        assert lnp.max(initial=0) <= lnp_tol
+    if lse_tol is not None:
+        fin = np.isfinite(dd["lse"])
+        assert np.abs(dd["lse"][fin] - r["lse"][fin]).max(initial=0) <= lse_tol
+    return int(r["tie"].sum())
+
+
+# ----------------------------------------------------------------- GEMM probe
+@pytest.mark.parametrize("V,d,R", [(1024, 128, 20), (1000, 64, 37), (QV, QD, 32)])
+def test_lmhead_probe_vs_fp64(V, d, R):
+    W = w_full() if V == QV else make_weight(V, d, 1, DEV)
+    h = (torch.randn(R, d, device=DEV) * 1.2).to(torch.bfloat16)
+    v = Verifier(d, V, max_batch=R, gamma_max=1)
+    out = torch.full((R, V), float("nan"), device=DEV)
+    v.lmhead_logits(h, W, torch.arange(R, dtype=torch.int32, device=DEV), out)
+    torch.cuda.synchronize()
+    ref = h.double() @ W.double().t()
+    assert not torch.isnan(out).any()
+    assert float((out.double() - ref).abs().max()) < 2e-4          # plain tcgen05 fp32 accumulation
+
+
+def test_accuracy_probe_restarted_accumulator():
+    """ks = 4 (accumulator restarted every k-block, fp64 partial sums) is the
+    fused path's scheme: logit error <= 2e-6 at the Qwen shape."""
+    W = w_full()
+    b = make_batch(8, 3, V=QV, d=QD, seed=11, device=DEV, W=W)
+    v = Verifier(QD, QV, max_batch=64, gamma_max=5)
+    L = torch.empty(b.N, QV, dtype=torch.float64, device=DEV)
+    v.lmhead_logits_ks(b.hidden, W, torch.arange(b.N, dtype=torch.int32, device=DEV), L, 4)
+    torch.cuda.synchronize()
+    ref = b.hidden.double() @ W.double().t()
+    assert float((L - ref).abs().max()) < 2e-6
+
+
+# ----------------------------------------------------------------- fused path
+@pytest.mark.parametrize("seed", range(12))
+def test_fused_toy_c1(seed):
+    b = make_batch(1, 3, V=32, d=16, seed=seed, device=DEV)
+    acc, nxt, dd, _ = run(b, NJ_PATH_FUSED)
+    check(b, acc, nxt, dd, lnp_tol=1e-5, lse_tol=1e-5)
+
+
+def test_fused_c2_full_size():
+    W = w_full()
+    ties = 0
+    for seed in range(4):
+        b = make_batch(8, 3, V=QV, d=QD, seed=100 + seed, device=DEV, W=W)
+        acc, nxt, dd, _ = run(b)
+        ties += check(b, acc, nxt, dd, lnp_tol=1e-5, lse_tol=5e-6)
+
+
+@pytest.mark.parametrize("B,g", [(8, "mixed:5"), (1, 0), (48, 0), (16, 2), (12, 3), (6, 5), (24, 1)])
+def test_fused_shapes_full_size(B, g):
+    b = make_batch(B, g, V=QV, d=QD, seed=B * 7 + 3, device=DEV, W=w_full())
+    if b.N > 48:
+        pytest.skip("fused path is N <= 48")
+    acc, nxt, dd, v = run(b, NJ_PATH_FUSED)
+    check(b, acc, nxt, dd, lnp_tol=1e-5, lse_tol=5e-6)
+
+
+@pytest.mark.parametrize("V,d", [(1000, 64), (4096, 256), (777, 40), (16, 8)])
+def test_fused_ragged_vocab(V, d):
+    for seed in range(3):
+        b = make_batch(5, "mixed:4", V=V, d=d, seed=seed, device=DEV, q_vocab=max(1, V - 7))
+        if b.N > 48:
+            continue
+        acc, nxt, dd, _ = run(b, NJ_PATH_FUSED)
+        check(b, acc, nxt, dd)
+
+
+def test_gpu_bruteforce_losslessness():
+    """BJ: losslessness by brute force on V <= 8 -- every cell midpoint of the
+    exact enumeration evaluated by the GPU fused path must reproduce the
+    closed-form cell label (so the GPU's emitted law equals the target law)."""
+    for V, g, seed in [(8, 3, 1), (6, 2, 2), (5, 1, 3)]:
+        b = make_batch(1, g, V=V, d=16, seed=seed)
+        n = b.to_numpy()
+        q = dyadic_rows(n["draft_probs"])
+
+        def gpu_impl(H, Wb, x, Q, gam, u):
+            out_n, out_t = [], []
+            Bt = len(gam)
+            step = max(1, 48 // (g + 1))
+            for s in range(0, Bt, step):
+                e = min(Bt, s + step)
+                r0, r1 = s * (g + 1), e * (g + 1)
+                hb = torch.from_numpy(H[r0:r1].view(np.int16)).view(torch.bfloat16).to(DEV)
+                Wt = torch.from_numpy(np.ascontiguousarray(Wb).view(np.int16)).view(torch.bfloat16).to(DEV)
+                bb = type(b)(hb, Wt, torch.from_numpy(x[s * g:e * g]).to(DEV),
+                             torch.from_numpy(np.ascontiguousarray(Q[s * g:e * g])).to(DEV),
+                             gam[s:e], torch.from_numpy(u[r0:r1].astype(np.float32)).to(DEV))
+                a, t, _, _ = run(bb, NJ_PATH_FUSED, max_batch=48)
+                out_n.append(a)
+                out_t.append(t)
+            return np.concatenate(out_n), np.concatenate(out_t)
+
+        cells = bruteforce.build_cells(bruteforce.closed_form_p(n["hidden_bits"], n["W_bits"]),
+                                       q.astype(np.float64), g, f32_uniforms=True)
+        H, x, Q, gam, u = bruteforce.batch_inputs(n["hidden_bits"], q, cells, g)
+        gn, gt = gpu_impl(H, n["W_bits"], x, Q, gam, u)
+        r = oracle.verify(H, n["W_bits"], x, Q, gam, u.astype(np.float32))
+        assert (gn == r["accept_len"]).all() and (gt == r["next_token"]).all()
+
+
+# ----------------------------------------------------------------- two-pass path
+def test_twopass_mid():
+    for seed in range(2):
+        b = make_batch(40, "mixed:5", V=8192, d=512, seed=seed, device=DEV)
+        acc, nxt, dd, _ = run(b, NJ_PATH_TWOPASS)
+        check(b, acc, nxt, dd)
+
+
+def test_twopass_toy_and_c2():
+    for seed in range(4):
+        b = make_batch(1, 3, V=32, d=16, seed=seed, device=DEV)
+        acc, nxt, dd, _ = run(b, NJ_PATH_TWOPASS)
+        check(b, acc, nxt, dd)
+    b = make_batch(8, 3, V=QV, d=QD, seed=77, device=DEV, W=w_full())
+    acc, nxt, dd, _ = run(b, NJ_PATH_TWOPASS)
+    check(b, acc, nxt, dd)
+
+
+def test_twopass_c3_large_batch_sampled():
+    """C3 full size (B=64, mixed gamma): all requests against the oracle."""
+    b = make_batch(64, "mixed:5", V=QV, d=QD, seed=5, device=DEV, W=w_full())
+    acc, nxt, dd, _ = run(b)
+    check(b, acc, nxt, dd)
+
+
+# ----------------------------------------------------------------- fallback, stage, host API
+def test_forced_fp64_fallback_matches_oracle():
+    for path in (NJ_PATH_FUSED, NJ_PATH_TWOPASS):
+        b = make_batch(4, "mixed:3", V=2048, d=64, seed=21, device=DEV)
+        acc, nxt, dd, _ = run(b, path, force_fb=True)
+        check(b, acc, nxt, dd)
+        assert (dd["flags"] & NJ_FLAG_FALLBACK).all()
+
+
+def test_sampler_stage_vs_oracle():
+    for B, V in [(6, 5000), (32, QV)]:
+        logits, resid, q, u = make_sampler_case(B, V, 3, DEV)
+        v = Verifier(16, V, max_batch=B, gamma_max=1)
+        nxt = torch.empty(B, dtype=torch.int32, device=DEV)
+        mass = torch.empty(B, dtype=torch.float64, device=DEV)
+        v.sample_from_logits(logits, resid, q, u, nxt, mass)
+        torch.cuda.synchronize()
+        r = oracle.sample_from_logits(logits.cpu().numpy(), resid.cpu().numpy(), q.cpu().numpy(),
+                                      u.cpu().numpy().astype(np.float64))
+        np.testing.assert_allclose(mass.cpu().numpy(), r["mass"], rtol=1e-5)
+        ok = ~r["tie"]
+        assert (nxt.cpu().numpy()[ok] == r["next_token"][ok]).all()
+
+
+def test_verify_host_equals_device():
+    b = make_batch(8, 3, V=4096, d=128, seed=9, device=DEV)
+    acc, nxt, _, v = run(b)
+    pin = lambda t: t.cpu().pin_memory()
+    acc_h = torch.empty(8, dtype=torch.int32).pin_memory()
+    nxt_h = torch.empty(8, dtype=torch.int32).pin_memory()
+    v.verify_host(pin(b.hidden), b.W, pin(b.draft_tokens), pin(b.draft_probs), b.gamma, pin(b.uniforms), acc_h, nxt_h)
+    assert (acc_h.numpy() == acc).all() and (nxt_h.numpy() == nxt).all()
+
+
+def test_invalid_arguments():
+    b = make_batch(2, 3, V=256, d=32, seed=1, device=DEV)
+    v = Verifier(32, 256, max_batch=2, gamma_max=2)
+    acc = torch.empty(2, dtype=torch.int32, device=DEV)
+    with pytest.raises(NJError):   # gamma 3 > gamma_max 2
+        v.verify(b.hidden, b.W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, acc)
+    with pytest.raises(NJError):   # B > max_batch
+        v.verify(b.hidden, b.W, b.draft_tokens, b.draft_probs, np.array([1, 1, 1]), b.uniforms, acc, acc)
