@@ -114,8 +114,8 @@ const char* nj_last_error(const nj_ctx* ctx);
  *   hidden       [N, d]      bf16 row-major
  *   W_lm         [v_end - v_begin, d] bf16 row-major (nn.Linear weight layout)
  *   draft_tokens [G]         int32 global token ids
- *   draft_probs  [G, ldq]    fp32 full draft distributions q_i (ldq >= V,
- *                            ldq % 4 == 0); sharded ranks read cols [v_begin,v_end)
+ *   draft_probs  [G, ldq]    fp32 full draft distributions q_i (ldq >= V);
+ *                            sharded ranks read cols [v_begin,v_end)
  *   uniforms     [N]         fp32 in [0,1)
  *   accept_len   [B]         int32 out
  *   next_token   [B]         int32 out

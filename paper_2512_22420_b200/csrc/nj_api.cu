@@ -505,7 +505,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
     if (!hidden || !W_lm || !uniforms || !accept_len || !next_token)
         return set_err(c, NJ_EINVAL, "NULL device pointer");
     if (pl.G > 0 && (!draft_tokens || !draft_probs)) return set_err(c, NJ_EINVAL, "NULL draft buffers with G=%d", pl.G);
-    if (ldq < c->cfg.V || ldq % 4 != 0) return set_err(c, NJ_ESHAPE, "ldq=%lld must be >= V and a multiple of 4", (long long)ldq);
+    if (ldq < c->cfg.V) return set_err(c, NJ_ESHAPE, "ldq=%lld must be >= V", (long long)ldq);
     if ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(W_lm)) & 15)
         return set_err(c, NJ_ESHAPE, "hidden / W_lm must be 16-byte aligned");
     if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
@@ -605,7 +605,7 @@ nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, cons
     if (s != NJ_OK) return s;
     if (!hidden_h || !u_h || !acc_h || !next_h || (pl.G > 0 && (!tok_h || !q_h)))
         return set_err(c, NJ_EINVAL, "NULL host pointer");
-    if (ldq < c->cfg.V || ldq % 4 != 0) return set_err(c, NJ_ESHAPE, "ldq=%lld", (long long)ldq);
+    if (ldq < c->cfg.V) return set_err(c, NJ_ESHAPE, "ldq=%lld must be >= V", (long long)ldq);
     if (!c->st_hidden || c->st_ldq < ldq) {
         if (c->st_q) { cudaFree(c->st_q); c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void*)c->st_q)); }
         if (!c->st_hidden) {

@@ -313,6 +313,9 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
             if (fabs(uq - pd) <= (double)p.eps_acc * pd) flag = 1;
             if (!(uq < pd)) { n = i; break; }
         }
+        if (cta == 0 && p.dbg_pdraft)   // untested drafts still report p_i(x_i)
+            for (int i = n + 1; i < gam; ++i)
+                p.dbg_pdraft[g0 + i] = (float)exp(__ldcg(&p.dl[g0 + i]) - lse_s[ro + i]);
         ReqInfo r;
         r.n = n; r.gam = gam; r.srow = ro + n; r.qrow = g0 + n; r.resid = n < gam;
         r.flag = flag; r.lse_s = lse_s[ro + n];
