@@ -81,7 +81,7 @@ size_t fused_tail(int NPAD, int S) {
     t += (size_t)NPAD * kMaxT * 4 * sizeof(float);
     t += (size_t)NPAD * (kMaxT + 1) * sizeof(double);
     t += NPAD * sizeof(double);
-    t += 3 * NPAD * sizeof(int32_t) + 4 * sizeof(int32_t);
+    t += 5 * NPAD * sizeof(int32_t) + 4 * sizeof(int32_t) + 2 * NPAD * sizeof(float);
     t = align_up(t, 8);
     t += (size_t)(2 * S + 16) * 8 + 8;
     return t;
@@ -112,6 +112,7 @@ struct nj_ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;
     double prof_ms = 0.0;
     int64_t prof_n = 0;
+    unsigned long long* phase_ts = nullptr;   // debug (NJ_PHASE_TS=1)
     // certificate margins: fused path logits err <= 6e-7 (ln p);
     // two-pass path (plain tcgen05 accumulation) err <= 8e-5 (lse)
     float eps_acc_fused = 2e-6f, eps_draw_fused = 0.f;
@@ -263,26 +264,50 @@ nj_status prof_end(nj_ctx* c, cudaStream_t st, std::pair<cudaEvent_t, cudaEvent_
 
 template <int NPAD>
 nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtensorMap& tmH, FusedParams& fp) {
-    // ring stages of GK k-blocks: one barrier round trip per 4 x 16 KB of W keeps
-    // the TMA stream at HBM speed (scripts/stream_test.py: 16-KB stages reach
-    // 4.75 TB/s, 64-KB stages 6.6 TB/s on B200)
-    int GK = 4;
-    if (const char* e = getenv("NJ_KGROUP")) GK = std::max(1, atoi(e));
-    const size_t stage = (size_t)GK * (kTileBytesA + NPAD * 128);
-    int S = (int)std::min<size_t>(8, (kSmemLimit - fused_tail(NPAD, 8) - 1024) / stage);
-    if (S < 2) { GK = 2; }
+    // ring stages of GK k-blocks: one barrier round trip per GK x 16 KB of W keeps
+    // the TMA stream at HBM speed (scripts/stream_test*.py: 16-KB stages reach
+    // 4.75 TB/s, 48-64-KB stages 6.3-6.8 TB/s on B200).  The k-block partials of a
+    // stage are drained with ONE handshake into double-buffered scratch groups,
+    // which must fit in TMEM next to the resident logits (max_tiles x NPAD).
+    fp.scratch_col = c->max_tiles * NPAD;
+    const int spare = 512 - fp.scratch_col;
+    int GK = std::min(4, spare / (2 * NPAD));
+    fp.kpd = 1;
+    if (GK >= 2) {
+        fp.ngroups = 2;
+        fp.nbuf = 2 * GK;
+    } else {   // no room for two groups (NPAD = 48): per-partial handshake, one
+        GK = 4;    // buffer, partials of 2 k-blocks (restart every 8 MMAs)
+        fp.ngroups = 0;
+        fp.nbuf = std::max(1, std::min(8, spare / NPAD));
+        fp.kpd = 2;
+    }
+    if (const char* e = getenv("NJ_KGROUP")) GK = std::max(1, atoi(e));   // tuning knobs
+    if (const char* e = getenv("NJ_KPD")) fp.kpd = std::max(1, atoi(e));
     const size_t stage2 = (size_t)GK * (kTileBytesA + NPAD * 128);
-    S = (int)std::min<size_t>(8, (kSmemLimit - fused_tail(NPAD, 8) - 1024) / stage2);
+    const int S = (int)std::min<size_t>(8, (kSmemLimit - fused_tail(NPAD, 8) - 1024) / stage2);
     fp.nstages = S;
     fp.kgroup = GK;
-    fp.scratch_col = c->max_tiles * NPAD;
-    fp.nbuf = std::min(8, (512 - fp.scratch_col) / NPAD);
-    fp.kpd = 1;
-    fp.f32drain = 0;
-    if (const char* e = getenv("NJ_NBUF")) fp.nbuf = std::max(1, std::min(fp.nbuf, atoi(e)));   // tuning knobs
-    if (const char* e = getenv("NJ_KPD")) fp.kpd = std::max(1, atoi(e));
-    if (const char* e = getenv("NJ_F32DRAIN")) fp.f32drain = atoi(e);
+    fp.eps_acc = fp.kpd == 1 ? c->eps_acc_fused : 2.0f * c->eps_acc_fused;
+    if (const char* e = getenv("NJ_PHASE_TS")) {
+        if (*e == '1' && !c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
+        fp.phase_ts = c->phase_ts;
+    }
     const size_t smem = (size_t)S * stage2 + fused_tail(NPAD, S);
+    // post-GEMM scratch in the idle ring: q slices [G (prefetch) or nq][rows_cap] fp32,
+    // then partials [N][grid] float2 (phase 2) and masses [B][grid] fp64 (phase 4)
+    fp.rows_cap = c->max_tiles * kTileV;
+    const size_t ring = (size_t)S * stage2;
+    const size_t all_q = align_up((size_t)pl.G * fp.rows_cap * 4, 16);
+    fp.q_prefetch = all_q <= ring ? 1 : 0;
+    const int nq = std::min(pl.B, pl.G);
+    fp.q_bytes_cap = (int)(fp.q_prefetch ? all_q : align_up((size_t)nq * fp.rows_cap * 4, 16));
+    const size_t tailb = 0;
+    fp.q_vec16 = (fp.ldq % 4 == 0 && c->cfg.v_begin % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(fp.q) & 15) == 0) ? 1 : 0;
+    if ((size_t)fp.q_bytes_cap + tailb > ring)
+        return set_err(c, NJ_EUNSUPPORTED, "fused path: post-GEMM scratch %zu > ring %zu",
+                       (size_t)fp.q_bytes_cap + tailb, ring);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->grid);
     cfg.blockDim = dim3(kFusedThreads);
@@ -350,10 +375,27 @@ FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const i
     return f;
 }
 
+// launch with programmatic stream serialization (PDL): the kernel may start
+// before its predecessor finishes and waits in-kernel (griddepcontrol.wait)
+template <typename K, typename... Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 nj_status launch_fallback(nj_ctx* c, cudaStream_t st, const FbParams& f, const ReqMeta& m) {
-    k_fb_logits<<<c->num_sms * 2, 256, 0, st>>>(f, m);
+    NJ_CUDA(c, launch_pdl(k_fb_logits, dim3(c->num_sms * 2), dim3(256), st, f, m));
     NJ_LAUNCHED(c, "k_fb_logits", st);
-    k_fb_decide<<<std::min(c->cfg.max_batch, c->num_sms), 256, 0, st>>>(f, m);
+    NJ_CUDA(c, launch_pdl(k_fb_decide, dim3(std::min(c->cfg.max_batch, c->num_sms)), dim3(256), st, f, m));
     NJ_LAUNCHED(c, "k_fb_decide", st);
     return NJ_OK;
 }
@@ -373,6 +415,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     if (cfg->v_begin < 0 || cfg->v_end > cfg->V || cfg->v_begin >= cfg->v_end)
         return set_err(nullptr, NJ_ESHAPE, "bad shard [%d,%d) of V=%d", cfg->v_begin, cfg->v_end, cfg->V);
     if (cfg->nccl_comm) return set_err(nullptr, NJ_EUNSUPPORTED, "vocab-sharded mode is not built in this round");
+    // (the fused kernel keeps every lane's CTA partials in registers: grid <= 160)
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         return set_err(nullptr, NJ_ECUDA, "no CUDA device visible (libnj has no CPU fallback)");
@@ -389,7 +432,15 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     c->V_local = cfg->v_end - cfg->v_begin;
     c->num_sms = prop.multiProcessorCount;
     c->U = (c->V_local + kUnit - 1) / kUnit;
-    c->grid = std::min(c->num_sms, c->U);
+    // tile-balanced persistent grid: every CTA gets ceil(T/grid) or fewer whole
+    // 128-row tiles (V = 152064 -> 132 CTAs x 9 tiles; a ragged 148-CTA split
+    // leaves 16-row tail tiles that run latency-bound and finish last)
+    {
+        const int T = (c->V_local + kTileV - 1) / kTileV;
+        const int tpc = (T + c->num_sms - 1) / c->num_sms;
+        c->grid = std::max(1, std::min(c->U, (T + tpc - 1) / tpc));
+        if (const char* e = getenv("NJ_GRID")) c->grid = std::max(1, std::min(c->U, atoi(e)));
+    }
     const int upc = (c->U + c->grid - 1) / c->grid;
     c->max_tiles = (upc * kUnit + kTileV - 1) / kTileV;
     c->nchunks = (c->V_local + kChunk - 1) / kChunk;
@@ -462,6 +513,12 @@ nj_status nj_set_option(nj_ctx* c, nj_option opt, int64_t v) {
     return set_err(c, NJ_EINVAL, "unknown option %d", (int)opt);
 }
 
+nj_status nj_debug_phase_times(nj_ctx* c, unsigned long long* host_out, int32_t n) {
+    if (!c || !c->phase_ts) return NJ_EINVAL;
+    NJ_CUDA(c, cudaMemcpy(host_out, c->phase_ts, sizeof(unsigned long long) * std::min(n, 16 * 1024), cudaMemcpyDeviceToHost));
+    return NJ_OK;
+}
+
 nj_status nj_kernel_time(nj_ctx* c, double* ms_total, int64_t* launches, int32_t reset) {
     if (!c) return NJ_EINVAL;
     for (auto& e : c->ev) {
@@ -523,7 +580,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         fp.draft_tokens = draft_tokens; fp.q = draft_probs; fp.ldq = ldq; fp.u = uniforms;
         fp.accept_len = accept_len; fp.next_token = next_token;
         fp.part_m = c->part_m; fp.part_s = c->part_s; fp.dl = c->dl; fp.wpart = c->wpart;
-        fp.bar_count = c->bar; fp.bar_gen = c->bar + 1;
+        fp.bar = c->bar;
         fp.fb_count = c->fb_count(); fp.fb_list = c->fb_list(); fp.req_flags = c->req_flags();
         fp.dbg_lse = dbg ? dbg->lse : nullptr; fp.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
         fp.dbg_mass = dbg ? dbg->mass : nullptr; fp.dbg_flags = dbg ? dbg->flags : nullptr;
@@ -696,7 +753,9 @@ nj_status nj_stream_test(nj_ctx* c, void* stream, const uint16_t* W, int32_t mod
     const size_t smem = (size_t)nstages * group * (kTileBytesA + sp.hrows * 128) + 2 * nstages * 8 + 16;
     if (smem > (size_t)kSmemLimit) return set_err(c, NJ_ESHAPE, "smem %zu", smem);
     NJ_CUDA(c, set_smem_attr(k_stream_test));
-    k_stream_test<<<c->grid, 128, smem, st>>>(m128, m16, mh, sp);
+    int grid = c->grid;
+    if (const char* e = getenv("NJ_GRID")) grid = std::max(1, std::min(c->grid, atoi(e)));
+    k_stream_test<<<grid, 128, smem, st>>>(m128, m16, mh, sp);
     NJ_LAUNCHED(c, "k_stream_test", st);
     return NJ_OK;
 }

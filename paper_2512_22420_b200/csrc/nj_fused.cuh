@@ -46,16 +46,82 @@ __device__ __forceinline__ void st_cols(uint32_t taddr, const float (&v)[NC]) {
     }
 }
 
+// Warp reduce-scatter of online-softmax pairs over 32 lanes for NCP columns
+// (NCP = 8/16/32): at every step each lane keeps half of its columns and merges
+// the other half received from lane ^ o.  NCP merges per lane instead of
+// 5 * NCP for per-column butterflies.  On return lane l holds the warp-wide
+// (m, s) of column col_of_lane<NCP>(l) (every column is held by 32/NCP lanes).
+template <int NCP>
+__device__ __forceinline__ int col_of_lane(int l) {
+    // bits consumed in order 16, 8, 4, ... while columns remain; bit set = upper half
+    int col = 0, width = NCP;
+#pragma unroll
+    for (int o = 16; o >= 1 && width > 1; o >>= 1) {
+        width >>= 1;
+        if (l & o) col += width;
+    }
+    return col;
+}
+template <int NCP>
+__device__ __forceinline__ void warp_scatter_ms(float (&m)[NCP], float (&s)[NCP], float& mo, float& so) {
+    const int l = (int)lane_id();
+    int width = NCP;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        if (width > 1) {
+            const int h = width >> 1;
+            const bool up = (l & o) != 0;
+#pragma unroll
+            for (int j = 0; j < NCP / 2; ++j) {
+                if (j < h) {
+                    // keep half [up ? h : 0, +h), send the other half
+                    const float sm_m = up ? m[j] : m[h + j];
+                    const float sm_s = up ? s[j] : s[h + j];
+                    const float rm = __shfl_xor_sync(0xffffffffu, sm_m, o);
+                    const float rs = __shfl_xor_sync(0xffffffffu, sm_s, o);
+                    float km = up ? m[h + j] : m[j];
+                    float ks = up ? s[h + j] : s[j];
+                    ms_merge(km, ks, rm, rs);
+                    m[j] = km;
+                    s[j] = ks;
+                }
+            }
+            width = h;
+        } else {
+            const float rm = __shfl_xor_sync(0xffffffffu, m[0], o);
+            const float rs = __shfl_xor_sync(0xffffffffu, s[0], o);
+            ms_merge(m[0], s[0], rm, rs);
+        }
+    }
+    mo = m[0];
+    so = s[0];
+}
+
 constexpr int kFusedThreads = 384;   // warps 0-3 control, 4-11 epilogue (2 per TMEM lane quadrant)
 
 // residual / bonus weight of one vocab entry (BJ step 3); the lse shift is
 // taken in fp64 so no common-mode fp32 rounding of lse scales p against q.
-__device__ __forceinline__ float sample_weight(float l, double lse, bool resid, const float* qrow, int xl,
+// qrow: this CTA's slice of the q row in smem (x relative to the CTA start).
+// p = exp(l - c) * corr with c = fp32(lse), corr = exp(c - lse) computed once in
+// fp64 per request: no common-mode fp32 rounding of lse scales p against q, and
+// no fp64 work per vocab entry.
+__device__ __forceinline__ float sample_weight(float l, float c, float corr, bool resid, const float* qrow, int xr,
                                                bool valid) {
     if (!valid) return 0.f;
-    const float pe = __expf((float)((double)l - lse));
-    return resid ? fmaxf(pe - __ldg(&qrow[xl]), 0.f) : pe;
+    const float pe = __expf(l - c) * corr;
+    return resid ? fmaxf(pe - qrow[xr], 0.f) : pe;
 }
+
+// Debug phase stamps (NJ_PHASE_TS=1): the extra barrier plus a dependent shared
+// load make the stamp wait for the whole CTA (BAR.SYNC itself is defer-blocking).
+#define NJ_STAMP(k)                                                                   \
+    do {                                                                              \
+        if (p.phase_ts) {                                                             \
+            __syncthreads();                                                          \
+            const int dep_ = *reinterpret_cast<volatile int*>(&spick[0]);             \
+            if (threadIdx.x == 0 && dep_ != 0x7fffffff) p.phase_ts[cta * 16 + (k)] = globaltimer(); \
+        }                                                                             \
+    } while (0)
 
 template <int NPAD>
 __global__ void __launch_bounds__(kFusedThreads, 1)
@@ -83,8 +149,12 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
     int32_t* cg = ctok + NPAD;                                            // [NPAD]
     int32_t* owner = cg + NPAD;                                           // [NPAD]
     int32_t* spick = owner + NPAD;                                        // [4]
+    int32_t* dpass = spick + 4;                                           // [NPAD] per-draft test result
+    int32_t* qslot = dpass + NPAD;                                        // [NPAD] q-slice slot of request b
+    float* qx_sm = reinterpret_cast<float*>(qslot + NPAD);                // [NPAD] q_i(x_i) of draft rows
+    float* u_sm = qx_sm + NPAD;                                           // [NPAD] uniforms
     uint64_t* bars = reinterpret_cast<uint64_t*>(
-        (reinterpret_cast<uintptr_t>(spick + 4) + 7) & ~uintptr_t(7));
+        (reinterpret_cast<uintptr_t>(u_sm + NPAD) + 7) & ~uintptr_t(7));
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
     uint64_t* pfull = bars + 2 * S;   // [kMaxBufs] scratch accumulator ready
@@ -126,6 +196,10 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
         }
         ctok[j] = tok;
         cg[j] = g;
+        // inputs of the acceptance tests, fetched now so they never sit on the
+        // critical path after the grid barrier
+        u_sm[j] = j < N ? __ldg(&p.u[j]) : 0.f;
+        qx_sm[j] = g >= 0 ? __ldg(&p.q[(int64_t)g * p.ldq + tok + p.v_begin]) : 0.f;
     }
     if (cta == 0)
         for (int b = threadIdx.x; b < B; b += kFusedThreads) p.req_flags[b] = 0;
@@ -133,6 +207,7 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    NJ_STAMP(0);
 
     // =============================================================== phase 1
     if (warp == 0 && lane == 0) {
@@ -163,28 +238,41 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
         const int kpd = p.kpd;
         int s = 0, buf = 0, kin = 0;
         uint32_t ph = 0, bph = 0;
+        const int NGRP = p.ngroups;   // > 0: one handshake per ring stage (GK partials)
+        int grp = 0;
+        uint32_t gph = 0;
         for (int t = 0; t < ntiles; ++t) {
             for (int kg = 0; kg < nkg; ++kg) {
                 const int ng = min(GK, p.num_kb - kg * GK);
+                if (NGRP > 0) mbar_wait(&pempty[grp], gph ^ 1);   // group buffers drained
                 mbar_wait(&full[s], ph);
+                tc_fence_after();
                 for (int g = 0; g < ng; ++g) {
                     const int kb = kg * GK + g;
-                    if (kin == 0) mbar_wait(&pempty[buf], bph ^ 1);
-                    tc_fence_after();
-                    const uint32_t dt = tbase + scol + (uint32_t)(buf * NPAD);
+                    uint32_t dt;
+                    if (NGRP > 0) {
+                        dt = tbase + scol + (uint32_t)((grp * GK + g) * NPAD);
+                    } else {
+                        if (kin == 0) { mbar_wait(&pempty[buf], bph ^ 1); tc_fence_after(); }
+                        dt = tbase + scol + (uint32_t)(buf * NPAD);
+                    }
                     const size_t slot = (size_t)s * GK + g;
                     const uint64_t ad = sdesc_sw128(sA + slot * kTileBytesA);
                     const uint64_t bd = sdesc_sw128(sB + slot * kBBytes);
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k)
                         mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
-                    if (++kin == kpd || kb + 1 == p.num_kb) {
+                    if (NGRP == 0 && (++kin == kpd || kb + 1 == p.num_kb)) {
                         mma_commit(&pfull[buf]);
                         kin = 0;
                         if (++buf == NB) { buf = 0; bph ^= 1; }
                     }
                 }
                 mma_commit(&empty[s]);
+                if (NGRP > 0) {
+                    mma_commit(&pfull[grp]);
+                    if (++grp == NGRP) { grp = 0; gph ^= 1; }
+                }
                 if (++s == S) { s = 0; ph ^= 1; }
             }
         }
@@ -199,36 +287,60 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
         int buf = 0;
         uint32_t bph = 0;
         const int ndrain = (p.num_kb + p.kpd - 1) / p.kpd;
+        const int NGRP = p.ngroups;
+        int grp = 0;
+        uint32_t gph = 0;
+        // softmax statistics: at every tile end a warp reduce-scatter turns this
+        // warp's (tile x NC columns) values into one (m, s) per column, merged into
+        // a running pair held by the lanes owning that column (2 registers).
+        constexpr int NCP = NC <= 8 ? 8 : (NC <= 16 ? 16 : 32);
+        float run_m = -INFINITY, run_s = 0.f;
         for (int t = 0; t < ntiles; ++t) {
             double acc[NC];
 #pragma unroll
             for (int j = 0; j < NC; ++j) acc[j] = 0.0;
-            float accf[NC];
+            if (NGRP > 0) {
+                for (int kg = 0; kg < nkg; ++kg) {   // one group = the GK partials of a ring stage
+                    const int ng = min(GK, p.num_kb - kg * GK);
+                    mbar_wait(&pfull[grp], gph);
+                    tc_fence_after();
+                    // the stage's k-block partials (each restarted: no RZ bias) are summed
+                    // in fp32 round-to-nearest (unbiased, ~1e-8 |l|), then once in fp64
+                    float ssum[NC];
 #pragma unroll
-            for (int j = 0; j < NC; ++j) accf[j] = 0.f;
-            for (int dk = 0; dk < ndrain; ++dk) {   // drain one partial
-                mbar_wait(&pfull[buf], bph);
-                tc_fence_after();
-                float v[NC];
-                ld_cols<NC>(lane_base + scol + (uint32_t)(buf * NPAD), v);
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&pempty[buf]);
-                if (++buf == NB) { buf = 0; bph ^= 1; }
-                if (p.f32drain) {
+                    for (int j = 0; j < NC; ++j) ssum[j] = 0.f;
+                    for (int g = 0; g < ng; ++g) {
+                        float v[NC];
+                        ld_cols<NC>(lane_base + scol + (uint32_t)((grp * GK + g) * NPAD), v);
 #pragma unroll
-                    for (int j = 0; j < NC; ++j) accf[j] += v[j];
-                } else {
+                        for (int j = 0; j < NC; ++j) ssum[j] += v[j];
+                    }
+#pragma unroll
+                    for (int j = 0; j < NC; ++j) acc[j] += (double)ssum[j];
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&pempty[grp]);
+                    if (++grp == NGRP) { grp = 0; gph ^= 1; }
+                }
+            } else {
+                for (int dk = 0; dk < ndrain; ++dk) {   // drain one partial
+                    mbar_wait(&pfull[buf], bph);
+                    tc_fence_after();
+                    float v[NC];
+                    ld_cols<NC>(lane_base + scol + (uint32_t)(buf * NPAD), v);
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&pempty[buf]);
+                    if (++buf == NB) { buf = 0; bph ^= 1; }
 #pragma unroll
                     for (int j = 0; j < NC; ++j) acc[j] += (double)v[j];
                 }
             }
-            if (p.f32drain) {
-#pragma unroll
-                for (int j = 0; j < NC; ++j) acc[j] = (double)accf[j];
-            }
             const bool valid = vr < min(kTileV, rows - t * kTileV);
             const int xl = r0 + t * kTileV + vr;
+            float f[NC];
+#pragma unroll
+            for (int j = 0; j < NC; ++j) f[j] = (float)acc[j];
             if (valid) {
 #pragma unroll
                 for (int j = 0; j < NC; ++j) {
@@ -236,37 +348,23 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
                     if (col < N && ctok[col] == xl) p.dl[cg[col]] = acc[j];   // fp64 draft logit
                 }
             }
-            float f[NC];
-#pragma unroll
-            for (int j = 0; j < NC; ++j) f[j] = (float)acc[j];
             st_cols<NC>(lane_base + (uint32_t)(t * NPAD), f);
-        }
-        // softmax statistics of this thread's vocab lanes from the stored logits
-        // (tcgen05.ld is warp-collective: every lane loads, invalid lanes are masked after)
-        float m[NC], sm[NC];
+            float tm[NCP], ts[NCP];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) { m[j] = -INFINITY; sm[j] = 0.f; }
-        for (int t = 0; t < ntiles; ++t) {
-            float v[NC];
-            ld_cols<NC>(lane_base + (uint32_t)(t * NPAD), v);
-            if (vr < min(kTileV, rows - t * kTileV)) {
-#pragma unroll
-                for (int j = 0; j < NC; ++j) m[j] = fmaxf(m[j], v[j]);
+            for (int j = 0; j < NCP; ++j) {
+                const bool ok = valid && j < NC;
+                tm[j] = ok ? f[j < NC ? j : 0] : -INFINITY;
+                ts[j] = ok ? 1.f : 0.f;
             }
+            float wm, ws;
+            warp_scatter_ms<NCP>(tm, ts, wm, ws);
+            ms_merge(run_m, run_s, wm, ws);
         }
-        for (int t = 0; t < ntiles; ++t) {
-            float v[NC];
-            ld_cols<NC>(lane_base + (uint32_t)(t * NPAD), v);
-            if (vr < min(kTileV, rows - t * kTileV)) {
-#pragma unroll
-                for (int j = 0; j < NC; ++j) sm[j] += __expf(v[j] - m[j]);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < NC; ++j) {
-            float mj = m[j], sj = sm[j];
-            warp_ms_merge(mj, sj);
-            if (lane == 0) red[q * NPAD + e * NC + j] = make_float2(mj, sj);
+        {
+            const int c = col_of_lane<NCP>(lane);
+            // the lowest lane holding column c writes it
+            if (c < NC && lane == (lane & ~((32 / NCP) - 1)) && ((lane & ((32 / NCP) - 1)) == 0 || NCP == 32))
+                red[q * NPAD + e * NC + c] = make_float2(run_m, run_s);
         }
         named_bar(2, 256);
         const int et = threadIdx.x - 128;
@@ -278,125 +376,237 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
             p.part_s[(int64_t)et * grid + cta] = sj;
         }
     }
-    grid_barrier(p.bar_count, p.bar_gen, grid);
+    __syncthreads();   // phase 1 done: the TMA ring is idle from here on
+    NJ_STAMP(1);
+    // The idle ring becomes scratch for the latency-bound phases (every global
+    // read below is one cooperative sweep, so each phase pays ~one memory
+    // latency instead of one per request).
+    const int rows_cap = p.rows_cap;                                      // max rows per CTA
+    float* qsl = reinterpret_cast<float*>(smem);                          // [G or nq][rows_cap] (3-4)
+    grid_barrier(p.bar, grid);
     tc_fence_after();
+    NJ_STAMP(2);
 
     // =============================================================== phase 2
-    for (int j = warp; j < N; j += kFusedThreads / 32) {   // lse_j, warp per row
-        float mx = -INFINITY;
-        for (int c = lane; c < grid; c += 32) mx = fmaxf(mx, __ldcg(&p.part_m[(int64_t)j * grid + c]));
-        mx = warp_max(mx);
-        double sacc = 0.0;
-        for (int c = lane; c < grid; c += 32) {
-            const float mc = __ldcg(&p.part_m[(int64_t)j * grid + c]);
-            const float sc = __ldcg(&p.part_s[(int64_t)j * grid + c]);
-            if (mc != -INFINITY) sacc += (double)sc * (double)__expf(mc - mx);
+    // (a) lse_j = M + log(sum_c s_c e^{m_c - M}): 8 lanes per row, all rows at
+    //     once, partials read straight from L2 (L1 was invalidated by the barrier)
+    // the acceptance test's fp64 draft logit rides on the same memory round trip
+    const double dlv = ((int)threadIdx.x < N && cg[threadIdx.x] >= 0) ? p.dl[cg[threadIdx.x]] : 0.0;
+    {   // N <= 48 = kFusedThreads / 8 row groups: one pass
+        const int j = warp * 4 + (lane >> 3);
+        const int sub = lane & 7;
+        const bool act = j < N;
+        constexpr int kPer = 20;   // grid <= 160: every lane's partials in registers, loads issued together
+        float mv[kPer], sv[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int c = sub + 8 * k;
+            const bool ok = act && c < grid;
+            mv[k] = ok ? p.part_m[(int64_t)j * grid + c] : -INFINITY;
+            sv[k] = ok ? p.part_s[(int64_t)j * grid + c] : 0.f;
         }
-        sacc = warp_sum_d(sacc);
-        if (lane == 0) {
+    if (p.q_prefetch) {
+        // every draft row's q slice [r0, r0+rows) -> smem, fire-and-forget; it lands
+        // while this CTA runs phase 2 (issued after the barrier: its fence would wait on it)
+        const int G = p.G;
+        if (p.q_vec16) {
+            const int n4 = (rows + 3) >> 2;
+            for (int i = threadIdx.x; i < G * n4; i += kFusedThreads) {
+                const int g = i / n4, x = (i - g * n4) * 4;
+                cp_async16(qsl + (size_t)g * rows_cap + x, p.q + (int64_t)g * p.ldq + p.v_begin + r0 + x);
+            }
+        } else {
+            for (int i = threadIdx.x; i < G * rows; i += kFusedThreads) {
+                const int g = i / rows, x = i - g * rows;
+                cp_async4(qsl + (size_t)g * rows_cap + x, p.q + (int64_t)g * p.ldq + p.v_begin + r0 + x);
+            }
+        }
+        cp_async_commit();
+    }
+        NJ_STAMP(3);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) mx = fmaxf(mx, mv[k]);
+#pragma unroll
+        for (int o = 4; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        double sacc = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPer; ++k)
+            if (mv[k] != -INFINITY) sacc += (double)sv[k] * (double)__expf(mv[k] - mx);
+#pragma unroll
+        for (int o = 4; o; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (act && sub == 0) {
             lse_s[j] = (double)mx + log(sacc);
             if (cta == 0 && p.dbg_lse) p.dbg_lse[j] = (float)lse_s[j];
         }
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < B; b += kFusedThreads) {   // Leviathan acceptance (R2: u*q < p)
-        const int ro = p.row_off[b];
-        const int gam = p.row_off[b + 1] - ro - 1;
-        const int g0 = ro - b;
-        int n = gam, flag = 0;
-        for (int i = 0; i < gam; ++i) {
-            const int g = g0 + i;
-            const double pd = exp(__ldcg(&p.dl[g]) - lse_s[ro + i]);
-            const double qx = (double)p.q[(int64_t)g * p.ldq + p.draft_tokens[g]];
-            const double uq = (double)p.u[ro + i] * qx;
+    NJ_STAMP(4);
+    // (b) every drafted token tested in parallel (Leviathan, R2: accept iff u*q < p)
+    for (int j = threadIdx.x; j < N; j += kFusedThreads) {   // N <= 48 < threads: j == jd
+        int res = 1;   // 1 accept, 0 reject, | 2 near-tie (certificate)
+        const int g = cg[j];
+        if (g >= 0) {
+            const double pd = exp(dlv - lse_s[j]);
+            const double uq = (double)u_sm[j] * (double)qx_sm[j];
+            res = (uq < pd) ? 1 : 0;
+            if (fabs(uq - pd) <= (double)p.eps_acc * pd) res |= 2;
             if (cta == 0 && p.dbg_pdraft) p.dbg_pdraft[g] = (float)pd;
-            if (fabs(uq - pd) <= (double)p.eps_acc * pd) flag = 1;
-            if (!(uq < pd)) { n = i; break; }
         }
-        if (cta == 0 && p.dbg_pdraft)   // untested drafts still report p_i(x_i)
-            for (int i = n + 1; i < gam; ++i)
-                p.dbg_pdraft[g0 + i] = (float)exp(__ldcg(&p.dl[g0 + i]) - lse_s[ro + i]);
-        ReqInfo r;
-        r.n = n; r.gam = gam; r.srow = ro + n; r.qrow = g0 + n; r.resid = n < gam;
-        r.flag = flag; r.lse_s = lse_s[ro + n];
-        req[b] = r;
-        if (cta == 0 && p.certify && (flag || p.force_fallback))
-            push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
+        dpass[j] = res;
     }
     __syncthreads();
+    // (c) first rejection per request; q-slice slots for rejected requests
+    if (threadIdx.x < 32) {
+        int base = 0;
+        for (int b0 = 0; b0 < B; b0 += 32) {
+            const int b = b0 + lane;
+            int is_rej = 0;
+            ReqInfo r;
+            if (b < B) {
+                const int ro = p.row_off[b];
+                const int gam = p.row_off[b + 1] - ro - 1;
+                int n = gam, flag = 0;
+                for (int i = 0; i < gam; ++i) {
+                    const int res = dpass[ro + i];
+                    if (res & 2) flag = 1;
+                    if (!(res & 1)) { n = i; break; }
+                }
+                r.n = n; r.gam = gam; r.srow = ro + n; r.qrow = ro - b + n; r.resid = n < gam;
+                r.flag = flag; r.lse_s = lse_s[ro + n];
+                req[b] = r;
+                is_rej = r.resid;
+                if (cta == 0 && p.certify && (flag || p.force_fallback))
+                    push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, is_rej);
+            if (b < B) qslot[b] = is_rej ? base + __popc(m & ((1u << lane) - 1u)) : -1;
+            base += __popc(m);
+        }
+    }
+    __syncthreads();
+    NJ_STAMP(5);
+    // (d) the rejected requests' q slices [r0, r0+rows) -> smem (unless prefetched)
+    if (p.q_prefetch) cp_async_wait_all();
+    for (int b = 0; b < B && !p.q_prefetch; ++b) {
+        const int s = qslot[b];
+        if (s < 0) continue;
+        const float* src = p.q + (int64_t)req[b].qrow * p.ldq + p.v_begin + r0;
+        float* dst = qsl + (size_t)s * rows_cap;
+        for (int x = threadIdx.x; x < rows; x += kFusedThreads) dst[x] = __ldg(&src[x]);
+    }
+    __syncthreads();
+    NJ_STAMP(6);
 
     // =============================================================== phase 3
-    if (warp >= 4 && warp < 8) {
+    // this CTA's residual max(0, p_n - q_n) / bonus p_gamma mass of every
+    // request, straight from TMEM: all 12 warps (3 sets x 4 lane quadrants) split
+    // the requests; per lane a sequential sum over its tiles, then one warp sum.
+    {
         const int q = warp & 3;
+        const int set = warp >> 2;
         const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
         const int vr = q * 32 + lane;
-        for (int b = 0; b < B; ++b) {
+        for (int b = set; b < B; b += kFusedThreads / 128) {
             const ReqInfo r = req[b];
-            const float* qrow = p.q + (int64_t)r.qrow * p.ldq + p.v_begin;
+            const float* qrow = !r.resid ? nullptr
+                                : qsl + (size_t)(p.q_prefetch ? r.qrow : qslot[b]) * rows_cap;
+            const float c = (float)r.lse_s;
+            const float corr = (float)exp((double)c - r.lse_s);
             uint32_t a[kMaxT];
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t)
                 a[t] = lane_base + (uint32_t)((t < ntiles ? t : 0) * NPAD + r.srow);
             float lv[kMaxT];
             tmem_ld1x16(a, lv);
+            float s = 0.f;
 #pragma unroll
             for (int t = 0; t < kMaxT; ++t) {
-                if (t < ntiles) {
-                    const bool valid = vr < min(kTileV, rows - t * kTileV);
-                    const float w = sample_weight(lv[t], r.lse_s, r.resid, qrow, r0 + t * kTileV + vr, valid);
-                    const float inc = warp_incl_scan(w);
-                    if (lane == 31) wtile[(b * kMaxT + t) * 4 + q] = inc;
+                const bool valid = t < ntiles && vr < min(kTileV, rows - t * kTileV);
+                s += sample_weight(lv[t], c, corr, r.resid, qrow, t * kTileV + vr, valid);
+            }
+            s = warp_sum(s);
+            if (lane == 0) wtile[b * 4 + q] = s;
+        }
+    }
+    __syncthreads();
+    NJ_STAMP(7);
+    for (int b = threadIdx.x; b < B; b += kFusedThreads) {   // CTA mass, fixed fp64 order
+        const float* wq = &wtile[b * 4];
+        p.wpart[(int64_t)b * grid + cta] = (((double)wq[0] + (double)wq[1]) + (double)wq[2]) + (double)wq[3];
+    }
+    NJ_STAMP(8);
+    grid_barrier(p.bar, grid);
+    tc_fence_after();
+    NJ_STAMP(9);
+
+    // =============================================================== phase 4
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // warp per request: each lane sums a contiguous run of CTA masses, an inclusive
+    // warp scan of the run totals gives every CTA's interval [E_c, I_c) with
+    // E_c = I_{c-1} taken from the same values, so the intervals tile [0, W)
+    // exactly and every CTA computes bit-identical bounds.
+    for (int b = warp; b < B; b += kFusedThreads / 32) {
+        const ReqInfo r = req[b];
+        const int per = (grid + 31) / 32;
+        const int c0 = lane * per, c1 = min(grid, c0 + per);
+        double wv[8];
+        double run = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            wv[k] = (k < per && c0 + k < c1) ? p.wpart[(int64_t)b * grid + c0 + k] : 0.0;
+            if (k < per && c0 + k < c1) run = run + wv[k];
+        }
+        const double incl = warp_incl_scan_d(run);
+        const double W = __shfl_sync(0xffffffffu, incl, 31);
+        double base = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) base = 0.0;
+        double Ec = 0.0, Ic = 0.0;
+        int last_pos = -1;
+        {
+            double acc = base;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int c = c0 + k;
+                if (k < per && c < c1) {
+                    const double nx = (c == c1 - 1) ? incl : acc + wv[k];   // run end = scan value
+                    if (c == cta) { Ec = acc; Ic = nx; }
+                    if (wv[k] > 0.0) last_pos = c;
+                    acc = nx;
                 }
             }
         }
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < B; b += kFusedThreads) {   // CTA mass, fixed fp64 order
-        double acc = 0.0;
-        for (int t = 0; t < ntiles; ++t) {
-            cprefix[b * (kMaxT + 1) + t] = acc;
-            const float* wt = &wtile[(b * kMaxT + t) * 4];
-            acc = acc + ((((double)wt[0] + (double)wt[1]) + (double)wt[2]) + (double)wt[3]);
-        }
-        cprefix[b * (kMaxT + 1) + ntiles] = acc;
-        p.wpart[(int64_t)b * grid + cta] = acc;
-    }
-    grid_barrier(p.bar_count, p.bar_gen, grid);
-    tc_fence_after();
-
-    // =============================================================== phase 4
-    for (int b = threadIdx.x; b < B; b += kFusedThreads) {
-        const ReqInfo r = req[b];
-        double P = 0.0, Pc = 0.0, mine = 0.0;
-        int last_pos = -1;
-        for (int c = 0; c < grid; ++c) {   // P_{c+1} = P_c + wpart_c, c ascending
-            const double wc = __ldcg(&p.wpart[(int64_t)b * grid + c]);
-            if (c == cta) { Pc = P; mine = wc; }
-            if (wc > 0.0) last_pos = c;
-            P = P + wc;
-        }
-        const double W = P;
-        const double T = (double)p.u[p.row_off[b] + r.gam] * W;   // final-draw slot (R3)
-        int own = 0;
-        double tp = T - Pc;
-        if (W > 0.0) {
-            if (T >= W) {                  // rounding overshoot (R5): clamp in the last positive CTA
-                own = (cta == last_pos) ? 2 : 0;
-            } else if (Pc <= T && T < Pc + mine) {
-                own = 1;
+        int lp = last_pos;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) lp = max(lp, __shfl_xor_sync(0xffffffffu, lp, o));
+        const int src = min(cta / max(per, 1), 31);
+        Ec = __shfl_sync(0xffffffffu, Ec, src);
+        Ic = __shfl_sync(0xffffffffu, Ic, src);
+        if (lane == 0) {
+            const double T = (double)u_sm[p.row_off[b] + r.gam] * W;   // final-draw slot (R3)
+            int own = 0;
+            double tp = T - Ec;
+            if (W > 0.0) {
+                if (T >= W) own = (cta == lp) ? 2 : 0;   // rounding overshoot (R5): clamp
+                else if (Ec <= T && T < Ic) own = 1;
+            } else if (cta == 0) {   // zero residual mass (R6): the fp64 fallback draws from p_n
+                p.accept_len[b] = r.n;
+                p.next_token[b] = 0;
+                if (p.dbg_mass) p.dbg_mass[b] = 0.0;
+                if (p.dbg_flags) p.dbg_flags[b] = 2;
+                if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 2);
             }
-        } else if (cta == 0) {             // zero residual mass (R6): the fp64 fallback draws from p_n
-            p.accept_len[b] = r.n;
-            p.next_token[b] = 0;
-            if (p.dbg_mass) p.dbg_mass[b] = 0.0;
-            if (p.dbg_flags) p.dbg_flags[b] = 2;
-            if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 2);
+            owner[b] = own;
+            tprime[b] = tp;
+            if (own && p.dbg_mass) p.dbg_mass[b] = W;
         }
-        owner[b] = own;
-        tprime[b] = tp;
-        if (own && p.dbg_mass) p.dbg_mass[b] = W;
     }
     __syncthreads();
+    NJ_STAMP(11);
+    // owner CTA: per-tile inclusive scans of its weights (tile-major = vocab
+    // order), fixed-order tile prefix, then the token whose interval [E, I)
+    // holds tp; E(x) = I(x-1) from the same scan values.  If rounding puts tp
+    // past this CTA's recomputed total the draw is clamped and certified.
     if (warp >= 4 && warp < 8) {
         const int q = warp & 3;
         const int et = threadIdx.x - 128;
@@ -407,7 +617,48 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
             if (!own) continue;
             const ReqInfo r = req[b];
             const double tp = tprime[b];
-            const double* cp = &cprefix[b * (kMaxT + 1)];
+            const float* qrow = !r.resid ? nullptr
+                                : qsl + (size_t)(p.q_prefetch ? r.qrow : qslot[b]) * rows_cap;
+            const float c = (float)r.lse_s;
+            const float corr = (float)exp((double)c - r.lse_s);
+            uint32_t a[kMaxT];
+#pragma unroll
+            for (int t = 0; t < kMaxT; ++t)
+                a[t] = lane_base + (uint32_t)((t < ntiles ? t : 0) * NPAD + r.srow);
+            float lv[kMaxT], w[kMaxT], inc[kMaxT];
+            tmem_ld1x16(a, lv);
+#pragma unroll
+            for (int t = 0; t < kMaxT; ++t) {
+                const bool valid = t < ntiles && vr < min(kTileV, rows - t * kTileV);
+                w[t] = sample_weight(lv[t], c, corr, r.resid, qrow, t * kTileV + vr, valid);
+                inc[t] = w[t];
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int t = 0; t < kMaxT; ++t) {
+                    const float y = __shfl_up_sync(0xffffffffu, inc[t], o);
+                    if (lane >= o) inc[t] += y;
+                }
+            }
+            float* wt = &wtile[B * 4];   // [kMaxT][4] quadrant totals (after the phase-3 area)
+            if (lane == 31) {
+#pragma unroll
+                for (int t = 0; t < kMaxT; ++t)
+                    if (t < ntiles) wt[t * 4 + q] = inc[t];
+            }
+            named_bar(1, 128);
+            double* cp = &cprefix[0];
+            if (et == 0) {
+                double acc = 0.0;
+                for (int t = 0; t < ntiles; ++t) {
+                    cp[t] = acc;
+                    acc = acc + ((((double)wt[t * 4] + (double)wt[t * 4 + 1]) + (double)wt[t * 4 + 2]) +
+                                 (double)wt[t * 4 + 3]);
+                }
+                cp[ntiles] = acc;
+            }
+            named_bar(1, 128);
             int tsel = -1;
             bool clamp = (own == 2);
             if (!clamp)
@@ -418,21 +669,19 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
                 for (int t = ntiles - 1; t >= 0; --t)
                     if (cp[t + 1] > cp[t]) { tsel = t; break; }
             }
-            const float l = tmem_ld1(lane_base + (uint32_t)(tsel * NPAD + r.srow));
-            const bool valid = vr < min(kTileV, rows - tsel * kTileV);
-            const int xl = r0 + tsel * kTileV + vr;
-            const float w = sample_weight(l, r.lse_s, r.resid,
-                                          p.q + (int64_t)r.qrow * p.ldq + p.v_begin, xl, valid);
-            const float inc = warp_incl_scan(w);
-            float exc = __shfl_up_sync(0xffffffffu, inc, 1);
+            float wsel = 0.f, isel = 0.f;
+#pragma unroll
+            for (int t = 0; t < kMaxT; ++t)
+                if (t == tsel) { wsel = w[t]; isel = inc[t]; }
+            float exc = __shfl_up_sync(0xffffffffu, isel, 1);
             if (lane == 0) exc = 0.f;
-            const float* wt = &wtile[(b * kMaxT + tsel) * 4];
             double Sq = 0.0;
-            for (int w2 = 0; w2 < q; ++w2) Sq = Sq + (double)wt[w2];
+            for (int w2 = 0; w2 < q; ++w2) Sq = Sq + (double)wt[tsel * 4 + w2];
             const double lo = cp[tsel] + (Sq + (double)exc);   // E(x) = I(x-1)
-            const double hi = cp[tsel] + (Sq + (double)inc);   // I(x)
+            const double hi = cp[tsel] + (Sq + (double)isel);  // I(x)
+            const int xl = r0 + tsel * kTileV + vr;
             if (clamp) {
-                const unsigned mpos = __ballot_sync(0xffffffffu, w > 0.f);
+                const unsigned mpos = __ballot_sync(0xffffffffu, wsel > 0.f);
                 if (lane == 0) spick[q] = mpos ? (31 - __clz((int)mpos)) : -1;
                 named_bar(1, 128);
                 if (et == 0) {
@@ -447,7 +696,7 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
                 named_bar(1, 128);
                 continue;
             }
-            if (w > 0.f && lo <= tp && tp < hi) {   // exactly one lane of the CTA
+            if (wsel > 0.f && lo <= tp && tp < hi) {   // exactly one lane of the CTA
                 p.accept_len[b] = r.n;
                 p.next_token[b] = xl + p.v_begin;
                 if (p.dbg_flags) p.dbg_flags[b] = 0;
@@ -455,9 +704,11 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
                 if (p.certify && (margin <= (double)p.eps_draw || r.flag || p.force_fallback))
                     push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
             }
+            named_bar(1, 128);   // wt / cp reused by the next owned request
         }
     }
     tc_fence_before();
     __syncthreads();
+    NJ_STAMP(12);
     if (warp == 2) tmem_dealloc(tbase, 512);
 }

@@ -268,7 +268,12 @@ struct FusedParams {
     int32_t nbuf, scratch_col;   // scratch accumulators: nbuf x NPAD columns at scratch_col
     int32_t kpd;                 // k-blocks per drained partial (accuracy: 1)
     int32_t kgroup;              // k-blocks per TMA ring stage
-    int32_t f32drain;            // debug: sum partials in fp32 (accuracy experiments only)
+    int32_t ngroups;             // >0: drain handshake per ring stage with ngroups x kgroup scratch buffers
+    unsigned long long* phase_ts; // debug: [grid][8] %globaltimer stamps at phase boundaries (NULL: off)
+    int32_t rows_cap;            // max vocab rows per CTA (q-slice pitch in smem)
+    int32_t q_bytes_cap;         // bytes reserved for q slices at the start of the ring
+    int32_t q_prefetch;          // 1: every draft row's q slice is cp.async'ed before barrier 1
+    int32_t q_vec16;             // q rows 16-byte aligned at CTA starts (16-B cp.async)
     const int32_t* draft_tokens;
     const float* q;
     int64_t ldq;
@@ -279,8 +284,7 @@ struct FusedParams {
     float* part_s;
     double* dl;         // [G] fp64 draft logits
     double* wpart;      // [B][grid]
-    uint32_t* bar_count;
-    uint32_t* bar_gen;
+    uint32_t* bar;      // grid-barrier word
     int32_t* fb_count;  // certified-fallback work list
     int32_t* fb_list;
     int32_t* req_flags; // [B]

@@ -11,6 +11,12 @@
 
 namespace nj {
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -97,6 +103,16 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, ui
           "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+
+// Ampere-style async copies (LDGSTS): fire-and-forget global -> shared.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ------------------------------------------------------------------- tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {  // whole warp
@@ -293,24 +309,32 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen, uint32_t nblocks) {
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Grid-wide barrier over `nblocks` co-resident CTAs on ONE word: block 0 adds
+// 0x80000000 - (nblocks - 1), every other block adds 1, so each completed
+// barrier flips the top bit and leaves the low bits unchanged (state survives
+// relaunches and CUDA-graph replays).  Waiters poll with volatile loads.
+__device__ __forceinline__ void grid_barrier(uint32_t* bar, uint32_t nblocks, unsigned long long* ts = nullptr) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const uint32_t g = ld_acquire_gpu(gen);
+        const uint32_t add = blockIdx.x == 0 ? (0x80000000u - (nblocks - 1u)) : 1u;
+        if (ts) ts[0] = globaltimer();
         __threadfence();
-        if (atomicAdd(count, 1u) == nblocks - 1) {
-            atomicExch(count, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            const long long t0 = clock64();
-            int spins = 0;
-            while (ld_acquire_gpu(gen) == g) {
-                __nanosleep(64);
-                if ((++spins & 255) == 0) watchdog(t0);
-            }
+        if (ts) ts[1] = globaltimer();
+        const uint32_t old = atomicAdd(bar, add);
+        if (ts) ts[2] = globaltimer();
+        const long long t0 = clock64();
+        int spins = 0;
+        while (((old ^ ld_volatile_u32(bar)) & 0x80000000u) == 0u) {
+            if ((++spins & 1023) == 0) watchdog(t0);
         }
+        if (ts) ts[3] = globaltimer();
         __threadfence();
+        if (ts) ts[4] = globaltimer();
     }
     __syncthreads();
 }

@@ -401,7 +401,14 @@ struct FbParams {
 __device__ __forceinline__ float bf16f(uint16_t h) { return __uint_as_float(((uint32_t)h) << 16); }
 
 // FB-A: fp64 logits of every row of every queued request (warp per vocab id).
+// Both fallback kernels are launched with programmatic dependent launch: they
+// are scheduled while the producer kernel still runs and block here until its
+// writes are visible, so an empty queue costs almost no launch latency.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __global__ void __launch_bounds__(256) k_fb_logits(const FbParams p, const ReqMeta m) {
+    pdl_wait();
     const int nfb = __ldcg(p.fb_count);
     if (nfb == 0) return;
     const int lane = (int)lane_id();
@@ -466,6 +473,7 @@ __device__ double row_lse_d(const LT* row, int V, double* sh) {
 // FB-B: block per queued request.  fp64 lse, acceptance, residual / bonus,
 // inverse CDF (block scan, ascending id) -- the plain definition.
 __global__ void __launch_bounds__(256) k_fb_decide(const FbParams p, const ReqMeta m) {
+    pdl_wait();
     const int nfb = __ldcg(p.fb_count);
     __shared__ double sh[32];
     __shared__ double lse[32];
