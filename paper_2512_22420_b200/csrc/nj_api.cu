@@ -114,10 +114,10 @@ struct nj_ctx {
     int64_t prof_n = 0;
     unsigned long long* phase_ts = nullptr;   // debug (NJ_PHASE_TS=1)
     // certificate margins: fused path logits err <= 6e-7 (ln p);
-    // two-pass path (plain tcgen05 accumulation) err <= 8e-5 (lse)
+    // two-pass path (restarted accumulators, fp32 RN running sums) ln p err ~1e-6
     float eps_acc_fused = 2e-6f, eps_draw_fused = 0.f;
-    float eps_acc = 2e-4f;
-    float eps_draw = 1.5e-5f;
+    float eps_acc = 4e-6f;
+    float eps_draw = 0.f;
     std::string err;
     // workspace
     std::vector<void*> allocs;
@@ -352,6 +352,31 @@ nj_status launch_gemm_rows(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R,
     return NJ_OK;
 }
 
+// k_gemm_acc launcher (two-pass path): accurate LM-head GEMM over R contiguous rows
+template <bool WRITE, bool STATS, bool CAPTURE>
+nj_status launch_gemm_acc(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, GemmAccParams gp) {
+    if (R <= 0) return NJ_OK;
+    CUtensorMap tmH;
+    if (!encode_2d(&tmH, h, R, c->cfg.d, kAccT)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
+    gp.R = R;
+    gp.nchunks = (R + kAccT - 1) / kAccT;
+    gp.V_local = c->V_local;
+    gp.U = c->U;
+    gp.num_kb = (c->cfg.d + kBK - 1) / kBK;
+    gp.v_begin = c->cfg.v_begin;
+    gp.part_ld = c->grid;
+    const size_t stage = (size_t)kAccGK * (kTileBytesA + kAccT * 128);
+    size_t tail = 2 * 4 * kAccNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
+    tail = align_up(tail, 8) + (2 * 8 + 4) * 8 + 8;
+    const int S = (int)std::min<size_t>(4, (kSmemLimit - tail - 1024) / stage);
+    if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_acc: not enough shared memory (R=%d)", R);
+    gp.nstages = S;
+    const size_t smem = (size_t)S * stage + tail;
+    k_gemm_acc<WRITE, STATS, CAPTURE><<<c->grid, kAccThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
+    NJ_LAUNCHED(c, "k_gemm_acc", st);
+    return NJ_OK;
+}
+
 FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const int32_t* tok, const float* q,
                    int64_t ldq, const float* u, int32_t* acc, int32_t* nxt, const nj_debug* dbg) {
     FbParams f{};
@@ -481,6 +506,8 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_gemm_rows<true, false, false>);
     e = e ? e : set_smem_attr(k_gemm_rows<false, true, true>);
     e = e ? e : set_smem_attr(k_gemm_rows<true, true, false>);
+    e = e ? e : set_smem_attr(k_gemm_acc<false, true, true>);
+    e = e ? e : set_smem_attr(k_gemm_acc<true, true, false>);
     if (e != cudaSuccess) {
         nj_destroy(c);
         return set_err(nullptr, NJ_ECUDA, "cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
@@ -600,14 +627,14 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             NJ_LAUNCHED(c, "k_gather_drafts", st);
             for (int r0 = 0; r0 < pl.G; r0 += kMaxStatRows) {
                 const int R = std::min(kMaxStatRows, pl.G - r0);
-                GemmRowsParams gp{};
+                GemmAccParams gp{};
                 gp.part_m = c->part_m + (size_t)r0 * c->grid;
                 gp.part_s = c->part_s + (size_t)r0 * c->grid;
                 gp.tok = draft_tokens + r0;
                 gp.dl = c->dl + r0;
                 std::pair<cudaEvent_t, cudaEvent_t> ev;
                 if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
-                if ((s = launch_gemm_rows<false, true, true>(c, st, c->hd + (size_t)r0 * c->cfg.d, R, gp)) != NJ_OK)
+                if ((s = launch_gemm_acc<false, true, true>(c, st, c->hd + (size_t)r0 * c->cfg.d, R, gp)) != NJ_OK)
                     return s;
                 if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
             }
@@ -625,10 +652,10 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         NJ_LAUNCHED(c, "k_accept", st);
         // K-C: sample-row GEMM -> fp32 logits [B, V_local] + stats (bonus-row lse)
         {
-            GemmRowsParams gp{};
+            GemmAccParams gp{};
             gp.logits = c->logits_s; gp.ld_out = c->V_local;
             gp.part_m = c->part2_m; gp.part_s = c->part2_s;
-            if ((s = launch_gemm_rows<true, true, false>(c, st, c->hs, pl.B, gp)) != NJ_OK) return s;
+            if ((s = launch_gemm_acc<true, true, false>(c, st, c->hs, pl.B, gp)) != NJ_OK) return s;
         }
         // K-D: residual / bonus masses and the inverse-CDF draw
         MassParams mp{};
