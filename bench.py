@@ -182,7 +182,7 @@ def bench_nj(args, ws, rank, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     B, gamma, path = CONFIGS[args.config]
-    path = {"auto": NJ_PATH_AUTO, "fused": NJ_PATH_FUSED, "twopass": NJ_PATH_TWOPASS}[args.path or path]
+    path = PATH_NAMES.index(args.path or path)
     W = make_weight(V_Q, D_Q, args.seed, dev)
     nb = 4   # rotate independent batches (each rank its own seeds)
     batches = [make_batch(B, gamma, V=V_Q, d=D_Q, seed=args.seed * 1000 + rank * 16 + i, device=dev, W=W)
@@ -308,6 +308,128 @@ def bench_nj(args, ws, rank, local):
         dist.destroy_process_group()
 
 
+def bench_c4(args, ws, rank, local):
+    """BASELINE configs[3]: Nightjar-driven trace.  B_t follows a synthetic QPS
+    ramp 5 -> 300 -> 5 (fig:trace1 shape); gamma_t = nj_select_gamma
+    (Algorithm 1 + Eq. 3, Table 1 c_prefill scaled by --cprefill-scale); every
+    step runs nj_verify on the first B_t requests of a pre-generated pool with
+    gamma_t drafts each, is timed with CUDA events, and feeds the realised
+    goodput sum(n_b + 1) / t_step back through nj_observe."""
+    import numpy as np
+    import torch
+
+    from paper_2512_22420_b200 import Bandit, Verifier
+    from synth.inputs import make_batch, make_weight, qps_ramp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    BMAX, GMAX = 256, 5
+    W = make_weight(V_Q, D_Q, args.seed, dev)
+    pools = {g: make_batch(BMAX, g, V=V_Q, d=D_Q, seed=args.seed * 100 + g, device=dev, W=W) for g in range(GMAX + 1)}
+    v = Verifier(D_Q, V_Q, max_batch=BMAX, gamma_max=GMAX, device=local)
+    tab = os.path.join(ROOT, "tests", "golden", "table1_cprefill.csv")
+    rows = [l.strip().split(",") for l in open(tab) if l[0].isdigit()]
+    L = sorted({int(r[0]) for r in rows})
+    Bb = sorted({int(r[1]) for r in rows})
+    C = np.zeros((len(L), len(Bb)))
+    for r in rows:
+        C[L.index(int(r[0])), Bb.index(int(r[1]))] = float(r[2]) * args.cprefill_scale
+    bandit = Bandit(GMAX, BMAX, args.seed, L, Bb, C)
+    trace = qps_ramp(args.trace_steps, seed=args.seed)
+    acc = torch.empty(BMAX, dtype=torch.int32, device=dev)
+    nxt = torch.empty(BMAX, dtype=torch.int32, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lag, tok_tot, t_tot, pos_tot = 0, 0, 0.0, 0
+    hist = {}
+    sel_us = []
+    for t, B in enumerate(trace):
+        B = int(B)
+        t0 = time.perf_counter()
+        g = bandit.select(B, lag if bandit.last_gamma == 0 else 0)
+        sel_us.append((time.perf_counter() - t0) * 1e6)
+        b = pools[g]
+        n_rows, n_dr = B * (g + 1), B * g
+        gam = np.full(B, g, np.int32)
+        e0.record()
+        v.verify(b.hidden[:n_rows], W, b.draft_tokens[:max(n_dr, 0)], b.draft_probs[:max(n_dr, 1)], gam,
+                 b.uniforms[:n_rows], acc, nxt)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        toks = int((acc[:B] + 1).sum().item())
+        bandit.observe(B, g, toks / (ms / 1e3))
+        lag = lag + 1 if g == 0 else 0
+        if t >= args.warmup:
+            tok_tot += toks
+            pos_tot += n_rows
+            t_tot += ms / 1e3
+            key = f"B{(B - 1) // 32 * 32 + 1}-{(B - 1) // 32 * 32 + 32}"
+            hist.setdefault(key, [0] * (GMAX + 1))[g] += 1
+    line = {"metric": "accepted tokens/s (bandit-driven trace)", "value": tok_tot / t_tot, "unit": "tokens/s",
+            "n_gpus": 1, "steps": len(trace) - args.warmup, "warmup": args.warmup,
+            "ms_per_step": t_tot / (len(trace) - args.warmup) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "qwen7b_c4_nightjar_trace", "qps": "5->300->5 linear ramp",
+                       "batch_max": BMAX, "gamma_max": GMAX, "cprefill_scale": args.cprefill_scale},
+            "verified_positions_per_s": pos_tot / t_tot,
+            "gamma_histogram_per_B": hist,
+            "select_gamma_us_median": statistics.median(sel_us),
+            "bandit_snapshot_batches": len(bandit.snapshot()["batches"])}
+    print(json.dumps(line), flush=True)
+
+
+PATH_NAMES = ["auto", "fused", "twopass", "staged"]
+
+
+def bench_sweep(args, ws, rank, local):
+    """BASELINE configs[2]: B x gamma sweep (C3); one JSON line per point."""
+    import torch
+
+    from paper_2512_22420_b200 import NJ_OPT_PATH, NJ_OPT_PROFILE, Verifier
+    from synth.inputs import make_batch, make_weight
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    W = make_weight(V_Q, D_Q, args.seed, dev)
+    hbm, tf_burst, _, _ = load_peaks()
+    Bs = [int(x) for x in args.sweep_B.split(",")]
+    Gs = [x if x.startswith("mixed") else int(x) for x in args.sweep_gamma.split(",")]
+    for g in Gs:
+        for B in Bs:
+            b = make_batch(B, g, V=V_Q, d=D_Q, seed=args.seed + B, device=dev, W=W)
+            v = Verifier(D_Q, V_Q, max_batch=B, gamma_max=5, device=local)
+            if args.path:
+                v.set_option(NJ_OPT_PATH, PATH_NAMES.index(args.path))
+            try:
+                path, launches = v.plan(b.gamma)
+            except Exception as e:   # forced path not applicable at this point
+                print(json.dumps({"config": f"B{B}_g{g}", "skipped": str(e)}), flush=True)
+                continue
+            acc = torch.empty(B, dtype=torch.int32, device=dev)
+            nxt = torch.empty(B, dtype=torch.int32, device=dev)
+            for _ in range(3):
+                v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            v.set_option(NJ_OPT_PROFILE, 1)
+            v.kernel_time(True)
+            e0.record()
+            for _ in range(args.steps):
+                v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            kms, kn = v.kernel_time(True)
+            toks = int((acc + 1).sum().item())
+            N = b.N
+            t_star = max(2.0 * N * V_Q * D_Q / (tf_burst * 1e12), (2.0 * V_Q * D_Q + 2 * N * D_Q) / (hbm * 1e9))
+            print(json.dumps({"config": f"B{B}_g{g}", "B": B, "gamma": g, "N": N, "path": PATH_NAMES[path],
+                              "us_per_step": ms * 1e3, "positions_per_s": N / (ms / 1e3),
+                              "accepted_tokens_per_s": toks / (ms / 1e3), "roofline_us": t_star * 1e6,
+                              "frac_of_roofline": t_star / (ms / 1e3), "dominant_kernel_us": kms / max(kn, 1) * 1e3,
+                              "launches": launches}), flush=True)
+            del v
+
+
 def _cpu_batch(b):
     import torch
     from synth.inputs import Batch
@@ -320,14 +442,25 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="nj", choices=["nj", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--path", default=None, choices=[None, "auto", "fused", "twopass"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4"])
+    ap.add_argument("--path", default=None, choices=[None] + PATH_NAMES)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--sweep", action="store_true", help="C3 grid: one JSON line per (B, gamma) point")
+    ap.add_argument("--sweep-B", default="1,2,4,8,16,32,48,64,96,128,192,256")
+    ap.add_argument("--sweep-gamma", default="0,1,2,3,4,5,mixed:5")
+    ap.add_argument("--trace-steps", type=int, default=1200)
+    ap.add_argument("--cprefill-scale", type=float, default=0.01)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_setup()
+    if args.sweep:
+        bench_sweep(args, ws, rank, local)
+        return
+    if args.config == "c4":
+        bench_c4(args, ws, rank, local)
+        return
     if args.impl == "reference":
         bench_reference(args, ws, rank)
     else:

@@ -145,8 +145,11 @@ nj_status nj_verify_host(nj_ctx* ctx, void* stream,
 typedef enum {
     NJ_PATH_AUTO = 0,    /* pick by size            */
     NJ_PATH_FUSED = 1,   /* one persistent kernel, logits resident in TMEM       */
-    NJ_PATH_TWOPASS = 2  /* stats GEMM over drafts, accept, sample-row GEMM,     */
+    NJ_PATH_TWOPASS = 2, /* stats GEMM over drafts, accept, sample-row GEMM,     */
                          /* sampler kernels                                      */
+    NJ_PATH_STAGED = 3   /* N <= 256: ONE GEMM pass over all N rows whose fp32   */
+                         /* logits are staged in L2 (evict_last stores), accept, */
+                         /* sampler kernels reading the B sample rows            */
 } nj_path;
 
 typedef enum {

@@ -20,7 +20,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libnj.so")
 
 NJ_OK, NJ_EINVAL, NJ_ESHAPE, NJ_ECUDA, NJ_ENCCL, NJ_ENOMEM, NJ_EUNSUPPORTED = range(7)
-NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_TWOPASS = 0, 1, 2
+NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_TWOPASS, NJ_PATH_STAGED = 0, 1, 2, 3
 NJ_OPT_PATH, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PROFILE = 1, 2, 3, 4
 NJ_FLAG_FALLBACK, NJ_FLAG_ZERO_MASS, NJ_FLAG_CLAMP = 1, 2, 4
 

@@ -60,6 +60,8 @@ bool encode_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t d, int bo
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+constexpr int kStagedMaxN = kAccMaxRowG;   // staged path: rows of one GEMM pass (2 token chunks)
+
 inline int round16(int x) { return (x + 15) & ~15; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -126,10 +128,12 @@ struct nj_ctx {
     double *wpart = nullptr, *s_lse = nullptr, *cmass = nullptr, *fb_logits = nullptr, *lse_tmp = nullptr;
     uint16_t *hd = nullptr, *hs = nullptr;
     float* logits_s = nullptr;
+    float* logits_st = nullptr;    // staged path: [min(Nmax, kStagedMaxN)][V_local]
     int32_t *s_resid = nullptr, *s_qrow = nullptr;
     int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
     uint32_t* bar = nullptr;       // count, gen
     int32_t* scratch_i = nullptr;  // [MB]
+    int32_t* s_row = nullptr;      // [MB] staged path: sample row of each request
     // host-API staging (lazy)
     uint16_t* st_hidden = nullptr;
     int32_t* st_tok = nullptr;
@@ -226,10 +230,13 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
     pl.npad = round16(pl.N);
     const bool fused_ok = pl.N <= kFusedMaxN && c->max_tiles <= 16 && (c->max_tiles + 1) * pl.npad <= 512 &&
                           c->cfg.nccl_comm == nullptr;
+    const bool staged_ok = pl.N <= kStagedMaxN && c->logits_st != nullptr;
     int path = c->path_opt;
-    if (path == NJ_PATH_AUTO) path = fused_ok ? NJ_PATH_FUSED : NJ_PATH_TWOPASS;
+    if (path == NJ_PATH_AUTO) path = fused_ok ? NJ_PATH_FUSED : staged_ok ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
         return set_err(c, NJ_EUNSUPPORTED, "fused path needs N <= %d and TMEM room (N=%d)", kFusedMaxN, pl.N);
+    if (path == NJ_PATH_STAGED && !staged_ok)
+        return set_err(c, NJ_EUNSUPPORTED, "staged path needs N <= %d (N=%d)", kStagedMaxN, pl.N);
     pl.path = path;
     return NJ_OK;
 }
@@ -488,11 +495,13 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     A(hd, (size_t)c->Gmax * cfg->d);
     A(hs, (size_t)MB * cfg->d);
     A(logits_s, (size_t)MB * c->V_local);
+    A(logits_st, (size_t)std::min(c->Nmax, kStagedMaxN) * c->V_local);
     A(s_resid, (size_t)MB);
     A(s_qrow, (size_t)MB);
     A(fb_block, (size_t)1 + 2 * MB);
     A(bar, 2);
     A(scratch_i, (size_t)MB);
+    A(s_row, (size_t)MB);
 #undef A
     if (cudaMemset(c->bar, 0, 2 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMemset(c->fb_block, 0, (1 + 2 * MB) * sizeof(int32_t)) != cudaSuccess) {
@@ -508,6 +517,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_gemm_rows<true, true, false>);
     e = e ? e : set_smem_attr(k_gemm_acc<false, true, true>);
     e = e ? e : set_smem_attr(k_gemm_acc<true, true, false>);
+    e = e ? e : set_smem_attr(k_gemm_acc<true, true, true>);
     if (e != cudaSuccess) {
         nj_destroy(c);
         return set_err(nullptr, NJ_ECUDA, "cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
@@ -530,7 +540,7 @@ nj_status nj_set_option(nj_ctx* c, nj_option opt, int64_t v) {
     if (!c) return NJ_EINVAL;
     switch (opt) {
         case NJ_OPT_PATH:
-            if (v < NJ_PATH_AUTO || v > NJ_PATH_TWOPASS) return set_err(c, NJ_EINVAL, "bad path %lld", (long long)v);
+            if (v < NJ_PATH_AUTO || v > NJ_PATH_STAGED) return set_err(c, NJ_EINVAL, "bad path %lld", (long long)v);
             c->path_opt = (int)v;
             return NJ_OK;
         case NJ_OPT_CERTIFY: c->certify = v != 0; return NJ_OK;
@@ -570,6 +580,7 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
     if (s != NJ_OK) return s;
     int n = 0;
     if (pl.path == NJ_PATH_FUSED) n = 1;
+    else if (pl.path == NJ_PATH_STAGED) n = 4;   // GEMM, accept, mass, locate
     else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) : 0) + 4;   // gather+KA, KB, KC, KD1, KD2
     if (c->certify) n += 2;
     if (path_out) *path_out = pl.path;
@@ -618,6 +629,51 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         else if (pl.npad == 32) s = launch_fused<32>(c, st, pl, tmH, fp);
         else s = launch_fused<48>(c, st, pl, tmH, fp);
         if (s != NJ_OK) return s;
+    } else if (pl.path == NJ_PATH_STAGED) {
+        // one GEMM pass over all N rows: per-row stats, draft-logit capture, and every
+        // row's fp32 logits stored with an L2 evict_last policy (W streams evict_first)
+        NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
+        if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
+        GemmAccParams gp{};
+        gp.logits = c->logits_st; gp.ld_out = c->V_local;
+        gp.part_m = c->part_m; gp.part_s = c->part_s;
+        gp.tok = draft_tokens; gp.dl = c->dl;
+        gp.use_row_g = 1;
+        gp.w_evict_first = pl.N <= kAccT ? 1 : 0;
+        if (const char* e = getenv("NJ_W_EVICT_FIRST")) gp.w_evict_first = atoi(e);
+        for (int b = 0; b < pl.B; ++b)
+            for (int r = pl.row_off[b]; r < pl.row_off[b + 1]; ++r)
+                gp.row_g[r] = r + 1 < pl.row_off[b + 1] ? r - b : -1;
+        std::pair<cudaEvent_t, cudaEvent_t> ev;
+        if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
+        if ((s = launch_gemm_acc<true, true, true>(c, st, hidden, pl.N, gp)) != NJ_OK) return s;
+        if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
+        AcceptParams ap{};
+        ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = c->grid; ap.dl = c->dl;
+        ap.draft_tokens = draft_tokens; ap.q = draft_probs; ap.ldq = ldq; ap.u = uniforms;
+        ap.hidden = hidden; ap.d = c->cfg.d; ap.hs = nullptr;
+        ap.accept_len = accept_len; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
+        ap.fb_count = c->fb_count(); ap.fb_list = c->fb_list(); ap.req_flags = c->req_flags();
+        ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
+        ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc;
+        ap.staged = 1; ap.s_row = c->s_row;
+        k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
+        NJ_LAUNCHED(c, "k_accept", st);
+        MassParams mp{};
+        mp.logits = c->logits_st; mp.ld = c->V_local; mp.s_row = c->s_row;
+        mp.V_local = c->V_local; mp.v_begin = c->cfg.v_begin;
+        mp.nchunks = c->nchunks; mp.s_resid = c->s_resid; mp.s_qrow = c->s_qrow; mp.s_lse = c->s_lse;
+        mp.part2_m = c->part_m; mp.part2_s = c->part_s; mp.grid2 = c->grid;
+        mp.q = draft_probs; mp.ldq = ldq; mp.u = uniforms; mp.stage_mode = 0; mp.cmass = c->cmass;
+        mp.accept_len = accept_len; mp.next_token = next_token;
+        mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
+        mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
+        mp.dbg_lse = dbg ? dbg->lse : nullptr;
+        mp.certify = certify; mp.eps_draw = c->eps_draw;
+        k_mass<<<dim3(c->nchunks, pl.B), kSampThreads, 0, st>>>(mp);
+        NJ_LAUNCHED(c, "k_mass", st);
+        k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
+        NJ_LAUNCHED(c, "k_locate", st);
     } else {
         NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
         if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));

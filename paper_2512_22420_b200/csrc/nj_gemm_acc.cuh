@@ -21,6 +21,7 @@ constexpr int kAccThreads = 384;
 constexpr int kAccT = 128;        // token chunk (MMA N)
 constexpr int kAccGK = 2;         // k-blocks per ring stage
 constexpr int kAccNC = 64;        // columns per epilogue warp
+constexpr int kAccMaxRowG = 256;  // staged path: rows mapped to draft indices (by value)
 
 struct GemmAccParams {
     int32_t R, nchunks;
@@ -30,8 +31,11 @@ struct GemmAccParams {
     float* part_m;          // [R][part_ld]
     float* part_s;
     int32_t part_ld;
-    const int32_t* tok;     // [R] global token ids (CAPTURE)
-    double* dl;             // [R]
+    const int32_t* tok;     // [R] global token ids (CAPTURE), or with row_g: draft_tokens
+    double* dl;             // [R] (or [G] with row_g)
+    int32_t w_evict_first;  // single chunk: W is streamed once, keep L2 for the staged logits
+    int32_t use_row_g;      // staged path: row r is draft row_g[r] (-1: bonus row)
+    int32_t row_g[kAccMaxRowG];
 };
 
 template <bool WRITE, bool STATS, bool CAPTURE>
@@ -75,7 +79,10 @@ k_gemm_acc(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
     if (STATS)
         for (int i = threadIdx.x; i < p.R; i += kAccThreads) state[i] = make_float2(-INFINITY, 0.f);
     if (CAPTURE)
-        for (int i = threadIdx.x; i < p.R; i += kAccThreads) stok[i] = p.tok[i] - p.v_begin;
+        for (int i = threadIdx.x; i < p.R; i += kAccThreads) {
+            if (p.use_row_g) stok[i] = p.row_g[i] >= 0 ? p.tok[p.row_g[i]] - p.v_begin : -1;
+            else stok[i] = p.tok[i] - p.v_begin;
+        }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -83,7 +90,8 @@ k_gemm_acc(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
 
     if (warp == 0 && lane == 0) {
         // ------------------------------------------------ TMA producer
-        const uint64_t pol_w = policy_evict_last();    // a W tile is re-read for every chunk
+        // a W tile is re-read for every chunk (evict_last), unless there is one chunk
+        const uint64_t pol_w = p.w_evict_first ? policy_evict_first() : policy_evict_last();
         const uint64_t pol_h = policy_evict_last();
         int s = 0;
         uint32_t ph = 0;
@@ -137,6 +145,7 @@ k_gemm_acc(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         const int e = (warp - 4) >> 2;   // column half
         const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(e * kAccNC);
         const int vr = q * 32 + lane;
+        const uint64_t pol_keep = policy_evict_last();   // staged logits stay in L2 for the sampler
         int grp = 0;
         uint32_t gph = 0;
         for (int it = 0; it < nitems; ++it) {
@@ -171,8 +180,8 @@ k_gemm_acc(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 const int col = e * kAccNC + j;
                 if (col < ncol) {
                     const int row = c0 + col;
-                    if (WRITE && valid) p.logits[(int64_t)row * p.ld_out + xl] = acc[j];
-                    if (CAPTURE && valid && stok[row] == xl) p.dl[row] = (double)acc[j];
+                    if (WRITE && valid) st_evict_last(&p.logits[(int64_t)row * p.ld_out + xl], acc[j], pol_keep);
+                    if (CAPTURE && valid && stok[row] == xl) p.dl[p.use_row_g ? p.row_g[row] : row] = (double)acc[j];
                 }
             }
             if (STATS) {

@@ -103,6 +103,10 @@ struct AcceptParams {
     float* dbg_pdraft;
     int32_t certify, force_fallback;
     float eps_acc;
+    // staged path: stats are per ROW (part index = row, not draft index), every
+    // row's logits are staged, so no hidden-row copy; s_row[b] = sample row
+    int32_t staged;
+    int32_t* s_row;
 };
 
 // K-B: warp per request — lse of its draft rows, acceptance tests, first
@@ -116,7 +120,7 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
     double lse_n = __longlong_as_double(0x7ff8000000000000ll);
     for (int i = 0; i < gam; ++i) {
         const int g = g0 + i;
-        const double lse = warp_lse(p.part_m, p.part_s, p.grid, g, p.grid);
+        const double lse = warp_lse(p.part_m, p.part_s, p.grid, p.staged ? ro + i : g, p.grid);
         const double pd = exp(__ldcg(&p.dl[g]) - lse);
         const double qx = (double)p.q[(int64_t)g * p.ldq + p.draft_tokens[g]];
         const double uq = (double)p.u[ro + i] * qx;
@@ -130,14 +134,19 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
     // remaining drafts (untested) still get debug values
     for (int i = n + 1; i < gam && p.dbg_pdraft; ++i) {
         const int g = g0 + i;
-        const double lse = warp_lse(p.part_m, p.part_s, p.grid, g, p.grid);
+        const double lse = warp_lse(p.part_m, p.part_s, p.grid, p.staged ? ro + i : g, p.grid);
         if (lane == 0) {
             if (p.dbg_lse) p.dbg_lse[ro + i] = (float)lse;
             p.dbg_pdraft[g] = (float)exp(__ldcg(&p.dl[g]) - lse);
         }
     }
-    copy_row(p.hs + (int64_t)b * p.d, p.hidden + (int64_t)(ro + n) * p.d, p.d, lane, 32);
+    if (p.staged) {
+        if (n == gam) lse_n = warp_lse(p.part_m, p.part_s, p.grid, ro + gam, p.grid);   // bonus row
+    } else {
+        copy_row(p.hs + (int64_t)b * p.d, p.hidden + (int64_t)(ro + n) * p.d, p.d, lane, 32);
+    }
     if (lane == 0) {
+        if (p.staged) p.s_row[b] = ro + n;
         p.accept_len[b] = n;
         p.s_resid[b] = n < gam;
         p.s_qrow[b] = g0 + n;
@@ -176,8 +185,9 @@ constexpr int kSubTiles = 16;                         // chunk = 16 sub-tiles of
 constexpr int kChunk = kSampThreads * kSubTiles;      // 4096 vocab ids per chunk
 
 struct MassParams {
-    const float* logits;   // [B][ld] local vocab
+    const float* logits;   // [B][ld] local vocab (or [N][ld] with s_row)
     int64_t ld;
+    const int32_t* s_row;  // staged path: logits row of request b (NULL: row b)
     int32_t V_local, v_begin, nchunks;
     const int32_t* s_resid;
     const int32_t* s_qrow;
@@ -217,11 +227,14 @@ __device__ __forceinline__ double sample_lse(const MassParams& p, int b) {
 }
 
 // weights of sub-tile s of chunk c for this thread (one element per thread)
-__device__ __forceinline__ float chunk_weight(const MassParams& p, int b, int c, int s, float lsef, bool resid,
-                                              const float* qrow) {
+__device__ __forceinline__ const float* logits_row(const MassParams& p, int b) {
+    return p.logits + (int64_t)(p.s_row ? p.s_row[b] : b) * p.ld;
+}
+__device__ __forceinline__ float chunk_weight(const MassParams& p, const float* lrow, int c, int s, float lsef,
+                                              bool resid, const float* qrow) {
     const int x = c * kChunk + s * kSampThreads + (int)threadIdx.x;
     if (x >= p.V_local) return 0.f;
-    const float pe = __expf(__ldcg(&p.logits[(int64_t)b * p.ld + x]) - lsef);
+    const float pe = __expf(__ldcg(&lrow[x]) - lsef);
     return resid ? fmaxf(pe - __ldg(&qrow[x]), 0.f) : pe;
 }
 
@@ -239,10 +252,11 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p) {
     const float lsef = (float)lse;
     const bool resid = p.s_resid[b] != 0;
     const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
+    const float* lrow = logits_row(p, b);
     __shared__ float wt[kSubTiles][8];
     float w[kSubTiles];
 #pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, b, c, s, lsef, resid, qrow);
+    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, lrow, c, s, lsef, resid, qrow);
 #pragma unroll
     for (int s = 0; s < kSubTiles; ++s) {
         float inc;
@@ -267,6 +281,7 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     const float lsef = (float)lse;
     const bool resid = p.s_resid[b] != 0;
     const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
+    const float* lrow = logits_row(p, b);
     __shared__ double sh[4];
     __shared__ int shi[4];
     __shared__ float wt[kSubTiles][8];
@@ -308,7 +323,7 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     const double tp = sh[0];
     float w[kSubTiles], inc[kSubTiles];
 #pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, b, c, s, lsef, resid, qrow);
+    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, lrow, c, s, lsef, resid, qrow);
 #pragma unroll
     for (int s = 0; s < kSubTiles; ++s) subtile_scan(w[s], inc[s], wt[s]);
     __syncthreads();

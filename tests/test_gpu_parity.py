@@ -15,7 +15,7 @@ import torch
 import oracle
 from oracle import bruteforce
 from paper_2512_22420_b200 import (NJ_FLAG_FALLBACK, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PATH,
-                                   NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_TWOPASS, NJError, Verifier)
+                                   NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_STAGED, NJ_PATH_TWOPASS, NJError, Verifier)
 from synth.inputs import dyadic_rows, make_batch, make_sampler_case, make_weight
 
 pytestmark = pytest.mark.gpu
@@ -182,13 +182,42 @@ def test_twopass_toy_and_c2():
 def test_twopass_c3_large_batch_sampled():
     """C3 full size (B=64, mixed gamma): all requests against the oracle."""
     b = make_batch(64, "mixed:5", V=QV, d=QD, seed=5, device=DEV, W=w_full())
-    acc, nxt, dd, _ = run(b)
+    acc, nxt, dd, _ = run(b, NJ_PATH_TWOPASS)
     check(b, acc, nxt, dd)
+
+
+def test_twopass_above_staged_limit():
+    """N > 256 (AUTO picks two-pass): B=80, gamma=3 -> N=320, 3 token chunks."""
+    b = make_batch(80, 3, V=QV, d=QD, seed=31, device=DEV, W=w_full())
+    acc, nxt, dd, v = run(b)
+    assert v.plan(b.gamma)[0] == NJ_PATH_TWOPASS
+    check(b, acc, nxt, dd)
+
+
+# ----------------------------------------------------------------- staged path (48 < N <= 256)
+@pytest.mark.parametrize("B,g,V,d", [(1, 3, 32, 16), (20, "mixed:5", 8192, 512), (40, "mixed:5", 8192, 512),
+                                     (64, 3, 1000, 64), (9, 5, 777, 40), (60, 0, 4096, 128)])
+def test_staged_small(B, g, V, d):
+    for seed in range(2):
+        b = make_batch(B, g, V=V, d=d, seed=seed + 3, device=DEV, q_vocab=max(1, V - 5))
+        acc, nxt, dd, _ = run(b, NJ_PATH_STAGED)
+        check(b, acc, nxt, dd, lse_tol=1e-4)
+
+
+@pytest.mark.parametrize("B,g", [(16, 3), (32, 3), (64, 3), (256, 0), (50, "mixed:5")])
+def test_staged_full_size(B, g):
+    """C3 points in the memory-bound band at the Qwen shape, every request vs the oracle."""
+    b = make_batch(B, g, V=QV, d=QD, seed=B + 17, device=DEV, W=w_full())
+    if b.N > 256:
+        pytest.skip("staged path is N <= 256")
+    acc, nxt, dd, v = run(b)
+    assert v.plan(b.gamma)[0] == (NJ_PATH_FUSED if b.N <= 48 else NJ_PATH_STAGED)
+    check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
 
 
 # ----------------------------------------------------------------- fallback, stage, host API
 def test_forced_fp64_fallback_matches_oracle():
-    for path in (NJ_PATH_FUSED, NJ_PATH_TWOPASS):
+    for path in (NJ_PATH_FUSED, NJ_PATH_TWOPASS, NJ_PATH_STAGED):
         b = make_batch(4, "mixed:3", V=2048, d=64, seed=21, device=DEV)
         acc, nxt, dd, _ = run(b, path, force_fb=True)
         check(b, acc, nxt, dd)
