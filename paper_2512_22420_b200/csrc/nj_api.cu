@@ -101,6 +101,9 @@ struct nj_ctx {
     int V_local = 0;
     int num_sms = 0;
     int grid = 0;       // persistent grid (CTAs)
+    int pld = 0;        // row stride of the per-CTA softmax partials (>= every GEMM grid)
+    int gemm_ks = 4;    // k_gemm_big: k-blocks per accumulator restart
+    int gemm_acc = 0;   // 1: use the per-k-block-restart k_gemm_acc instead (A/B, NJ_GEMM=acc)
     int U = 0;          // 16-row vocab units
     int max_tiles = 0;  // max 128-row tiles per CTA
     int nchunks = 0;    // sampler chunks
@@ -117,9 +120,9 @@ struct nj_ctx {
     unsigned long long* phase_ts = nullptr;   // debug (NJ_PHASE_TS=1)
     // certificate margins: fused path logits err <= 6e-7 (ln p);
     // two-pass path (restarted accumulators, fp32 RN running sums) ln p err ~1e-6
-    float eps_acc_fused = 2e-6f, eps_draw_fused = 0.f;
-    float eps_acc = 4e-6f;
-    float eps_draw = 0.f;
+    float eps_acc_fused = 2e-6f, eps_draw_fused = 2e-6f;
+    float eps_acc = 1e-5f;     // k_gemm_big (restart every 4 k-blocks): |d ln p| <= 3.7e-6 measured
+    float eps_draw = 1e-5f;    // mass units: sum_x |d w(x)| <= max|d ln p|
     std::string err;
     // workspace
     std::vector<void*> allocs;
@@ -371,7 +374,7 @@ nj_status launch_gemm_acc(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, 
     gp.U = c->U;
     gp.num_kb = (c->cfg.d + kBK - 1) / kBK;
     gp.v_begin = c->cfg.v_begin;
-    gp.part_ld = c->grid;
+    gp.part_ld = c->pld;
     const size_t stage = (size_t)kAccGK * (kTileBytesA + kAccT * 128);
     size_t tail = 2 * 4 * kAccNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 4) * 8 + 8;
@@ -381,6 +384,56 @@ nj_status launch_gemm_acc(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, 
     const size_t smem = (size_t)S * stage + tail;
     k_gemm_acc<WRITE, STATS, CAPTURE><<<c->grid, kAccThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
     NJ_LAUNCHED(c, "k_gemm_acc", st);
+    return NJ_OK;
+}
+
+
+// LM-head GEMM of the staged / two-pass paths over R contiguous rows of h.
+// k_gemm_big (default) or, with NJ_GEMM=acc, the per-k-block-restart
+// k_gemm_acc (A/B only).  rr: deal (tile, chunk) items round-robin over
+// grid_rr = min(SMs, tiles) CTAs (forced on by the caller when several
+// launches must share one partial layout); otherwise the tile-balanced
+// vocab split over c->grid.  *grid_used = CTAs that wrote partials.
+template <bool WRITE, bool STATS, bool CAPTURE>
+nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, const GemmBigParams& in, bool rr,
+                        int* grid_used) {
+    if (R <= 0) return NJ_OK;
+    if (c->gemm_acc) {
+        if (rr) return set_err(c, NJ_EUNSUPPORTED, "NJ_GEMM=acc: no round-robin mode");
+        GemmAccParams gp{};
+        gp.logits = in.logits; gp.ld_out = in.ld_out; gp.part_m = in.part_m; gp.part_s = in.part_s;
+        gp.tok = in.tok; gp.dl = in.dl; gp.w_evict_first = in.w_evict_first; gp.use_row_g = in.use_row_g;
+        for (int i = 0; i < kAccMaxRowG && i < kBigMaxRowG; ++i) gp.row_g[i] = in.row_g[i];
+        nj_status s = launch_gemm_acc<WRITE, STATS, CAPTURE>(c, st, h, R, gp);
+        if (grid_used) *grid_used = c->grid;
+        return s;
+    }
+    GemmBigParams gp = in;
+    gp.R = R;
+    gp.nchunks = (R + kBigMaxT - 1) / kBigMaxT;
+    gp.chunk = round16((R + gp.nchunks - 1) / gp.nchunks);
+    gp.V_local = c->V_local;
+    gp.U = c->U;
+    gp.num_kb = (c->cfg.d + kBK - 1) / kBK;
+    gp.v_begin = c->cfg.v_begin;
+    gp.part_ld = c->pld;
+    gp.ntiles_g = (c->V_local + kTileV - 1) / kTileV;
+    gp.rr = rr ? 1 : 0;
+    const int grid = rr ? std::max(1, std::min(c->num_sms, gp.ntiles_g)) : c->grid;
+    gp.gk = (gp.nchunks == 1 && gp.chunk <= 128) ? 2 : 1;
+    gp.ks = std::max(gp.gk, (c->gemm_ks + gp.gk - 1) / gp.gk * gp.gk);
+    CUtensorMap tmH;
+    if (!encode_2d(&tmH, h, R, c->cfg.d, gp.chunk)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
+    const size_t stage = (size_t)gp.gk * (kTileBytesA + (size_t)gp.chunk * 128);
+    size_t tail = 4 * 4 * kBigNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
+    tail = align_up(tail, 8) + (2 * 8 + 4) * 8 + 8;
+    const int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
+    if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_big: not enough shared memory (R=%d)", R);
+    gp.nstages = S;
+    const size_t smem = (size_t)S * stage + tail;
+    k_gemm_big<WRITE, STATS, CAPTURE><<<grid, kBigThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
+    NJ_LAUNCHED(c, "k_gemm_big", st);
+    if (grid_used) *grid_used = grid;
     return NJ_OK;
 }
 
@@ -480,12 +533,15 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     c->Nmax = MB * (GM + 1);
     c->Gmax = std::max(1, MB * GM);
     nj_status s = NJ_OK;
-    const size_t g = (size_t)c->grid;
+    c->pld = std::max(c->grid, c->num_sms);
+    if (const char* e = getenv("NJ_GEMM")) c->gemm_acc = strcmp(e, "acc") == 0;
+    if (const char* e = getenv("NJ_KS")) c->gemm_ks = std::max(1, atoi(e));
+    const size_t g = (size_t)c->grid, gp_ = (size_t)c->pld;
 #define A(ptr, n) if ((s = alloc(c, &c->ptr, (n))) != NJ_OK) { nj_destroy(c); return s; }
-    A(part_m, (size_t)c->Nmax * g);
-    A(part_s, (size_t)c->Nmax * g);
-    A(part2_m, (size_t)MB * g);
-    A(part2_s, (size_t)MB * g);
+    A(part_m, (size_t)c->Nmax * gp_);
+    A(part_s, (size_t)c->Nmax * gp_);
+    A(part2_m, (size_t)MB * gp_);
+    A(part2_s, (size_t)MB * gp_);
     A(dl, (size_t)c->Gmax);
     A(wpart, (size_t)MB * g);
     A(s_lse, (size_t)MB);
@@ -518,6 +574,9 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_gemm_acc<false, true, true>);
     e = e ? e : set_smem_attr(k_gemm_acc<true, true, false>);
     e = e ? e : set_smem_attr(k_gemm_acc<true, true, true>);
+    e = e ? e : set_smem_attr(k_gemm_big<false, true, true>);
+    e = e ? e : set_smem_attr(k_gemm_big<true, true, false>);
+    e = e ? e : set_smem_attr(k_gemm_big<true, true, true>);
     if (e != cudaSuccess) {
         nj_destroy(c);
         return set_err(nullptr, NJ_ECUDA, "cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
@@ -634,22 +693,23 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         // row's fp32 logits stored with an L2 evict_last policy (W streams evict_first)
         NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
         if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
-        GemmAccParams gp{};
+        GemmBigParams gp{};
         gp.logits = c->logits_st; gp.ld_out = c->V_local;
         gp.part_m = c->part_m; gp.part_s = c->part_s;
         gp.tok = draft_tokens; gp.dl = c->dl;
         gp.use_row_g = 1;
-        gp.w_evict_first = pl.N <= kAccT ? 1 : 0;
+        gp.w_evict_first = 1;
         if (const char* e = getenv("NJ_W_EVICT_FIRST")) gp.w_evict_first = atoi(e);
         for (int b = 0; b < pl.B; ++b)
             for (int r = pl.row_off[b]; r < pl.row_off[b + 1]; ++r)
                 gp.row_g[r] = r + 1 < pl.row_off[b + 1] ? r - b : -1;
         std::pair<cudaEvent_t, cudaEvent_t> ev;
         if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
-        if ((s = launch_gemm_acc<true, true, true>(c, st, hidden, pl.N, gp)) != NJ_OK) return s;
+        int gridA = c->grid;
+        if ((s = launch_lmhead<true, true, true>(c, st, hidden, pl.N, gp, false, &gridA)) != NJ_OK) return s;
         if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
         AcceptParams ap{};
-        ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = c->grid; ap.dl = c->dl;
+        ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = gridA; ap.pld = c->pld; ap.dl = c->dl;
         ap.draft_tokens = draft_tokens; ap.q = draft_probs; ap.ldq = ldq; ap.u = uniforms;
         ap.hidden = hidden; ap.d = c->cfg.d; ap.hs = nullptr;
         ap.accept_len = accept_len; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
@@ -663,7 +723,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         mp.logits = c->logits_st; mp.ld = c->V_local; mp.s_row = c->s_row;
         mp.V_local = c->V_local; mp.v_begin = c->cfg.v_begin;
         mp.nchunks = c->nchunks; mp.s_resid = c->s_resid; mp.s_qrow = c->s_qrow; mp.s_lse = c->s_lse;
-        mp.part2_m = c->part_m; mp.part2_s = c->part_s; mp.grid2 = c->grid;
+        mp.part2_m = c->part_m; mp.part2_s = c->part_s; mp.grid2 = gridA; mp.pld2 = c->pld;
         mp.q = draft_probs; mp.ldq = ldq; mp.u = uniforms; mp.stage_mode = 0; mp.cmass = c->cmass;
         mp.accept_len = accept_len; mp.next_token = next_token;
         mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
@@ -677,27 +737,31 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
     } else {
         NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
         if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
-        // K-A: stats GEMM over the draft rows (gathered contiguous), draft-logit capture
+        // K-A: stats GEMM over the draft rows (gathered contiguous), draft-logit capture;
+        // all K-A launches share one partial layout (round-robin mode when G > 256)
+        const bool rrA = pl.G > kBigMaxT && !c->gemm_acc;
+        int gridA = c->grid;
         if (pl.G > 0) {
             k_gather_drafts<<<pl.G, 128, 0, st>>>(hidden, c->cfg.d, meta, c->hd);
             NJ_LAUNCHED(c, "k_gather_drafts", st);
             for (int r0 = 0; r0 < pl.G; r0 += kMaxStatRows) {
                 const int R = std::min(kMaxStatRows, pl.G - r0);
-                GemmAccParams gp{};
-                gp.part_m = c->part_m + (size_t)r0 * c->grid;
-                gp.part_s = c->part_s + (size_t)r0 * c->grid;
+                GemmBigParams gp{};
+                gp.part_m = c->part_m + (size_t)r0 * c->pld;
+                gp.part_s = c->part_s + (size_t)r0 * c->pld;
                 gp.tok = draft_tokens + r0;
                 gp.dl = c->dl + r0;
                 std::pair<cudaEvent_t, cudaEvent_t> ev;
                 if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
-                if ((s = launch_gemm_acc<false, true, true>(c, st, c->hd + (size_t)r0 * c->cfg.d, R, gp)) != NJ_OK)
+                if ((s = launch_lmhead<false, true, true>(c, st, c->hd + (size_t)r0 * c->cfg.d, R, gp, rrA,
+                                                          &gridA)) != NJ_OK)
                     return s;
                 if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
             }
         }
         // K-B: acceptance, first rejection, sample-row gather
         AcceptParams ap{};
-        ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = c->grid; ap.dl = c->dl;
+        ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = gridA; ap.pld = c->pld; ap.dl = c->dl;
         ap.draft_tokens = draft_tokens; ap.q = draft_probs; ap.ldq = ldq; ap.u = uniforms;
         ap.hidden = hidden; ap.d = c->cfg.d; ap.hs = c->hs;
         ap.accept_len = accept_len; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
@@ -707,17 +771,19 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
         NJ_LAUNCHED(c, "k_accept", st);
         // K-C: sample-row GEMM -> fp32 logits [B, V_local] + stats (bonus-row lse)
+        int gridC = c->grid;
         {
-            GemmAccParams gp{};
+            GemmBigParams gp{};
             gp.logits = c->logits_s; gp.ld_out = c->V_local;
             gp.part_m = c->part2_m; gp.part_s = c->part2_s;
-            if ((s = launch_gemm_acc<true, true, false>(c, st, c->hs, pl.B, gp)) != NJ_OK) return s;
+            const bool rrC = pl.B > kBigMaxT && !c->gemm_acc;
+            if ((s = launch_lmhead<true, true, false>(c, st, c->hs, pl.B, gp, rrC, &gridC)) != NJ_OK) return s;
         }
         // K-D: residual / bonus masses and the inverse-CDF draw
         MassParams mp{};
         mp.logits = c->logits_s; mp.ld = c->V_local; mp.V_local = c->V_local; mp.v_begin = c->cfg.v_begin;
         mp.nchunks = c->nchunks; mp.s_resid = c->s_resid; mp.s_qrow = c->s_qrow; mp.s_lse = c->s_lse;
-        mp.part2_m = c->part2_m; mp.part2_s = c->part2_s; mp.grid2 = c->grid;
+        mp.part2_m = c->part2_m; mp.part2_s = c->part2_s; mp.grid2 = gridC; mp.pld2 = c->pld;
         mp.q = draft_probs; mp.ldq = ldq; mp.u = uniforms; mp.stage_mode = 0; mp.cmass = c->cmass;
         mp.accept_len = accept_len; mp.next_token = next_token;
         mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();

@@ -1,0 +1,291 @@
+// nj_gemm_big.cuh — k_gemm_big<WRITE,STATS,CAPTURE>: the LM-head GEMM of the
+// staged / two-pass paths (N > 48), built for the tensor-bound regime.
+// Included from nj_gemm.cuh (namespace nj).
+//
+// BJ step (1) l_j(x) = sum_k W[x,k] h_j[k] with BJ step (2)'s online-softmax
+// statistics fused into the epilogue.
+//
+// Why it exists (DESIGN.md §6/§12): k_gemm_acc restarts the TMEM accumulator
+// every k-block (4 MMAs) for accuracy, so every 128x128x64 MMA group (256
+// tensor cycles) is followed by a 64-KB TMEM drain; tcgen05.ld moves ~64 B per
+// cycle per SM, so that kernel is drain-bound at ~30 % of the tensor pipe
+// (ncu: profiles/r01_ncu_gemmacc_b256g5.json).  Here
+//   * the token chunk is up to 256 rows (MMA N = 256, M = 128 vocab rows), and
+//     the accumulator restarts every KS k-blocks (KS = 4 -> 16 MMAs, ks = 16 in
+//     DESIGN.md's accuracy table), so one drain of 256 columns x 128 lanes
+//     (128 KB, ~2048 cycles) is paid per 16 MMAs of 128 cycles: balanced;
+//   * two TMEM accumulators (2 x 256 columns) double-buffer MMA and drain;
+//   * 16 epilogue warps (4 per TMEM lane quadrant, 64 columns each) add the
+//     partials into fp32 round-to-nearest running sums in registers;
+//   * with more than one chunk, work items (vocab tile, chunk) are dealt
+//     round-robin over the CTAs, so the CTAs working at any moment share
+//     ~grid/nchunks W tiles and every W tile is read from HBM about once and
+//     from L2 by its other chunks (k_gemm_acc's per-CTA tile-major order kept
+//     132 x 917 KB of W live and re-read W ~9x from HBM at 10 chunks);
+//   * with one chunk (N <= 256, HBM-bound) the tile-balanced contiguous vocab
+//     split of the fused kernel is kept (W streamed once, evict_first).
+// The certificate margins of the paths that use this kernel are set from its
+// measured error.
+#pragma once
+
+constexpr int kBigEpiWarps = 16;
+constexpr int kBigThreads = (2 + kBigEpiWarps) * 32;   // warp 0 TMA, warp 1 MMA/TMEM, 2..17 epilogue
+constexpr int kBigMaxT = 256;                          // token chunk (MMA N) upper bound
+constexpr int kBigNC = 64;                             // columns per epilogue warp
+constexpr int kBigMaxRowG = 256;                       // staged path: rows mapped to draft indices
+
+struct GemmBigParams {
+    int32_t R, nchunks, chunk;           // rows, chunks, rows per chunk (multiple of 16, <= 256)
+    int32_t V_local, U, num_kb, nstages, v_begin;
+    int32_t gk;                          // k-blocks per TMA ring stage (1, 2 or 4)
+    int32_t ks;                          // k-blocks per accumulator restart (multiple of gk)
+    int32_t rr;                          // 1: round-robin (tile, chunk) items over global 128-row tiles
+    int32_t ntiles_g;                    // global 128-row tiles (rr mode)
+    float* logits;                       // WRITE: [R][ld_out] fp32
+    int64_t ld_out;
+    float* part_m;                       // STATS: [R][part_ld] per-CTA (m, s)
+    float* part_s;
+    int32_t part_ld;
+    const int32_t* tok;                  // CAPTURE: [R] global ids (or draft_tokens with use_row_g)
+    double* dl;                          // CAPTURE: [R] (or [G] with use_row_g)
+    int32_t w_evict_first;
+    int32_t use_row_g;                   // staged path: row r is draft row_g[r] (-1: bonus row)
+    int32_t row_g[kBigMaxRowG];
+};
+
+// Work item `it` of CTA `cta`: vocab rows [row0, row0 + trows) of the local
+// shard, token chunk c.  Returns false past the CTA's last item.
+__device__ __forceinline__ bool big_item(const GemmBigParams& p, int cta, int grid, int r0, int rows, int it,
+                                         int& row0, int& trows, int& c) {
+    if (p.rr) {
+        const int i = cta + it * grid;
+        if (i >= p.ntiles_g * p.nchunks) return false;
+        const int t = i / p.nchunks;
+        c = i - t * p.nchunks;
+        row0 = t * kTileV;
+        trows = min(kTileV, p.V_local - row0);
+        return true;
+    }
+    const int ntiles = (rows + kTileV - 1) / kTileV;
+    if (it >= ntiles * p.nchunks) return false;
+    const int t = it / p.nchunks;
+    c = it - t * p.nchunks;
+    row0 = r0 + t * kTileV;
+    trows = min(kTileV, rows - t * kTileV);
+    return true;
+}
+
+template <bool WRITE, bool STATS, bool CAPTURE>
+__global__ void __launch_bounds__(kBigThreads, 1)
+k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ CUtensorMap tmW16,
+           const __grid_constant__ CUtensorMap tmH, const GemmBigParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int S = p.nstages, GK = p.gk;
+    const int bBytes = p.chunk * 128;                                 // H box per k-block
+    const size_t stageBytes = (size_t)GK * (kTileBytesA + bBytes);
+    uint8_t* ring = smem;                                             // S x GK x (A 16 KB | B bBytes)
+    float2* scratch = reinterpret_cast<float2*>(ring + (size_t)S * stageBytes);   // [4 e][4 q][64]
+    float2* state = scratch + 4 * 4 * kBigNC;                                       // [R] (STATS)
+    int32_t* stok = reinterpret_cast<int32_t*>(state + (STATS ? p.R : 0));         // [R] (CAPTURE)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(stok + (CAPTURE ? p.R : 0)) + 7) & ~uintptr_t(7));
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* afull = bars + 2 * S;    // [2] accumulator buffers
+    uint64_t* aempty = afull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+
+    const int warp = (int)warp_id(), lane = (int)lane_id();
+    const int grid = gridDim.x, cta = blockIdx.x;
+    int r0 = 0, rows = 0;
+    if (!p.rr) vocab_range(p.U, grid, cta, p.V_local, r0, rows);
+    const int ngk = (p.num_kb + GK - 1) / GK;          // ring stages per item
+
+    if (threadIdx.x == 0) {
+        tma_prefetch_desc(&tmW128);
+        tma_prefetch_desc(&tmW16);
+        tma_prefetch_desc(&tmH);
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int g = 0; g < 2; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kBigEpiWarps); }
+        fence_barrier_init();
+        fence_proxy_async();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (STATS)
+        for (int i = threadIdx.x; i < p.R; i += kBigThreads) state[i] = make_float2(-INFINITY, 0.f);
+    if (CAPTURE)
+        for (int i = threadIdx.x; i < p.R; i += kBigThreads) {
+            if (p.use_row_g) stok[i] = p.row_g[i] >= 0 ? p.tok[p.row_g[i]] - p.v_begin : -1;
+            else stok[i] = p.tok[i] - p.v_begin;
+        }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            const uint64_t pol_w = p.w_evict_first ? policy_evict_first() : policy_evict_last();
+            const uint64_t pol_h = policy_evict_last();
+            int s = 0;
+            uint32_t ph = 0;
+            int row0, trows, c;
+            for (int it = 0; big_item(p, cta, grid, r0, rows, it, row0, trows, c); ++it) {
+                for (int kg = 0; kg < ngk; ++kg) {
+                    const int ng = min(GK, p.num_kb - kg * GK);
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)ng * (w_tile_bytes(trows) + (uint32_t)bBytes));
+                    uint8_t* st = ring + (size_t)s * stageBytes;
+                    for (int g = 0; g < ng; ++g) {
+                        const int kb = kg * GK + g;
+                        load_w_tile(st + (size_t)g * kTileBytesA, &tmW128, &tmW16, &full[s], kb, row0, trows,
+                                    pol_w);
+                        tma_load_2d(st + (size_t)GK * kTileBytesA + (size_t)g * bBytes, &tmH, &full[s], kb * kBK,
+                                    c * p.chunk, pol_h);
+                    }
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            int s = 0;
+            uint32_t ph = 0;
+            int ngrp = 0;   // accumulator groups issued (buffer ngrp & 1, phase (ngrp >> 1) & 1)
+            int row0, trows, c;
+            for (int it = 0; big_item(p, cta, grid, r0, rows, it, row0, trows, c); ++it) {
+                const int ncol = min(p.chunk, p.R - c * p.chunk);
+                const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)((ncol + 15) & ~15));
+                int kin = 0;   // k-blocks into the current accumulator group
+                uint32_t dt = 0;
+                for (int kg = 0; kg < ngk; ++kg) {
+                    const int ng = min(GK, p.num_kb - kg * GK);
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    uint8_t* st = ring + (size_t)s * stageBytes;
+                    for (int g = 0; g < ng; ++g) {
+                        if (kin == 0) {
+                            const int buf = ngrp & 1;
+                            mbar_wait(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
+                            tc_fence_after();
+                            dt = tbase + (uint32_t)(buf * kBigMaxT);
+                        }
+                        const uint64_t ad = sdesc_sw128(st + (size_t)g * kTileBytesA);
+                        const uint64_t bd = sdesc_sw128(st + (size_t)GK * kTileBytesA + (size_t)g * bBytes);
+#pragma unroll
+                        for (int k = 0; k < kBK / 16; ++k)
+                            mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                        const int kb = kg * GK + g;
+                        if (++kin == p.ks || kb == p.num_kb - 1) {
+                            mma_commit(&afull[ngrp & 1]);
+                            ++ngrp;
+                            kin = 0;
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                    if (++s == S) { s = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (16 warps)
+        const int q = warp & 3;             // TMEM lane quadrant this warp may access
+        const int e = (warp - 2) >> 2;      // 64-column slice
+        const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(e * kBigNC);
+        const int vr = q * 32 + lane;
+        const uint64_t pol_keep = policy_evict_last();   // staged logits stay in L2 for the sampler
+        const int ngroups = (p.num_kb + p.ks - 1) / p.ks;
+        int ngrp = 0;
+        int row0, trows, c;
+        for (int it = 0; big_item(p, cta, grid, r0, rows, it, row0, trows, c); ++it) {
+            const int c0 = c * p.chunk;
+            const int ncol = min(p.chunk, p.R - c0);
+            const int myc = ncol - e * kBigNC;   // columns of this warp's slice that exist (may be <= 0)
+            float acc[kBigNC];
+#pragma unroll
+            for (int j = 0; j < kBigNC; ++j) acc[j] = 0.f;
+            for (int g = 0; g < ngroups; ++g, ++ngrp) {
+                const int buf = ngrp & 1;
+                mbar_wait(&afull[buf], (ngrp >> 1) & 1);
+                tc_fence_after();
+                const uint32_t ta = lane_base + (uint32_t)(buf * kBigMaxT);
+                if (myc > 32) {
+                    float v[32];
+                    tmem_ld32(ta, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] += v[i];   // fp32 RN, unbiased
+                    tmem_ld32(ta + 32u, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[32 + i] += v[i];
+                } else if (myc > 16) {
+                    float v[32];
+                    tmem_ld32(ta, v);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] += v[i];
+                } else if (myc > 0) {
+                    float v[16];
+                    tmem_ld16(ta, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) acc[i] += v[i];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&aempty[buf]);
+            }
+            const bool valid = vr < trows;
+            const int xl = row0 + vr;
+#pragma unroll
+            for (int j = 0; j < kBigNC; ++j) {
+                if (j < myc) {
+                    const int row = c0 + e * kBigNC + j;
+                    if (WRITE && valid) st_evict_last(&p.logits[(int64_t)row * p.ld_out + xl], acc[j], pol_keep);
+                    if (CAPTURE && valid && stok[row] == xl) p.dl[p.use_row_g ? p.row_g[row] : row] = (double)acc[j];
+                }
+            }
+            if (STATS) {
+                // two reduce-scatters of 32 columns: lane l then owns column
+                // col_of_lane<32>(l) of each half -> scratch[e][q][col]; the 4
+                // quadrant warps of slice e merge them into the row state
+                if (myc > 0) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        float tm[32], ts[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const bool ok = valid && hh * 32 + j < myc;
+                            tm[j] = ok ? acc[hh * 32 + j] : -INFINITY;
+                            ts[j] = ok ? 1.f : 0.f;
+                        }
+                        float wm, ws;
+                        warp_scatter_ms<32>(tm, ts, wm, ws);
+                        scratch[(e * 4 + q) * kBigNC + hh * 32 + col_of_lane<32>(lane)] = make_float2(wm, ws);
+                    }
+                }
+                named_bar(1 + e, 128);
+                const int ht = ((warp - 2) & 3) * 32 + lane;   // 0..127 within the slice's 4 warps
+                if (ht < kBigNC && ht < myc) {
+                    const int col = c0 + e * kBigNC + ht;
+                    float2 st = state[col];
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const float2 o = scratch[(e * 4 + w) * kBigNC + ht];
+                        ms_merge(st.x, st.y, o.x, o.y);
+                    }
+                    state[col] = st;
+                }
+                named_bar(1 + e, 128);
+            }
+        }
+    }
+    __syncthreads();
+    if (STATS)
+        for (int i = threadIdx.x; i < p.R; i += kBigThreads) {
+            p.part_m[(int64_t)i * p.part_ld + cta] = state[i].x;
+            p.part_s[(int64_t)i * p.part_ld + cta] = state[i].y;
+        }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tbase, 512);
+}

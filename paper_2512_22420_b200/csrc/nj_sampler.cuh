@@ -83,7 +83,8 @@ __device__ __forceinline__ double warp_lse(const float* pm, const float* ps, int
 struct AcceptParams {
     const float* part_m;   // [G][grid] stats of draft rows (K-A)
     const float* part_s;
-    int32_t grid;
+    int32_t grid;          // CTAs that wrote partials
+    int32_t pld;           // partial row stride (>= grid)
     const double* dl;      // [G] draft logits
     const int32_t* draft_tokens;
     const float* q;
@@ -120,7 +121,7 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
     double lse_n = __longlong_as_double(0x7ff8000000000000ll);
     for (int i = 0; i < gam; ++i) {
         const int g = g0 + i;
-        const double lse = warp_lse(p.part_m, p.part_s, p.grid, p.staged ? ro + i : g, p.grid);
+        const double lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid);
         const double pd = exp(__ldcg(&p.dl[g]) - lse);
         const double qx = (double)p.q[(int64_t)g * p.ldq + p.draft_tokens[g]];
         const double uq = (double)p.u[ro + i] * qx;
@@ -134,14 +135,14 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
     // remaining drafts (untested) still get debug values
     for (int i = n + 1; i < gam && p.dbg_pdraft; ++i) {
         const int g = g0 + i;
-        const double lse = warp_lse(p.part_m, p.part_s, p.grid, p.staged ? ro + i : g, p.grid);
+        const double lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid);
         if (lane == 0) {
             if (p.dbg_lse) p.dbg_lse[ro + i] = (float)lse;
             p.dbg_pdraft[g] = (float)exp(__ldcg(&p.dl[g]) - lse);
         }
     }
     if (p.staged) {
-        if (n == gam) lse_n = warp_lse(p.part_m, p.part_s, p.grid, ro + gam, p.grid);   // bonus row
+        if (n == gam) lse_n = warp_lse(p.part_m, p.part_s, p.pld, ro + gam, p.grid);   // bonus row
     } else {
         copy_row(p.hs + (int64_t)b * p.d, p.hidden + (int64_t)(ro + n) * p.d, p.d, lane, 32);
     }
@@ -195,6 +196,7 @@ struct MassParams {
     const float* part2_m;  // [B][grid2] (K-C stats)
     const float* part2_s;
     int32_t grid2;
+    int32_t pld2;          // part2 row stride (>= grid2)
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -217,7 +219,7 @@ __device__ __forceinline__ double sample_lse(const MassParams& p, int b) {
     double l = p.s_lse[b];
     if (isnan(l)) {
         if (warp_id() == 0) {
-            const double v = warp_lse(p.part2_m, p.part2_s, p.grid2, b, p.grid2);
+            const double v = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
             if (lane_id() == 0) s_l = v;
         }
         __syncthreads();

@@ -5,7 +5,7 @@ from synth.inputs import make_batch, make_weight
 dev = torch.device("cuda:0")
 V, d = 152064, 3584
 B, g = int(sys.argv[1]), int(sys.argv[2])
-path = NJ_PATH_FUSED if (len(sys.argv) < 4 or sys.argv[3] == "fused") else NJ_PATH_TWOPASS
+path = {"fused": 1, "twopass": 2, "staged": 3}[sys.argv[3] if len(sys.argv) > 3 else "fused"]
 W = make_weight(V, d, 0, dev)
 b = make_batch(B, g, V=V, d=d, seed=0, device=dev, W=W)
 v = Verifier(d, V, max_batch=B, gamma_max=5)
