@@ -83,8 +83,9 @@ typedef struct {
     int32_t max_batch;  /* B_max, 1..4096                                   */
     int32_t gamma_max;  /* Γ_max, 0..15                                     */
     int32_t device;     /* CUDA device ordinal                                     */
-    void*   nccl_comm;  /* NULL: unsharded.  Else an ncclComm_t: vocab-sharded LM  */
-                        /* head (BJ config 5); this rank owns W rows [v_begin,v_end) */
+    void*   nccl_comm;  /* NULL: unsharded.  Else an ncclComm_t (nj_nccl_comm_init): */
+                        /* vocab-sharded LM head (BJ config 5, see below); this    */
+                        /* rank owns W rows [v_begin,v_end) = nj_shard_range(...)  */
     int32_t v_begin;    /* shard start (global id); unsharded: 0                   */
     int32_t v_end;      /* shard end (exclusive);   unsharded: V                   */
 } nj_config;
@@ -212,6 +213,54 @@ nj_status nj_sample_from_logits(nj_ctx* ctx, void* stream,
                                 const float* q, int64_t ldq,
                                 const float* u, int32_t B,
                                 int32_t* next_token, double* mass);
+
+/* ------------------------------------------------------ vocab-sharded mode */
+/* BJ config 5 / SURVEY §8a row a7, §8e: the LM head split along V over G
+ * ranks (one process per GPU).  Rank r owns the contiguous, 128-row aligned
+ * shard [v_begin, v_end) = nj_shard_range(V, G, r) (rank order = ascending
+ * token id, which is the inverse-CDF order of R5).  Pass the communicator
+ * (nj_nccl_comm_init) and the shard in nj_config; every rank then calls
+ * nj_verify with the SAME hidden / draft / uniform / gamma inputs and its own
+ * W shard (draft_probs rows are full-vocabulary rows; a rank reads only its
+ * columns).  nj_verify runs in phases separated by three small exchanges on
+ * `stream` (NCCL allgather of per-draft-row (lse_r, owned draft logit), of
+ * per-request (lse, shard mass), and an allreduce-MAX of [token | flags]);
+ * the certified fp64 fallback adds three more of the same kind.  Outputs
+ * (accept_len, next_token, debug) are identical on every rank and equal the
+ * unsharded definition (header comment) outside the 1e-6 tie band.
+ * Error behaviour: NJ_ENCCL if libnccl.so.2 cannot be loaded or a collective
+ * fails; NJ_ESHAPE if the shard is not nj_shard_range's.  The fused and
+ * staged paths are unsharded-only (the sharded driver is the two-pass path). */
+
+/* Shard of rank `rank` of `nranks`: [*v_begin, *v_end).  NJ_ESHAPE if V has
+ * fewer 128-row tiles than ranks. */
+nj_status nj_shard_range(int32_t V, int32_t nranks, int32_t rank, int32_t* v_begin, int32_t* v_end);
+
+#define NJ_NCCL_ID_BYTES 128
+/* NCCL bootstrap (libnccl.so.2 loaded at runtime): rank 0 creates the id,
+ * the caller broadcasts the NJ_NCCL_ID_BYTES bytes (e.g. torch.distributed),
+ * every rank calls nj_nccl_comm_init (collective; sets `device` current). */
+nj_status nj_nccl_get_unique_id(void* id_out);
+nj_status nj_nccl_comm_init(int32_t nranks, const void* id, int32_t rank, int32_t device, void** comm_out);
+void      nj_nccl_comm_destroy(void* comm);
+
+/* Single-process shard group: nshards contexts on cfg->device (cfg's shard
+ * fields and nccl_comm are ignored; member r owns nj_shard_range(V, nshards,
+ * r)) whose exchanges are device-to-device copies on `stream`.  Runs exactly
+ * the per-rank kernels of the NCCL mode, so one GPU can check sharded parity.
+ * nj_group_verify: W_shards is a HOST array of nshards device pointers (member
+ * r's [v_end - v_begin, d] rows); other arguments as nj_verify.  dbg is filled
+ * from member 0.  nj_group_member returns member r's context (options:
+ * nj_set_option on every member), NULL if out of range. */
+typedef struct nj_group nj_group;
+nj_status nj_group_create(const nj_config* cfg, int32_t nshards, nj_group** out);
+void      nj_group_destroy(nj_group* g);
+nj_ctx*   nj_group_member(nj_group* g, int32_t r);
+const char* nj_group_last_error(const nj_group* g);
+nj_status nj_group_verify(nj_group* g, void* stream, const uint16_t* hidden, const uint16_t* const* W_shards,
+                          const int32_t* draft_tokens, const float* draft_probs, int64_t ldq,
+                          const int32_t* gamma_per_req, const float* uniforms, int32_t B,
+                          int32_t* accept_len, int32_t* next_token, const nj_debug* dbg);
 
 /* ---------------------------------------------------------------- bandit */
 /* Nightjar arm selection (Algorithm 1) with the

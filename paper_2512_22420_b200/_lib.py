@@ -31,7 +31,10 @@ EXPORTS = [
     "nj_lmhead_logits", "nj_lmhead_logits_ks", "nj_sample_from_logits", "nj_bandit_create", "nj_bandit_destroy", "nj_select_gamma",
     "nj_observe", "nj_exploitation_score", "nj_prefill_cost_ms", "nj_bandit_state", "nj_bandit_arm",
     "nj_bandit_last_gamma", "nj_bandit_snapshot_json",
+    "nj_shard_range", "nj_nccl_get_unique_id", "nj_nccl_comm_init", "nj_nccl_comm_destroy", "nj_group_create",
+    "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify",
 ]
+NJ_NCCL_ID_BYTES = 128
 
 
 class NJError(RuntimeError):
@@ -87,6 +90,15 @@ def load():
         "nj_bandit_arm": ([P, I32, I32, P, P], I32),
         "nj_bandit_last_gamma": ([P], I32),
         "nj_bandit_snapshot_json": ([P, P, ctypes.c_size_t, P], I32),
+        "nj_shard_range": ([I32, I32, I32, P, P], I32),
+        "nj_nccl_get_unique_id": ([P], I32),
+        "nj_nccl_comm_init": ([I32, P, I32, I32, ctypes.POINTER(P)], I32),
+        "nj_nccl_comm_destroy": ([P], None),
+        "nj_group_create": ([ctypes.POINTER(nj_config), I32, ctypes.POINTER(P)], I32),
+        "nj_group_destroy": ([P], None),
+        "nj_group_member": ([P, I32], P),
+        "nj_group_last_error": ([P], ctypes.c_char_p),
+        "nj_group_verify": ([P, P, P, P, P, P, I64, P, P, I32, P, P, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -188,6 +200,95 @@ class Verifier:
         self._check(self._lib.nj_sample_from_logits(
             self._h, _stream(stream), _ptr(logits), int(logits.stride(0)), _ptr(residual), _ptr(q),
             int(q.stride(0)), _ptr(u), int(logits.shape[0]), _ptr(next_token), _ptr(mass)))
+
+
+def shard_range(V: int, nranks: int, rank: int):
+    """nj_shard_range: [v_begin, v_end) of `rank` (128-row aligned, rank order)."""
+    lib = load()
+    vb, ve = ctypes.c_int32(), ctypes.c_int32()
+    st = lib.nj_shard_range(V, nranks, rank, ctypes.byref(vb), ctypes.byref(ve))
+    if st != NJ_OK:
+        raise NJError(st, f"nj_shard_range({V}, {nranks}, {rank})")
+    return vb.value, ve.value
+
+
+def nccl_unique_id() -> bytes:
+    """nj_nccl_get_unique_id (rank 0); broadcast the bytes to the other ranks."""
+    buf = ctypes.create_string_buffer(NJ_NCCL_ID_BYTES)
+    st = load().nj_nccl_get_unique_id(buf)
+    if st != NJ_OK:
+        raise NJError(st, "nj_nccl_get_unique_id")
+    return buf.raw
+
+
+class NcclComm:
+    """RAII wrapper of the communicator libnj creates (nj_nccl_comm_init)."""
+
+    def __init__(self, nranks: int, uid: bytes, rank: int, device: int):
+        lib = load()
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(bytes(uid), NJ_NCCL_ID_BYTES)
+        st = lib.nj_nccl_comm_init(nranks, buf, rank, device, ctypes.byref(h))
+        if st != NJ_OK:
+            raise NJError(st, f"nj_nccl_comm_init(rank {rank} of {nranks})")
+        self._lib, self.handle, self.nranks, self.rank = lib, h.value, nranks, rank
+
+    def close(self):
+        if self.handle:
+            self._lib.nj_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+
+class ShardGroup:
+    """RAII wrapper of nj_group: `nshards` vocab shards on one device, exchanges
+    as device copies (the per-rank kernels of the NCCL mode, in one process)."""
+
+    def __init__(self, d: int, V: int, max_batch: int, gamma_max: int, nshards: int, device: int = 0):
+        lib = load()
+        cfg = nj_config(d, V, max_batch, gamma_max, device, None, 0, V)
+        h = ctypes.c_void_p()
+        st = lib.nj_group_create(ctypes.byref(cfg), nshards, ctypes.byref(h))
+        if st != NJ_OK:
+            raise NJError(st, lib.nj_group_last_error(None).decode())
+        self._lib, self._h, self.n, self.cfg = lib, h, nshards, cfg
+        self.ranges = [shard_range(V, nshards, r) for r in range(nshards)]
+
+    def close(self):
+        if self._h:
+            self._lib.nj_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, opt: int, value: int):
+        for r in range(self.n):
+            m = self._lib.nj_group_member(self._h, r)
+            st = self._lib.nj_set_option(m, opt, int(value))
+            if st != NJ_OK:
+                raise NJError(st, "nj_set_option")
+
+    def shards(self, W):
+        """Views of a full [V, d] weight as the members' shards."""
+        return [W[vb:ve] for vb, ve in self.ranges]
+
+    def verify(self, hidden, W_shards, draft_tokens, draft_probs, gamma, uniforms, accept_len, next_token,
+               debug: dict | None = None, stream=None):
+        g = np.ascontiguousarray(gamma, np.int32)
+        ptrs = (ctypes.c_void_p * self.n)(*[_ptr(w) for w in W_shards])
+        dbg = None
+        if debug is not None:
+            dbg = nj_debug(_ptr(debug.get("lse")), _ptr(debug.get("p_draft")), _ptr(debug.get("mass")),
+                           _ptr(debug.get("flags")))
+        st = self._lib.nj_group_verify(
+            self._h, _stream(stream), _ptr(hidden), ptrs, _ptr(draft_tokens), _ptr(draft_probs),
+            int(draft_probs.stride(0)), _ptr(g), _ptr(uniforms), g.shape[0], _ptr(accept_len), _ptr(next_token),
+            ctypes.byref(dbg) if dbg is not None else None)
+        if st != NJ_OK:
+            raise NJError(st, self._lib.nj_group_last_error(self._h).decode())
 
 
 class Bandit:

@@ -108,7 +108,12 @@ struct AcceptParams {
     // row's logits are staged, so no hidden-row copy; s_row[b] = sample row
     int32_t staged;
     int32_t* s_row;
+    // vocab-sharded mode (nj_shard.cuh): merged X1 entries [nranks][xld][2]
+    const double* xr1;
+    int32_t nranks, xld;
 };
+
+__device__ __forceinline__ double xmerge_lse(const double* xr, int nranks, int ld, int g, double& dl);
 
 // K-B: warp per request — lse of its draft rows, acceptance tests, first
 // rejection, sample-row bookkeeping, and the copy of the sample hidden row.
@@ -121,8 +126,10 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
     double lse_n = __longlong_as_double(0x7ff8000000000000ll);
     for (int i = 0; i < gam; ++i) {
         const int g = g0 + i;
-        const double lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid);
-        const double pd = exp(__ldcg(&p.dl[g]) - lse);
+        double lse, dlv;
+        if (p.xr1) lse = xmerge_lse(p.xr1, p.nranks, p.xld, g, dlv);
+        else { lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid); dlv = __ldcg(&p.dl[g]); }
+        const double pd = exp(dlv - lse);
         const double qx = (double)p.q[(int64_t)g * p.ldq + p.draft_tokens[g]];
         const double uq = (double)p.u[ro + i] * qx;
         if (lane == 0) {
@@ -135,10 +142,12 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
     // remaining drafts (untested) still get debug values
     for (int i = n + 1; i < gam && p.dbg_pdraft; ++i) {
         const int g = g0 + i;
-        const double lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid);
+        double lse, dlv;
+        if (p.xr1) lse = xmerge_lse(p.xr1, p.nranks, p.xld, g, dlv);
+        else { lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid); dlv = __ldcg(&p.dl[g]); }
         if (lane == 0) {
             if (p.dbg_lse) p.dbg_lse[ro + i] = (float)lse;
-            p.dbg_pdraft[g] = (float)exp(__ldcg(&p.dl[g]) - lse);
+            p.dbg_pdraft[g] = (float)exp(dlv - lse);
         }
     }
     if (p.staged) {
@@ -212,7 +221,18 @@ struct MassParams {
     float* dbg_lse;
     int32_t certify;
     float eps_draw;
+    // vocab-sharded mode: X2 entries [nranks][B][2] (lse used, local mass);
+    // next_token then points at the X3 buffer (-1 on non-owner ranks) and
+    // flags go to xflags[b] (reduced by MAX, queued by k_xfinish)
+    const double* xr2;
+    int32_t nranks, rank;
+    int32_t* xflags;
 };
+
+__device__ __forceinline__ void flag_draw(const MassParams& p, int b, int32_t bits) {
+    if (p.xflags) atomicOr(&p.xflags[b], bits | 0x100);
+    else if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, bits);
+}
 
 __device__ __forceinline__ double sample_lse(const MassParams& p, int b) {
     __shared__ double s_l;
@@ -289,12 +309,56 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     __shared__ float wt[kSubTiles][8];
     const int gam = p.stage_mode ? 0 : m.row_off[b + 1] - m.row_off[b] - 1;
     const float uf = p.stage_mode ? p.u[b] : p.u[m.row_off[b] + gam];
+    __shared__ int s_own;
+    __shared__ double s_scale;
     if (threadIdx.x == 0) {
         double P = 0.0, Pc = 0.0;
         int csel = -1, lastpos = -1;
         double W = 0.0;
         for (int c = 0; c < p.nchunks; ++c) W = W + p.cmass[(int64_t)b * p.nchunks + c];
-        const double T = (double)uf * W;
+        double T = (double)uf * W;
+        int own = 1, zero_g = 0, clamp_g = 0;
+        double scale = 1.0;   // local mass units -> natural (p) units
+        if (p.xr2) {
+            // global inverse CDF over the ranks' masses in rank order (nj_shard.cuh, X2)
+            double M = -INFINITY;
+            for (int r = 0; r < p.nranks; ++r)
+                if (p.xr2[((int64_t)r * m.B + b) * 2 + 1] > 0.0) M = fmax(M, p.xr2[((int64_t)r * m.B + b) * 2]);
+            double Tot = 0.0;
+            for (int r = 0; r < p.nranks; ++r) {
+                const double Wr = p.xr2[((int64_t)r * m.B + b) * 2 + 1];
+                if (Wr > 0.0) Tot += Wr * exp(p.xr2[((int64_t)r * m.B + b) * 2] - M);
+            }
+            const double nrm = resid ? 1.0 : 1.0 / Tot;   // bonus rows: natural mass = A / Tot
+            if (!(Tot > 0.0)) {
+                zero_g = 1;
+                own = 0;
+            } else {
+                const double Tg = (double)uf * Tot;
+                double Pg = 0.0, Po = 0.0, Ao = 0.0;
+                int o = -1, lastr = -1;
+                for (int r = 0; r < p.nranks; ++r) {
+                    const double Wr = p.xr2[((int64_t)r * m.B + b) * 2 + 1];
+                    const double A = Wr > 0.0 ? Wr * exp(p.xr2[((int64_t)r * m.B + b) * 2] - M) : 0.0;
+                    if (A > 0.0) {
+                        lastr = r;
+                        if (o < 0 && Tg < Pg + A) { o = r; Po = Pg; Ao = A; }
+                    }
+                    Pg += A;
+                }
+                if (o < 0) { o = lastr; clamp_g = 1; }
+                own = (o == p.rank);
+                if (own) {
+                    const double e = exp(p.xr2[((int64_t)p.rank * m.B + b) * 2] - M);
+                    scale = e * nrm;
+                    T = clamp_g ? W : (Tg - Po) / e;
+                    if (!clamp_g && fmin(Tg - Po, Po + Ao - Tg) * nrm <= (double)p.eps_draw) flag_draw(p, b, 0);
+                }
+            }
+            if (p.dbg_mass) p.dbg_mass[b] = zero_g ? 0.0 : (resid ? Tot : 1.0);
+        }
+        s_own = own;
+        s_scale = scale;
         for (int c = 0; c < p.nchunks; ++c) {
             const double wc = p.cmass[(int64_t)b * p.nchunks + c];
             if (wc > 0.0) lastpos = c;
@@ -302,7 +366,7 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
             P = P + wc;
         }
         int clamp = 0;
-        if (!(W > 0.0)) clamp = 2;                         // zero mass (R6) -> fallback
+        if (zero_g || !(W > 0.0)) clamp = 2;               // zero mass (R6) -> fallback
         else if (csel < 0) { clamp = 1; csel = lastpos; Pc = 0.0; }
         sh[0] = T - Pc;
         sh[1] = W;
@@ -312,12 +376,19 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     }
     __syncthreads();
     const int clamp = shi[1];
+    if (p.xr2 && !s_own) {   // another rank owns this draw (or zero mass everywhere)
+        if (threadIdx.x == 0) {
+            p.next_token[b] = -1;
+            if (clamp == 2) flag_draw(p, b, 2);
+        }
+        return;
+    }
     if (clamp == 2) {
         if (threadIdx.x == 0) {
             p.next_token[b] = 0;
             if (p.dbg_mass) p.dbg_mass[b] = 0.0;
             if (p.dbg_flags) p.dbg_flags[b] = 2;
-            if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 2);
+            flag_draw(p, b, 2);
         }
         return;
     }
@@ -371,18 +442,18 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
             for (int k = 7; k >= 0 && pick < 0; --k)
                 if (wpick[k] >= 0) pick = k * 32 + wpick[k];
             p.next_token[b] = c * kChunk + s * kSampThreads + (pick < 0 ? 0 : pick) + p.v_begin;
-            if (p.dbg_mass) p.dbg_mass[b] = sh[1];
+            if (p.dbg_mass && !p.xr2) p.dbg_mass[b] = sh[1];
             if (p.dbg_flags) p.dbg_flags[b] = 4;
-            if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 4);
+            flag_draw(p, b, 4);
         }
         return;
     }
     if (ws > 0.f && lo <= tp && tp < hi) {
         p.next_token[b] = x + p.v_begin;
-        if (p.dbg_mass) p.dbg_mass[b] = sh[1];
+        if (p.dbg_mass && !p.xr2) p.dbg_mass[b] = sh[1];
         if (p.dbg_flags) p.dbg_flags[b] = 0;
-        const double margin = fmin(tp - lo, hi - tp);
-        if (p.certify && margin <= (double)p.eps_draw) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
+        const double margin = fmin(tp - lo, hi - tp) * s_scale;
+        if (margin <= (double)p.eps_draw) flag_draw(p, b, 0);
     }
 }
 

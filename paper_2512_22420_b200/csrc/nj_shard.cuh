@@ -1,0 +1,287 @@
+// nj_shard.cuh — device side of the vocab-sharded mode (BJ config 5; SURVEY
+// §8a row a7, §8e "vocab-sharded").  Rank r of G owns the contiguous vocab
+// shard [v_begin, v_end) of W_lm (rank order = ascending token id, R5).  The
+// kernels here pack / merge the small per-rank summaries that the host
+// exchanges between the phases of nj_verify (NCCL allgather / allreduce-MAX,
+// or device copies inside an nj_group):
+//
+//   X1  per draft row g : (lse_r(g), l_g(x_g) if x_g is in this shard else NaN)
+//       -> every rank merges lse(g) = logsumexp_r lse_r(g) in rank order and
+//          takes the owner's draft logit: identical acceptance decisions
+//          everywhere (k_accept with xr1).
+//   X2  per request b   : (lse used for the sample row, local mass W_r)
+//       residual rows use the global lse from X1 (so W_r are natural masses);
+//       bonus rows use the rank-local lse (W_r ~ 1 in local units) and are
+//       rescaled by exp(lse_r - M).  The inverse CDF (R5) over the global
+//       ascending order is then: T = u * sum_r A_r, owner = the rank whose
+//       exclusive prefix interval holds T, local target (T - P_owner) /
+//       exp(lse_owner - M)  (k_locate with xr2).
+//   X3  allreduce-MAX of [next_token (-1 on non-owners) | flags] (k_xfinish).
+// The certified fallback (R11/R12) repeats the same three exchanges in fp64
+// for the queued requests (X4: per-row (lse_r, owned draft logit); X5:
+// per-request local residual / p masses; X6: MAX of [token | flags]).
+#pragma once
+#include "nj_sampler.cuh"
+
+namespace nj {
+
+// Merge of the X1 entries of draft row g: lse = M + log sum_r exp(lse_r - M)
+// (rank order), dl = the owner's draft logit (exactly one rank is not NaN).
+__device__ __forceinline__ double xmerge_lse(const double* xr, int nranks, int ld, int g, double& dl) {
+    double M = -INFINITY;
+    dl = __longlong_as_double(0x7ff8000000000000ll);
+    for (int r = 0; r < nranks; ++r) {
+        const double* e = xr + ((int64_t)r * ld + g) * 2;
+        M = fmax(M, __ldcg(&e[0]));
+        const double d = __ldcg(&e[1]);
+        if (!isnan(d)) dl = d;
+    }
+    double S = 0.0;
+    for (int r = 0; r < nranks; ++r) S += exp(__ldcg(&xr[((int64_t)r * ld + g) * 2]) - M);
+    return M + log(S);
+}
+
+// X1 pack: warp per draft row.
+__global__ void k_xpack1(const float* part_m, const float* part_s, int pld, int grid, const double* dl, int G,
+                         double* xs1) {
+    const int g = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
+    if (g >= G) return;
+    const double l = warp_lse(part_m, part_s, pld, g, grid);
+    if (lane_id() == 0) {
+        xs1[2 * g] = l;
+        xs1[2 * g + 1] = __ldcg(&dl[g]);
+    }
+}
+
+// X2 pack: warp per request: lse of the sample row as used by k_mass, and the
+// rank's mass sum_c cmass (fixed order, as k_locate sums it).
+__global__ void k_xpack2(const MassParams p, int B, double* xs2) {
+    const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
+    if (b >= B) return;
+    double l = __ldcg(&p.s_lse[b]);
+    if (isnan(l)) l = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
+    if (lane_id() == 0) {
+        double W = 0.0;
+        for (int c = 0; c < p.nchunks; ++c) W = W + __ldcg(&p.cmass[(int64_t)b * p.nchunks + c]);
+        xs2[2 * b] = l;
+        xs2[2 * b + 1] = W;
+    }
+}
+
+// After X3: outputs, flags and the canonical (ascending request) fallback
+// queue, identical on every rank.  One block.
+__global__ void k_xfinish(const int32_t* x3, int B, int32_t* next_token, int32_t* req_flags, int32_t* fb_count,
+                          int32_t* fb_list, int32_t* dbg_flags, int certify) {
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        next_token[b] = x3[b];
+        const int32_t f = x3[B + b] | req_flags[b];
+        req_flags[b] = f;
+        if (dbg_flags) dbg_flags[b] = f & 0xff;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int n = 0;
+        if (certify)
+            for (int b = 0; b < B; ++b)
+                if (req_flags[b] & 0x100) fb_list[n++] = b;
+        *fb_count = n;
+    }
+}
+
+// In-place max over n rank buffers (nj_group's allreduce-MAX): dst = max_r src[r].
+__global__ void k_imax(const int32_t* src, int n, int len, int32_t* dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= len) return;
+    int32_t v = src[i];
+    for (int r = 1; r < n; ++r) v = max(v, src[(int64_t)r * len + i]);
+    dst[i] = v;
+}
+
+// ------------------------------------------------------------ fp64 fallback
+// FBX-1: per queued request, per row j: rank-local fp64 lse and the owned
+// draft logit (fb_logits from k_fb_logits over the local shard).
+__global__ void __launch_bounds__(256) k_fbx_stats(const FbParams p, const ReqMeta m, int slots, double* s4) {
+    __shared__ double sh[32];
+    const int nfb = __ldcg(p.fb_count);
+    const int V = p.V_local;
+    for (int k = blockIdx.x; k < nfb; k += gridDim.x) {
+        const int b = __ldcg(&p.fb_list[k]);
+        const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1;
+        for (int j = 0; j <= gam; ++j) {
+            const double* L = p.fb_logits + (int64_t)(ro + j) * V;
+            const double l = row_lse_d(L, V, sh);
+            if (threadIdx.x == 0) {
+                double dl = __longlong_as_double(0x7ff8000000000000ll);
+                if (j < gam) {
+                    const int x = p.draft_tokens[ro - b + j] - p.v_begin;
+                    if (x >= 0 && x < V) dl = L[x];
+                }
+                s4[((int64_t)k * slots + j) * 2] = l;
+                s4[((int64_t)k * slots + j) * 2 + 1] = dl;
+            }
+        }
+    }
+}
+
+// FBX-2: merged fp64 lse, acceptance (identical on every rank), local masses
+// of the residual / bonus distribution and of p_n (zero-mass rule R6).
+__global__ void __launch_bounds__(256) k_fbx_accept(const FbParams p, const ReqMeta m, const double* r4, int nranks,
+                                                    int slots, int qcap, double* s5, int32_t* fbn, double* fblse) {
+    __shared__ double sh[32];
+    __shared__ double s_lse;
+    __shared__ int s_n;
+    const int nfb = __ldcg(p.fb_count);
+    const int V = p.V_local;
+    for (int k = blockIdx.x; k < nfb; k += gridDim.x) {
+        const int b = __ldcg(&p.fb_list[k]);
+        const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
+        if (threadIdx.x == 0) {
+            int n = gam;
+            double lse_n = 0.0;
+            for (int i = 0; i <= gam; ++i) {
+                double dl;
+                const double lse = xmerge_lse(r4, nranks, qcap * slots, k * slots + i, dl);
+                if (i == gam) { lse_n = lse; break; }
+                const double pd = exp(dl - lse);
+                const double qx = (double)p.q[(int64_t)(g0 + i) * p.ldq + p.draft_tokens[g0 + i]];
+                if (!((double)p.u[ro + i] * qx < pd)) { n = i; lse_n = lse; break; }
+            }
+            s_n = n;
+            s_lse = lse_n;
+        }
+        __syncthreads();
+        const int n = s_n;
+        const double ln = s_lse;
+        const bool resid = n < gam;
+        const double* L = p.fb_logits + (int64_t)(ro + n) * V;
+        const float* qrow = p.q + (int64_t)(g0 + n) * p.ldq + p.v_begin;
+        double Wl = 0.0, Wp = 0.0;
+        for (int x = threadIdx.x; x < V; x += blockDim.x) {
+            const double pe = exp(L[x] - ln);
+            Wp += pe;
+            if (resid) { const double d = pe - (double)qrow[x]; Wl += d > 0.0 ? d : 0.0; }
+            else Wl += pe;
+        }
+        Wl = block_sum_d(Wl, sh);
+        Wp = block_sum_d(Wp, sh);
+        if (threadIdx.x == 0) {
+            s5[2 * k] = Wl;
+            s5[2 * k + 1] = Wp;
+            fbn[k] = n;
+            fblse[k] = ln;
+        }
+        __syncthreads();
+    }
+}
+
+// FBX-3: owner rank of the draw (prefix over ranks in rank order) scans its
+// local fp64 weights in ascending id.  x6[k] = global token or -1,
+// x6[qcap + k] = flag bits (2 zero mass, 4 clamp).
+__global__ void __launch_bounds__(256) k_fbx_locate(const FbParams p, const ReqMeta m, const double* r5, int nranks,
+                                                    int rank, int qcap, const int32_t* fbn, const double* fblse,
+                                                    int32_t* x6) {
+    __shared__ double sh[32];
+    __shared__ double s_t, sbase;
+    __shared__ int s_own, s_clamp, s_zero, st;
+    const int nfb = __ldcg(p.fb_count);
+    const int V = p.V_local;
+    for (int k = blockIdx.x; k < nfb; k += gridDim.x) {
+        const int b = __ldcg(&p.fb_list[k]);
+        const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
+        const int n = fbn[k];
+        const double ln = fblse[k];
+        if (threadIdx.x == 0) {
+            double Tot = 0.0;
+            for (int r = 0; r < nranks; ++r) Tot += r5[((int64_t)r * qcap + k) * 2];
+            const int zero = !(Tot > 0.0);
+            const int col = zero ? 1 : 0;
+            if (zero) { Tot = 0.0; for (int r = 0; r < nranks; ++r) Tot += r5[((int64_t)r * qcap + k) * 2 + 1]; }
+            const double T = (double)p.u[ro + gam] * Tot;
+            double P = 0.0;
+            int own = -1, last = -1;
+            double Pown = 0.0;
+            for (int r = 0; r < nranks; ++r) {
+                const double A = r5[((int64_t)r * qcap + k) * 2 + col];
+                if (A > 0.0) {
+                    last = r;
+                    if (own < 0 && T < P + A) { own = r; Pown = P; }
+                }
+                P += A;
+            }
+            int clamp = 0;
+            if (own < 0) { own = last; clamp = 1; }
+            s_own = own;
+            s_clamp = clamp;
+            s_zero = zero;
+            s_t = T - Pown;
+            sbase = 0.0;
+            st = 0x7fffffff;
+        }
+        __syncthreads();
+        const bool resid = (n < gam) && !s_zero;
+        if (s_own != rank) {
+            if (threadIdx.x == 0) { x6[k] = -1; x6[qcap + k] = 0; }
+            __syncthreads();
+            continue;
+        }
+        const double* L = p.fb_logits + (int64_t)(ro + n) * V;
+        const float* qrow = p.q + (int64_t)(g0 + n) * p.ldq + p.v_begin;
+        auto weight = [&](int x) -> double {
+            const double pe = exp(L[x] - ln);
+            if (!resid) return pe;
+            const double d = pe - (double)qrow[x];
+            return d > 0.0 ? d : 0.0;
+        };
+        const double T = s_t;
+        if (!s_clamp) {
+            for (int x0 = 0; x0 < V; x0 += blockDim.x) {
+                const int x = x0 + threadIdx.x;
+                const double w = x < V ? weight(x) : 0.0;
+                const double inc = warp_incl_scan_d(w);
+                double exc = __shfl_up_sync(0xffffffffu, inc, 1);
+                if (lane_id() == 0) exc = 0.0;
+                if (lane_id() == 31) sh[warp_id()] = inc;
+                __syncthreads();
+                double off = sbase;
+                for (int k2 = 0; k2 < (int)warp_id(); ++k2) off += sh[k2];
+                double tot = sbase;
+                for (int k2 = 0; k2 < (int)(blockDim.x / 32); ++k2) tot += sh[k2];
+                __syncthreads();
+                if (w > 0.0 && off + exc <= T && T < off + inc) atomicMin(&st, x);
+                if (threadIdx.x == 0) sbase = tot;
+                __syncthreads();
+                if (st != 0x7fffffff) break;
+            }
+        }
+        int clampf = s_clamp;
+        if (st == 0x7fffffff) {   // overshoot (R5): last positive weight of this (last positive) shard
+            clampf = 1;
+            if (threadIdx.x == 0) {
+                int lastx = 0;
+                for (int x = V - 1; x >= 0; --x)
+                    if (weight(x) > 0.0) { lastx = x; break; }
+                st = lastx;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            x6[k] = st + p.v_begin;
+            x6[qcap + k] = (s_zero ? 2 : 0) | (clampf ? 4 : 0);
+        }
+        __syncthreads();
+    }
+}
+
+// FBX-4: write the fallback's outputs (after the MAX exchange of x6).
+__global__ void k_fbx_write(const FbParams p, const int32_t* fbn, const int32_t* x6, int qcap) {
+    const int nfb = __ldcg(p.fb_count);
+    for (int k = threadIdx.x; k < nfb; k += blockDim.x) {
+        const int b = p.fb_list[k];
+        p.accept_len[b] = fbn[k];
+        p.next_token[b] = x6[k];
+        if (p.dbg_flags) p.dbg_flags[b] = 1 | x6[qcap + k];
+        p.req_flags[b] = 0;
+    }
+}
+
+}  // namespace nj

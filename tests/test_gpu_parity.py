@@ -257,3 +257,13 @@ def test_invalid_arguments():
         v.verify(b.hidden, b.W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, acc)
     with pytest.raises(NJError):   # B > max_batch
         v.verify(b.hidden, b.W, b.draft_tokens, b.draft_probs, np.array([1, 1, 1]), b.uniforms, acc, acc)
+
+
+@pytest.mark.parametrize("B,g", [(8, 3), (64, 3), (40, "mixed:5"), (96, 3)])
+def test_uncertified_decisions_full_size(B, g):
+    """Raw GEMM accuracy: with the certificate OFF every decision outside the
+    1e-6 tie band must still equal the oracle's (fused, staged, two-pass
+    paths by size)."""
+    b = make_batch(B, g, V=QV, d=QD, seed=B * 3 + 1, device=DEV, W=w_full())
+    acc, nxt, dd, v = run(b, certify=False)
+    check(b, acc, nxt, dd, lnp_tol=2e-5)
