@@ -41,7 +41,24 @@ CONFIGS = {
     "c3_b256_g5": (256, 5, "auto"),
     "c3_b256_mixed": (256, "mixed:5", "auto"),
     "c3_b16_g2": (16, 2, "auto"),
+    "c5": (256, 2, "auto"),                # BASELINE configs[4] (vocab-sharded run: bench_c5)
 }
+
+
+_OUT = None   # the real stdout: result lines only (stray library output goes to stderr)
+
+
+def emit(obj):
+    print(json.dumps(obj), file=_OUT or sys.stdout, flush=True)
+
+
+def _claim_stdout():
+    """Route fd 1 to stderr for the rest of the run (NCCL prints its version
+    banner to stdout) and keep the original stdout for the JSON lines."""
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
 
 def load_peaks():
@@ -150,30 +167,38 @@ def bench_reference(args, ws, rank):
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
                              "sample": f"{args.steps} single-request steps of the {args.config} batch"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
-def cpu_baseline(b, budget_s: float):
-    """Oracle on the bounded sample: the full batch, repeated up to budget_s."""
+def cpu_baseline(b, budget_s: float, max_requests: int | None = None):
+    """Oracle on the bounded sample: the batch (or its first max_requests
+    requests), repeated up to budget_s."""
+    import numpy as np
+
     import oracle
     n = b.to_numpy()
+    g = n["gamma"]
+    k = len(g) if max_requests is None else min(len(g), max_requests)
+    nr, nd = int((g[:k] + 1).sum()), int(g[:k].sum())
+    args = (n["hidden_bits"][:nr], n["W_bits"], n["draft_tokens"][:nd],
+            n["draft_probs"][:max(nd, 1)], g[:k], n["uniforms"][:nr])
     runs, t0 = 0, time.perf_counter()
     while True:
-        oracle.verify(n["hidden_bits"], n["W_bits"], n["draft_tokens"], n["draft_probs"], n["gamma"], n["uniforms"])
+        oracle.verify(*args)
         runs += 1
         if time.perf_counter() - t0 > budget_s or runs >= 20:
             break
     dt = time.perf_counter() - t0
-    return {"value": b.N * runs / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": f"{runs} full run(s) of one {b.B}-request batch ({b.N} positions), {dt:.1f} s"}
+    return {"value": nr * runs / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"{runs} full run(s) of {k} request(s) of the {b.B}-request batch ({nr} positions), {dt:.1f} s"}
 
 
 def bench_nj(args, ws, rank, local):
     import numpy as np
     import torch
 
-    from paper_2512_22420_b200 import (NJ_OPT_PATH, NJ_OPT_PROFILE, NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_TWOPASS,
-                                       Verifier)
+    from paper_2512_22420_b200 import (NJ_OPT_PATH, NJ_OPT_PROFILE, NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_STAGED,
+                                       NJ_PATH_TWOPASS, Verifier)
     from synth.inputs import make_batch, make_weight
 
     torch.cuda.set_device(local)
@@ -238,20 +263,32 @@ def bench_nj(args, ws, rank, local):
     positions = N * args.steps * ws
     value = positions / (t_max / 1e3)
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
-    # roofline of the dominant kernel: fused path -> HBM bytes; two-pass -> stats GEMM flops
+    # roofline of the dominant kernel (DESIGN.md §5 / §8): fused path -> HBM bytes;
+    # staged -> the one GEMM pass over N rows; two-pass -> K-A over the G draft rows.
+    # A GEMM over R rows is HBM-bound below the ridge (R < peak_flops / (hbm_bw)
+    # ~ 250 rows: algorithmic bytes = W + H) and tensor-bound above (2 R V d flops).
     kern_ms = kms / max(kn, 1)
     R_avg = rejected / args.steps
+    ridge = tf_burst * 1e12 / (hbm * 1e9)
     if p_used == NJ_PATH_FUSED:
         byts = 2 * V_Q * D_Q + 2 * N * D_Q + 4 * R_avg * V_Q + 8 * G + 4 * N
         achieved = byts / (kern_ms / 1e3) / 1e9
         roof = {"kernel": "k_fused_verify", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "algorithmic_bytes_per_launch": byts}
     else:
-        flops = 2.0 * G * V_Q * D_Q
-        peak = tf_burst
-        achieved = flops / (kern_ms / 1e3) / 1e12
-        roof = {"kernel": "k_gemm_rows<stats> (K-A)", "bound": "tensor", "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "algorithmic_flops_per_launch": flops}
+        R = N if p_used == NJ_PATH_STAGED else G / max(kn // args.steps, 1)
+        name = "k_gemm_big<logits,stats,capture> (staged, all N rows)" if p_used == NJ_PATH_STAGED else \
+            "k_gemm_big<stats,capture> (K-A, draft rows)"
+        if R < ridge:
+            byts = 2 * V_Q * D_Q + 2 * R * D_Q
+            achieved = byts / (kern_ms / 1e3) / 1e9
+            roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "algorithmic_bytes_per_launch": byts, "rows": R}
+        else:
+            flops = 2.0 * R * V_Q * D_Q
+            achieved = flops / (kern_ms / 1e3) / 1e12
+            roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
+                    "frac": achieved / tf_burst, "algorithmic_flops_per_launch": flops, "rows": R}
     roof["peak_source"] = peak_src
     roof["kernel_ms_avg"] = kern_ms
     roof["kernel_share_of_step"] = kms / ms if ms > 0 else None
@@ -296,14 +333,14 @@ def bench_nj(args, ws, rank, local):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"qwen7b_{args.config}", "B": B, "gamma": gamma, "N_per_step": N,
                        "d": D_Q, "V": V_Q, "global_batch": B * ws,
-                       "path": {NJ_PATH_FUSED: "fused", NJ_PATH_TWOPASS: "twopass"}[p_used],
+                       "path": PATH_NAMES[p_used],
                        "parallelism": f"request-sharded x{ws} (no data-path collective)",
                        "l2": "inputs larger than L2: W_lm (1.09 GB) streamed from HBM every step"},
             "accepted_tokens_per_s": acc_tok * ws / (t_max / 1e3),
             "realised_beta_tokens_per_request": acc_tok / (args.steps * B),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": int(launches * args.steps)}
-    print(json.dumps(line), flush=True)
+    emit(line)
     if ws > 1:
         dist.destroy_process_group()
 
@@ -375,7 +412,115 @@ def bench_c4(args, ws, rank, local):
             "gamma_histogram_per_B": hist,
             "select_gamma_us_median": statistics.median(sel_us),
             "bandit_snapshot_batches": len(bandit.snapshot()["batches"])}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+def bench_c5(args, ws, rank, local):
+    """BASELINE configs[4]: vocab-sharded LM head (B=256, gamma=2) over the
+    ranks of this job, libnj's own NCCL communicator for the three exchanges
+    per step.  Strong scaling: the same batch on every rank,
+    each rank streams V/G rows of W.  At N=1 the same code runs with a one-rank
+    communicator."""
+    import torch
+
+    from paper_2512_22420_b200 import NJ_OPT_PROFILE, NcclComm, Verifier, nccl_unique_id, shard_range
+    from paper_2512_22420_b200 import dist as njdist
+    from synth.inputs import make_batch, make_weight
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        comm = njdist.nccl_comm_for_world(local)
+    else:
+        comm = NcclComm(1, nccl_unique_id(), 0, local)
+    B, g = 256, 2
+    vb, ve = shard_range(V_Q, ws, rank)
+    Wf = make_weight(V_Q, D_Q, args.seed, dev)
+    b = make_batch(B, g, V=V_Q, d=D_Q, seed=args.seed, device=dev, W=Wf)
+    W = Wf[vb:ve].contiguous()
+    del Wf
+    torch.cuda.empty_cache()
+    v = Verifier(D_Q, V_Q, max_batch=B, gamma_max=g, device=local, v_begin=vb, v_end=ve, nccl_comm=comm.handle)
+    _, launches = v.plan(b.gamma)
+    acc = torch.empty(B, dtype=torch.int32, device=dev)
+    nxt = torch.empty(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    v.set_option(NJ_OPT_PROFILE, 1)
+    v.kernel_time(reset=True)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    kms, kn = v.kernel_time(reset=True)
+    v.set_option(NJ_OPT_PROFILE, 0)
+    t_max = njdist.max_over_ranks(ms, dev)
+    toks = int((acc + 1).sum().item())
+    hbm, tf_burst, _, peak_src = load_peaks()
+    kern_ms = kms / max(kn, 1)
+    flops = 2.0 * b.G * (ve - vb) * D_Q
+    roof = {"kernel": "k_gemm_big<stats> (K-A, draft rows, this rank's shard)", "bound": "tensor",
+            "achieved": flops / (kern_ms / 1e3) / 1e12, "peak": tf_burst, "unit": "TFLOP/s",
+            "frac": flops / (kern_ms / 1e3) / 1e12 / tf_burst, "algorithmic_flops_per_launch": flops,
+            "peak_source": peak_src, "kernel_ms_avg": kern_ms, "kernel_share_of_step": kms / ms, "traffic": None}
+    # end to end through nj_verify_host (pinned host inputs, copies inside the timed region)
+    pin = lambda t: t.cpu().pin_memory()
+    hh, th, qh, uh = pin(b.hidden), pin(b.draft_tokens), pin(b.draft_probs), pin(b.uniforms)
+    ah = torch.empty(B, dtype=torch.int32).pin_memory()
+    nh = torch.empty(B, dtype=torch.int32).pin_memory()
+    k_e2e = max(5, min(args.steps, 30))
+    for _ in range(2):
+        v.verify_host(hh, W, th, qh, b.gamma, uh, ah, nh)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(k_e2e):
+        v.verify_host(hh, W, th, qh, b.gamma, uh, ah, nh)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = njdist.max_over_ranks(s0.elapsed_time(s1), dev)
+    h2d = b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.G * b.draft_probs.shape[1] * 4 + b.N * 4
+    e2e = {"value": b.N * k_e2e / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(2 * B * 4), "steps": k_e2e, "api": "nj_verify_host"}
+    v.close()
+    comm.close()
+    if ws > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    cpu = None if args.no_cpu_baseline else cpu_baseline(_cpu_batch(b), args.cpu_budget, max_requests=8)
+    line = {"metric": METRIC, "value": b.N * args.steps / (t_max / 1e3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "qwen7b_c5_vocab_sharded", "B": B, "gamma": g, "N_per_step": b.N, "d": D_Q,
+                       "V": V_Q, "V_per_rank_max": max(shard_range(V_Q, ws, r)[1] - shard_range(V_Q, ws, r)[0]
+                                                      for r in range(ws)),
+                       "parallelism": f"vocab-sharded x{ws} (NCCL allgather x2 + allreduce-MAX per step)",
+                       "l2": "inputs larger than L2 at G <= 4; W shard streamed every step"},
+            "accepted_tokens_per_s": toks * args.steps / (t_max / 1e3),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": int(launches * args.steps)}
+    emit(line)
+    if ws > 1:
+        dist.destroy_process_group()
 
 
 PATH_NAMES = ["auto", "fused", "twopass", "staged"]
@@ -403,7 +548,7 @@ def bench_sweep(args, ws, rank, local):
             try:
                 path, launches = v.plan(b.gamma)
             except Exception as e:   # forced path not applicable at this point
-                print(json.dumps({"config": f"B{B}_g{g}", "skipped": str(e)}), flush=True)
+                emit({"config": f"B{B}_g{g}", "skipped": str(e)})
                 continue
             acc = torch.empty(B, dtype=torch.int32, device=dev)
             nxt = torch.empty(B, dtype=torch.int32, device=dev)
@@ -422,11 +567,11 @@ def bench_sweep(args, ws, rank, local):
             toks = int((acc + 1).sum().item())
             N = b.N
             t_star = max(2.0 * N * V_Q * D_Q / (tf_burst * 1e12), (2.0 * V_Q * D_Q + 2 * N * D_Q) / (hbm * 1e9))
-            print(json.dumps({"config": f"B{B}_g{g}", "B": B, "gamma": g, "N": N, "path": PATH_NAMES[path],
+            emit({"config": f"B{B}_g{g}", "B": B, "gamma": g, "N": N, "path": PATH_NAMES[path],
                               "us_per_step": ms * 1e3, "positions_per_s": N / (ms / 1e3),
                               "accepted_tokens_per_s": toks / (ms / 1e3), "roofline_us": t_star * 1e6,
                               "frac_of_roofline": t_star / (ms / 1e3), "dominant_kernel_us": kms / max(kn, 1) * 1e3,
-                              "launches": launches}), flush=True)
+                              "launches": launches})
             del v
 
 
@@ -442,7 +587,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="nj", choices=["nj", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c5"])
     ap.add_argument("--path", default=None, choices=[None] + PATH_NAMES)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -454,12 +599,16 @@ def main():
     ap.add_argument("--cprefill-scale", type=float, default=0.01)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    _claim_stdout()
     ws, rank, local = dist_setup()
     if args.sweep:
         bench_sweep(args, ws, rank, local)
         return
     if args.config == "c4":
         bench_c4(args, ws, rank, local)
+        return
+    if args.config == "c5" and args.impl != "reference":
+        bench_c5(args, ws, rank, local)
         return
     if args.impl == "reference":
         bench_reference(args, ws, rank)
