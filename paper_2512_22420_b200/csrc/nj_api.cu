@@ -107,6 +107,9 @@ struct nj_ctx {
     int pld = 0;        // row stride of the per-CTA softmax partials (>= every GEMM grid)
     int gemm_ks = 4;    // k_gemm_big: k-blocks per accumulator restart
     int gemm_acc = 0;   // 1: use the per-k-block-restart k_gemm_acc instead (A/B, NJ_GEMM=acc)
+    int gemm_cg = 0;    // k_gemm_big CTA group: 0 auto, 1 single CTA, 2 CTA pair (NJ_CG)
+    int gemm_pf = 0;    // k_gemm_big: W k-blocks prefetched into L2 ahead of the ring (NJ_PF)
+    int gemm_maxt = 256;  // k_gemm_big: max token chunk (NJ_BIG_MAXT)
     int U = 0;          // 16-row vocab units
     int max_tiles = 0;  // max 128-row tiles per CTA
     int nchunks = 0;    // sampler chunks
@@ -297,24 +300,36 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     // which must fit in TMEM next to the resident logits (max_tiles x NPAD).
     fp.scratch_col = c->max_tiles * NPAD;
     const int spare = 512 - fp.scratch_col;
-    int GK = std::min(4, spare / (2 * NPAD));
+    // One accumulator partial per 4-k-block ring stage (restart every 16 MMAs,
+    // the k_gemm_big accuracy) needs two NPAD-column groups of
+    // scratch TMEM; without room for them (NPAD = 48) a single buffer takes
+    // partials of 4 k-blocks with a per-partial handshake.
+    int GK = 4;
     fp.kpd = 1;
-    if (GK >= 2) {
+    fp.sacc = 1;
+    if (spare >= 2 * NPAD) {
         fp.ngroups = 2;
-        fp.nbuf = 2 * GK;
-    } else {   // no room for two groups (NPAD = 48): per-partial handshake, one
-        GK = 4;    // buffer, partials of 2 k-blocks (restart every 8 MMAs)
+        fp.nbuf = 2;
+    } else {
         fp.ngroups = 0;
         fp.nbuf = std::max(1, std::min(8, spare / NPAD));
-        fp.kpd = 2;
+        fp.kpd = 4;
     }
-    if (const char* e = getenv("NJ_KGROUP")) GK = std::max(1, atoi(e));   // tuning knobs
-    if (const char* e = getenv("NJ_KPD")) fp.kpd = std::max(1, atoi(e));
+    if (const char* e = getenv("NJ_KPD")) fp.kpd = std::max(1, atoi(e));   // tuning knobs
+    if (const char* e = getenv("NJ_SACC")) fp.sacc = atoi(e);
+    if (!fp.sacc && fp.ngroups > 0) {   // one partial per k-block: GK partial slots per group
+        GK = std::max(1, std::min(4, spare / (2 * NPAD)));
+        fp.nbuf = 2 * GK;
+    }
+    if (const char* e = getenv("NJ_KGROUP")) GK = std::max(1, atoi(e));
     const size_t stage2 = (size_t)GK * (kTileBytesA + NPAD * 128);
     const int S = (int)std::min<size_t>(8, (kSmemLimit - fused_tail(NPAD, 8) - 1024) / stage2);
     fp.nstages = S;
     fp.kgroup = GK;
-    fp.eps_acc = fp.kpd == 1 ? c->eps_acc_fused : 2.0f * c->eps_acc_fused;
+    // accuracy of the partials: restart every k-block -> 2e-6;
+    // every 2 -> 4e-6; every 3-4 k-blocks (<= 16 MMAs) -> the k_gemm_big margin
+    const int kspan = (fp.ngroups > 0 && fp.sacc) ? GK : fp.kpd;
+    fp.eps_acc = kspan == 1 ? c->eps_acc_fused : kspan == 2 ? 2.0f * c->eps_acc_fused : c->eps_acc;
     if (const char* e = getenv("NJ_PHASE_TS")) {
         if (*e == '1' && !c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
         fp.phase_ts = c->phase_ts;
@@ -407,12 +422,13 @@ nj_status launch_gemm_acc(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, 
 // LM-head GEMM of the staged / two-pass paths over R contiguous rows of h.
 // k_gemm_big (default) or, with NJ_GEMM=acc, the per-k-block-restart
 // k_gemm_acc (A/B only).  rr: deal (tile, chunk) items round-robin over
-// grid_rr = min(SMs, tiles) CTAs (forced on by the caller when several
-// launches must share one partial layout); otherwise the tile-balanced
-// vocab split over c->grid.  *grid_used = CTAs that wrote partials.
+// grid_rr = min(SMs, tiles) CTAs; otherwise the tile-balanced vocab split
+// over c->grid (CG = 1).  CTA pairs (CG = 2) always deal (tile pair, chunk)
+// items round-robin.  grid_force > 0: use that grid (several launches that
+// write one partial layout).  *grid_used = CTAs that wrote partials.
 template <bool WRITE, bool STATS, bool CAPTURE>
 nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, const GemmBigParams& in, bool rr,
-                        int* grid_used) {
+                        int* grid_used, int grid_force = 0) {
     if (R <= 0) return NJ_OK;
     if (c->gemm_acc) {
         if (rr) return set_err(c, NJ_EUNSUPPORTED, "NJ_GEMM=acc: no round-robin mode");
@@ -426,28 +442,74 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     }
     GemmBigParams gp = in;
     gp.R = R;
-    gp.nchunks = (R + kBigMaxT - 1) / kBigMaxT;
-    gp.chunk = round16((R + gp.nchunks - 1) / gp.nchunks);
+    // CTA pair (cta_group::2) unless forced off or the token chunk is tiny
+    const int CG = c->gemm_cg == 2 ? 2 : 1;
+    gp.nchunks = (R + c->gemm_maxt - 1) / c->gemm_maxt;
+    gp.chunk = (R + gp.nchunks - 1) / gp.nchunks;
+    gp.chunk = CG == 2 ? (gp.chunk + 31) & ~31 : round16(gp.chunk);   // pair: each CTA a multiple-of-16 half
     gp.V_local = c->V_local;
     gp.U = c->U;
     gp.num_kb = (c->cfg.d + kBK - 1) / kBK;
     gp.v_begin = c->cfg.v_begin;
     gp.part_ld = c->pld;
     gp.ntiles_g = (c->V_local + kTileV - 1) / kTileV;
-    gp.rr = rr ? 1 : 0;
-    const int grid = rr ? std::max(1, std::min(c->num_sms, gp.ntiles_g)) : c->grid;
+    gp.rr = (rr || gp.nchunks > 1) ? 1 : 0;
+    int grid;
+    if (CG == 2) {
+        // pairs take (tile pair, chunk) items round-robin; as few pairs as give the same max load
+        const int items = (gp.ntiles_g + 1) / 2 * gp.nchunks;
+        const int np0 = std::max(1, std::min(c->num_sms / 2, items));
+        const int ipp = (items + np0 - 1) / np0;
+        grid = 2 * ((items + ipp - 1) / ipp);
+    } else {
+        grid = gp.rr ? std::max(1, std::min(c->num_sms, gp.ntiles_g)) : c->grid;
+    }
+    // several launches writing one partial layout share the first launch's grid
+    // (CTAs without items write (-inf, 0) partials)
+    if (grid_force > 0) grid = CG == 2 ? (grid_force + 1) & ~1 : grid_force;
     gp.gk = (gp.nchunks == 1 && gp.chunk <= 128) ? 2 : 1;
+    if (const char* e = getenv("NJ_BIG_GK")) gp.gk = std::max(1, atoi(e));
     gp.ks = std::max(gp.gk, (c->gemm_ks + gp.gk - 1) / gp.gk * gp.gk);
+    gp.pf = c->gemm_pf;
+    gp.dbg = 0;
+    if (const char* e = getenv("NJ_BIG_DBG")) gp.dbg = atoi(e);
+    gp.spin = 0;
+    if (const char* e = getenv("NJ_SPIN")) gp.spin = atoi(e);
+    gp.sleep_ns = 0;
+    if (const char* e = getenv("NJ_SLEEP")) gp.sleep_ns = atoi(e);
+    gp.ts = nullptr;
+    if (const char* e = getenv("NJ_PHASE_TS")) {
+        if (*e == '1' && !c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
+        gp.ts = c->phase_ts;
+    }
     CUtensorMap tmH;
-    if (!encode_2d(&tmH, h, R, c->cfg.d, gp.chunk)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
-    const size_t stage = (size_t)gp.gk * (kTileBytesA + (size_t)gp.chunk * 128);
+    if (!encode_2d(&tmH, h, R, c->cfg.d, gp.chunk / CG))
+        return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
+    const size_t stage = (size_t)gp.gk * (kTileBytesA + (size_t)(gp.chunk / CG) * 128);
     size_t tail = 4 * 4 * kBigNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 4) * 8 + 8;
-    const int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
+    int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
+    if (const char* e = getenv("NJ_BIG_S")) S = std::min(S, std::max(2, atoi(e)));
     if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_big: not enough shared memory (R=%d)", R);
     gp.nstages = S;
     const size_t smem = (size_t)S * stage + tail;
-    k_gemm_big<WRITE, STATS, CAPTURE><<<grid, kBigThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
+    if (CG == 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kBigThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        NJ_CUDA(c, cudaLaunchKernelEx(&cfg, k_gemm_big<WRITE, STATS, CAPTURE, 2>, c->tmW128, c->tmW16, tmH, gp));
+    } else {
+        k_gemm_big<WRITE, STATS, CAPTURE, 1><<<grid, kBigThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
+    }
     NJ_LAUNCHED(c, "k_gemm_big", st);
     if (grid_used) *grid_used = grid;
     return NJ_OK;
@@ -642,7 +704,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
                 std::pair<cudaEvent_t, cudaEvent_t> ev;
                 if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
                 if ((s = launch_lmhead<false, true, true>(c, st, c->hd + (size_t)r0 * c->cfg.d, R, gp, rrA,
-                                                          &a.gridA)) != NJ_OK)
+                                                          &a.gridA, r0 > 0 ? a.gridA : 0)) != NJ_OK)
                     return s;
                 if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
             }
@@ -835,6 +897,9 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     c->pld = std::max(c->grid, c->num_sms);
     if (const char* e = getenv("NJ_GEMM")) c->gemm_acc = strcmp(e, "acc") == 0;
     if (const char* e = getenv("NJ_KS")) c->gemm_ks = std::max(1, atoi(e));
+    if (const char* e = getenv("NJ_CG")) c->gemm_cg = atoi(e);
+    if (const char* e = getenv("NJ_PF")) c->gemm_pf = std::max(0, atoi(e));
+    if (const char* e = getenv("NJ_BIG_MAXT")) c->gemm_maxt = std::min(256, std::max(32, atoi(e)));
     const size_t g = (size_t)c->grid, gp_ = (size_t)c->pld;
 #define A(ptr, n) if ((s = alloc(c, &c->ptr, (n))) != NJ_OK) { nj_destroy(c); return s; }
     A(part_m, (size_t)c->Nmax * gp_);
@@ -874,9 +939,12 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_gemm_acc<false, true, true>);
     e = e ? e : set_smem_attr(k_gemm_acc<true, true, false>);
     e = e ? e : set_smem_attr(k_gemm_acc<true, true, true>);
-    e = e ? e : set_smem_attr(k_gemm_big<false, true, true>);
-    e = e ? e : set_smem_attr(k_gemm_big<true, true, false>);
-    e = e ? e : set_smem_attr(k_gemm_big<true, true, true>);
+    e = e ? e : set_smem_attr(k_gemm_big<false, true, true, 1>);
+    e = e ? e : set_smem_attr(k_gemm_big<true, true, false, 1>);
+    e = e ? e : set_smem_attr(k_gemm_big<true, true, true, 1>);
+    e = e ? e : set_smem_attr(k_gemm_big<false, true, true, 2>);
+    e = e ? e : set_smem_attr(k_gemm_big<true, true, false, 2>);
+    e = e ? e : set_smem_attr(k_gemm_big<true, true, true, 2>);
     if (e != cudaSuccess) {
         nj_destroy(c);
         return set_err(nullptr, NJ_ECUDA, "cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
@@ -1065,7 +1133,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
                 std::pair<cudaEvent_t, cudaEvent_t> ev;
                 if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
                 if ((s = launch_lmhead<false, true, true>(c, st, c->hd + (size_t)r0 * c->cfg.d, R, gp, rrA,
-                                                          &gridA)) != NJ_OK)
+                                                          &gridA, r0 > 0 ? gridA : 0)) != NJ_OK)
                     return s;
                 if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
             }

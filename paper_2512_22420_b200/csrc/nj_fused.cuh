@@ -251,7 +251,9 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
                     const int kb = kg * GK + g;
                     uint32_t dt;
                     if (NGRP > 0) {
-                        dt = tbase + scol + (uint32_t)((grp * GK + g) * NPAD);
+                        // sacc: the stage's GK k-blocks accumulate into ONE partial
+                        // (restart every GK k-blocks); else one partial per k-block
+                        dt = tbase + scol + (uint32_t)((p.sacc ? grp : grp * GK + g) * NPAD);
                     } else {
                         if (kin == 0) { mbar_wait(&pempty[buf], bph ^ 1); tc_fence_after(); }
                         dt = tbase + scol + (uint32_t)(buf * NPAD);
@@ -261,7 +263,7 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
                     const uint64_t bd = sdesc_sw128(sB + slot * kBBytes);
 #pragma unroll
                     for (int k = 0; k < kBK / 16; ++k)
-                        mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                        mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, ((NGRP > 0 && p.sacc ? g : kin) | k) != 0);
                     if (NGRP == 0 && (++kin == kpd || kb + 1 == p.num_kb)) {
                         mma_commit(&pfull[buf]);
                         kin = 0;
@@ -309,9 +311,9 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
                     float ssum[NC];
 #pragma unroll
                     for (int j = 0; j < NC; ++j) ssum[j] = 0.f;
-                    for (int g = 0; g < ng; ++g) {
+                    for (int g = 0; g < (p.sacc ? 1 : ng); ++g) {
                         float v[NC];
-                        ld_cols<NC>(lane_base + scol + (uint32_t)((grp * GK + g) * NPAD), v);
+                        ld_cols<NC>(lane_base + scol + (uint32_t)((p.sacc ? grp : grp * GK + g) * NPAD), v);
 #pragma unroll
                         for (int j = 0; j < NC; ++j) ssum[j] += v[j];
                     }

@@ -267,6 +267,7 @@ struct FusedParams {
     int32_t V_local, v_begin, U, num_kb, nstages;
     int32_t nbuf, scratch_col;   // scratch accumulators: nbuf x NPAD columns at scratch_col
     int32_t kpd;                 // k-blocks per drained partial (accuracy: 1)
+    int32_t sacc;                // grouped mode: 1 = one partial per ring stage (restart every GK k-blocks)
     int32_t kgroup;              // k-blocks per TMA ring stage
     int32_t ngroups;             // >0: drain handshake per ring stage with ngroups x kgroup scratch buffers
     unsigned long long* phase_ts; // debug: [grid][8] %globaltimer stamps at phase boundaries (NULL: off)

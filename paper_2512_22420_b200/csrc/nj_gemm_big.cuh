@@ -24,6 +24,12 @@
 //     132 x 917 KB of W live and re-read W ~9x from HBM at 10 chunks);
 //   * with one chunk (N <= 256, HBM-bound) the tile-balanced contiguous vocab
 //     split of the fused kernel is kept (W streamed once, evict_first).
+// CG = 2 (CTA pair, cta_group::2): the two CTAs of a cluster own vocab tiles
+// 2t and 2t+1 and each loads only HALF of the H chunk; the leader issues
+// 256 x N MMAs that read A from both CTAs and B halves from both, each CTA's
+// TMEM holds its 128 vocab rows x N.  Per SM and k-block the TMA stream drops
+// from 16 KB W + 32 KB H to 16 + 16 KB -- the L2->SM operand stream, not the
+// tensor pipe, is what limits CG = 1 above the ridge.
 // The certificate margins of the paths that use this kernel are set from its
 // measured error.
 #pragma once
@@ -49,12 +55,20 @@ struct GemmBigParams {
     const int32_t* tok;                  // CAPTURE: [R] global ids (or draft_tokens with use_row_g)
     double* dl;                          // CAPTURE: [R] (or [G] with use_row_g)
     int32_t w_evict_first;
+    int32_t pf;                          // W k-blocks prefetched into L2 ahead of the TMA ring (0: off)
+    int32_t spin;                        // 1: producer / MMA threads poll (test_wait); 2: epilogue too
+    int32_t sleep_ns;                    // epilogue accumulator waits: nanosleep backoff (0: try_wait)
+    unsigned long long* ts;              // debug timeline of CTA 0 (NJ_PHASE_TS): [0,4K) producer stage
+                                         // starts, [4K,8K) MMA stage starts, [8K,12K) epilogue group ends
+    int32_t dbg;                         // bottleneck probes (NJ_BIG_DBG): 1 no MMAs, 2 no TMEM drain,
+                                         // 4 no TMA loads, 8 no per-item epilogue output
+                                         // (results are garbage; timing only)
     int32_t use_row_g;                   // staged path: row r is draft row_g[r] (-1: bonus row)
     int32_t row_g[kBigMaxRowG];
 };
 
-// Work item `it` of CTA `cta`: vocab rows [row0, row0 + trows) of the local
-// shard, token chunk c.  Returns false past the CTA's last item.
+// Work item `it` of CTA `cta` (CG = 1): vocab rows [row0, row0 + trows) of
+// the local shard, token chunk c.  Returns false past the CTA's last item.
 __device__ __forceinline__ bool big_item(const GemmBigParams& p, int cta, int grid, int r0, int rows, int it,
                                          int& row0, int& trows, int& c) {
     if (p.rr) {
@@ -75,13 +89,37 @@ __device__ __forceinline__ bool big_item(const GemmBigParams& p, int cta, int gr
     return true;
 }
 
-template <bool WRITE, bool STATS, bool CAPTURE>
+// Work item `it` of CTA pair `pid` (CG = 2): tile pair tp (tiles 2tp, 2tp+1),
+// chunk c.  rank's tile: valid rows `trows` (0 past the last tile, whose CTA
+// then loads the last real tile and discards the result), load rows
+// [row0L, row0L + trowsL); trowsP = the peer's load rows (expect-tx bytes).
+__device__ __forceinline__ void big_pair_tile(const GemmBigParams& p, int tile, int& row0, int& trows, int& row0L,
+                                              int& trowsL) {
+    row0 = tile * kTileV;
+    trows = max(0, min(kTileV, p.V_local - row0));
+    row0L = trows > 0 ? row0 : (p.ntiles_g - 1) * kTileV;
+    trowsL = min(kTileV, p.V_local - row0L);
+}
+__device__ __forceinline__ bool big_item2(const GemmBigParams& p, int pid, int npairs, int crank, int it, int& row0,
+                                          int& trows, int& row0L, int& trowsL, int& trowsP, int& c) {
+    const int ntp = (p.ntiles_g + 1) >> 1;
+    const int i = pid + it * npairs;
+    if (i >= ntp * p.nchunks) return false;
+    const int tp = i / p.nchunks;
+    c = i - tp * p.nchunks;
+    big_pair_tile(p, 2 * tp + crank, row0, trows, row0L, trowsL);
+    int a, b, d;
+    big_pair_tile(p, 2 * tp + (crank ^ 1), a, b, d, trowsP);
+    return true;
+}
+
+template <bool WRITE, bool STATS, bool CAPTURE, int CG>
 __global__ void __launch_bounds__(kBigThreads, 1)
 k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ CUtensorMap tmW16,
            const __grid_constant__ CUtensorMap tmH, const GemmBigParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.nstages, GK = p.gk;
-    const int bBytes = p.chunk * 128;                                 // H box per k-block
+    const int bBytes = (p.chunk / CG) * 128;                          // this CTA's H box per k-block
     const size_t stageBytes = (size_t)GK * (kTileBytesA + bBytes);
     uint8_t* ring = smem;                                             // S x GK x (A 16 KB | B bBytes)
     float2* scratch = reinterpret_cast<float2*>(ring + (size_t)S * stageBytes);   // [4 e][4 q][64]
@@ -97,20 +135,36 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
 
     const int warp = (int)warp_id(), lane = (int)lane_id();
     const int grid = gridDim.x, cta = blockIdx.x;
+    const int crank = CG == 2 ? (int)cluster_ctarank() : 0;
+    const bool leader = crank == 0;
+    const int pid = CG == 2 ? (int)cluster_id_x() : cta;
+    const int npairs = CG == 2 ? (int)nclusters_x() : grid;
     int r0 = 0, rows = 0;
-    if (!p.rr) vocab_range(p.U, grid, cta, p.V_local, r0, rows);
+    if (CG == 1 && !p.rr) vocab_range(p.U, grid, cta, p.V_local, r0, rows);
     const int ngk = (p.num_kb + GK - 1) / GK;          // ring stages per item
+    // one item's tiles: valid rows (this CTA), load rows (this CTA, peer), chunk
+    auto next_item = [&](int it, int& row0, int& trows, int& row0L, int& trowsL, int& trowsP, int& c) -> bool {
+        if (CG == 2) return big_item2(p, pid, npairs, crank, it, row0, trows, row0L, trowsL, trowsP, c);
+        if (!big_item(p, cta, grid, r0, rows, it, row0, trows, c)) return false;
+        row0L = row0;
+        trowsL = trows;
+        trowsP = 0;
+        return true;
+    };
 
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmW128);
         tma_prefetch_desc(&tmW16);
         tma_prefetch_desc(&tmH);
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int g = 0; g < 2; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kBigEpiWarps); }
+        for (int g = 0; g < 2; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kBigEpiWarps * CG); }
         fence_barrier_init();
         fence_proxy_async();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    if (warp == 1) {
+        if (CG == 2) tmem_alloc_cg2(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     if (STATS)
         for (int i = threadIdx.x; i < p.R; i += kBigThreads) state[i] = make_float2(-INFINITY, 0.f);
     if (CAPTURE)
@@ -119,99 +173,170 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
             else stok[i] = p.tok[i] - p.v_begin;
         }
     tc_fence_before();
-    __syncthreads();
+    if (CG == 2) cluster_sync_all();   // peer barriers initialised before any remote signal
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ------------------------------------------------ TMA producer
+            // ------------------------------------------------ TMA producer (both CTAs)
             const uint64_t pol_w = p.w_evict_first ? policy_evict_first() : policy_evict_last();
             const uint64_t pol_h = policy_evict_last();
-            int s = 0;
+            int s = 0, pst = 0;
             uint32_t ph = 0;
-            int row0, trows, c;
-            for (int it = 0; big_item(p, cta, grid, r0, rows, it, row0, trows, c); ++it) {
+            int row0, trows, row0L, trowsL, trowsP, c;
+            // L2 prefetch cursor (item pit, k-block pkb), p.pf k-blocks ahead of the loads
+            int pit = 0, pkb = 0, prow = 0, pvalid = 0;
+            {
+                int a0, a1, a2, a3, a4;
+                pvalid = next_item(0, a0, a1, prow, a2, a3, a4);
+            }
+            auto prefetch_to = [&](int it_lim, int kb_lim) {   // advance the cursor to (it_lim, kb_lim)
+                while (pvalid && (pit < it_lim || (pit == it_lim && pkb < kb_lim))) {
+                    tma_prefetch_l2_2d(&tmW128, pkb * kBK, prow);
+                    if (++pkb == p.num_kb) {
+                        pkb = 0;
+                        ++pit;
+                        int a0, a1, a2, a3, a4;
+                        pvalid = next_item(pit, a0, a1, prow, a2, a3, a4);
+                    }
+                }
+            };
+            for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
+                const int hrow = c * p.chunk + crank * (p.chunk / CG);
                 for (int kg = 0; kg < ngk; ++kg) {
                     const int ng = min(GK, p.num_kb - kg * GK);
-                    mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)ng * (w_tile_bytes(trows) + (uint32_t)bBytes));
+                    if (p.pf > 0) {
+                        const int ahead = kg * GK + p.pf;
+                        prefetch_to(it + ahead / p.num_kb, ahead % p.num_kb);
+                    }
+                    if (p.ts && cta == 0 && pst < 4096) p.ts[pst] = globaltimer();
+                    ++pst;
+                    if (p.spin) mbar_wait_spin(&empty[s], ph ^ 1);
+                    else mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = ring + (size_t)s * stageBytes;
-                    for (int g = 0; g < ng; ++g) {
-                        const int kb = kg * GK + g;
-                        load_w_tile(st + (size_t)g * kTileBytesA, &tmW128, &tmW16, &full[s], kb, row0, trows,
-                                    pol_w);
-                        tma_load_2d(st + (size_t)GK * kTileBytesA + (size_t)g * bBytes, &tmH, &full[s], kb * kBK,
-                                    c * p.chunk, pol_h);
+                    if (p.dbg & 4) {
+                        if (leader) mbar_arrive(&full[s]);
+                    } else if (CG == 1) {
+                        mbar_arrive_expect_tx(&full[s], (uint32_t)ng * (w_tile_bytes(trowsL) + (uint32_t)bBytes));
+                        for (int g = 0; g < ng; ++g) {
+                            const int kb = kg * GK + g;
+                            load_w_tile(st + (size_t)g * kTileBytesA, &tmW128, &tmW16, &full[s], kb, row0L, trowsL,
+                                        pol_w);
+                            tma_load_2d(st + (size_t)GK * kTileBytesA + (size_t)g * bBytes, &tmH, &full[s], kb * kBK,
+                                        hrow, pol_h);
+                        }
+                    } else {
+                        // both CTAs' bytes complete on the LEADER's full[s]
+                        if (leader)
+                            mbar_arrive_expect_tx(&full[s], (uint32_t)ng * (w_tile_bytes(trowsL) + w_tile_bytes(trowsP) +
+                                                                            2u * (uint32_t)bBytes));
+                        const uint32_t fb = mapa_shared(&full[s], 0);
+                        for (int g = 0; g < ng; ++g) {
+                            const int kb = kg * GK + g;
+                            uint8_t* dA = st + (size_t)g * kTileBytesA;
+                            if (trowsL == kTileV) {
+                                tma_load_2d_cg2(dA, &tmW128, fb, kb * kBK, row0L, pol_w);
+                            } else {
+                                const int nl = (trowsL + 15) >> 4;
+                                for (int l = 0; l < nl; ++l)
+                                    tma_load_2d_cg2(dA + l * 2048, &tmW16, fb, kb * kBK, row0L + 16 * l, pol_w);
+                            }
+                            tma_load_2d_cg2(st + (size_t)GK * kTileBytesA + (size_t)g * bBytes, &tmH, fb, kb * kBK,
+                                            hrow, pol_h);
+                        }
                     }
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ------------------------------------------------ MMA issuer
+        if (lane == 0 && leader) {
+            // ------------------------------------------------ MMA issuer (leader CTA)
             int s = 0;
             uint32_t ph = 0;
             int ngrp = 0;   // accumulator groups issued (buffer ngrp & 1, phase (ngrp >> 1) & 1)
-            int row0, trows, c;
-            for (int it = 0; big_item(p, cta, grid, r0, rows, it, row0, trows, c); ++it) {
+            int mst = 0;
+            int row0, trows, row0L, trowsL, trowsP, c;
+            for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
                 const int ncol = min(p.chunk, p.R - c * p.chunk);
-                const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)((ncol + 15) & ~15));
+                const uint32_t nmma = CG == 2 ? (uint32_t)p.chunk : (uint32_t)((ncol + 15) & ~15);
+                const uint32_t idesc = idesc_bf16_f32(128 * CG, nmma);
                 int kin = 0;   // k-blocks into the current accumulator group
                 uint32_t dt = 0;
                 for (int kg = 0; kg < ngk; ++kg) {
                     const int ng = min(GK, p.num_kb - kg * GK);
-                    mbar_wait(&full[s], ph);
+                    if (p.spin) mbar_wait_spin(&full[s], ph);
+                    else mbar_wait(&full[s], ph);
+                    if (p.ts && cta == 0 && mst < 4096) p.ts[4096 + mst] = globaltimer();
+                    ++mst;
                     tc_fence_after();
                     uint8_t* st = ring + (size_t)s * stageBytes;
                     for (int g = 0; g < ng; ++g) {
                         if (kin == 0) {
                             const int buf = ngrp & 1;
-                            mbar_wait(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
+                            if (p.spin) mbar_wait_spin(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
+                            else mbar_wait(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
                             tc_fence_after();
                             dt = tbase + (uint32_t)(buf * kBigMaxT);
                         }
                         const uint64_t ad = sdesc_sw128(st + (size_t)g * kTileBytesA);
                         const uint64_t bd = sdesc_sw128(st + (size_t)GK * kTileBytesA + (size_t)g * bBytes);
+                        if (!(p.dbg & 1)) {
 #pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k)
-                            mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                            for (int k = 0; k < kBK / 16; ++k) {
+                                if (CG == 2) mma_bf16_cg2(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                                else mma_bf16(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                            }
+                        }
                         const int kb = kg * GK + g;
                         if (++kin == p.ks || kb == p.num_kb - 1) {
-                            mma_commit(&afull[ngrp & 1]);
+                            if (p.dbg & 16) mbar_arrive(&afull[ngrp & 1]);
+                            else if (CG == 2) mma_commit_mc2(&afull[ngrp & 1], 3);
+                            else mma_commit(&afull[ngrp & 1]);
                             ++ngrp;
                             kin = 0;
                         }
                     }
-                    mma_commit(&empty[s]);
+                    if (p.dbg & 16) mbar_arrive(&empty[s]);   // probe (CG = 1, no MMAs): plain arrive
+                    else if (CG == 2) mma_commit_mc2(&empty[s], 3);
+                    else mma_commit(&empty[s]);
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
         }
     } else {
-        // ------------------------------------------------ epilogue (16 warps)
+        // ------------------------------------------------ epilogue (16 warps per CTA)
         const int q = warp & 3;             // TMEM lane quadrant this warp may access
         const int e = (warp - 2) >> 2;      // 64-column slice
-        const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(e * kBigNC);
+        // column slice per warp: the chunk's columns spread over the 4 warps of a
+        // lane quadrant (16..64 columns), so small chunks still drain with all 16 warps
+        const int cw = min(kBigNC, max(16, ((p.chunk + 3) / 4 + 15) & ~15));
+        const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(e * cw);
         const int vr = q * 32 + lane;
         const uint64_t pol_keep = policy_evict_last();   // staged logits stay in L2 for the sampler
         const int ngroups = (p.num_kb + p.ks - 1) / p.ks;
+        uint32_t aempty_cl[2] = {0u, 0u};
+        if (CG == 2) { aempty_cl[0] = mapa_shared(&aempty[0], 0); aempty_cl[1] = mapa_shared(&aempty[1], 0); }
         int ngrp = 0;
-        int row0, trows, c;
-        for (int it = 0; big_item(p, cta, grid, r0, rows, it, row0, trows, c); ++it) {
+        int row0, trows, row0L, trowsL, trowsP, c;
+        for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
             const int c0 = c * p.chunk;
             const int ncol = min(p.chunk, p.R - c0);
-            const int myc = ncol - e * kBigNC;   // columns of this warp's slice that exist (may be <= 0)
+            const int myc = min(cw, ncol - e * cw);   // columns of this warp's slice that exist (may be <= 0)
             float acc[kBigNC];
 #pragma unroll
             for (int j = 0; j < kBigNC; ++j) acc[j] = 0.f;
             for (int g = 0; g < ngroups; ++g, ++ngrp) {
                 const int buf = ngrp & 1;
-                mbar_wait(&afull[buf], (ngrp >> 1) & 1);
+                if (p.sleep_ns > 0) mbar_wait_sleep(&afull[buf], (ngrp >> 1) & 1, (uint32_t)p.sleep_ns);
+                else if (p.spin & 2) mbar_wait_spin(&afull[buf], (ngrp >> 1) & 1);
+                else mbar_wait(&afull[buf], (ngrp >> 1) & 1);
                 tc_fence_after();
                 const uint32_t ta = lane_base + (uint32_t)(buf * kBigMaxT);
-                if (myc > 32) {
+                if (p.dbg & 2) {
+                } else if (myc > 32) {
                     float v[32];
                     tmem_ld32(ta, v);
 #pragma unroll
@@ -232,14 +357,19 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&aempty[buf]);
+                if (p.ts && cta == 0 && warp == 2 && lane == 0 && ngrp < 4096) p.ts[8192 + ngrp] = globaltimer();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(aempty_cl[buf]);
+                    else mbar_arrive(&aempty[buf]);
+                }
             }
+            if (p.dbg & 8) continue;   // probe: no per-item output work
             const bool valid = vr < trows;
             const int xl = row0 + vr;
 #pragma unroll
             for (int j = 0; j < kBigNC; ++j) {
                 if (j < myc) {
-                    const int row = c0 + e * kBigNC + j;
+                    const int row = c0 + e * cw + j;
                     if (WRITE && valid) st_evict_last(&p.logits[(int64_t)row * p.ld_out + xl], acc[j], pol_keep);
                     if (CAPTURE && valid && stok[row] == xl) p.dl[p.use_row_g ? p.row_g[row] : row] = (double)acc[j];
                 }
@@ -251,6 +381,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 if (myc > 0) {
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
+                        if (hh * 32 >= myc) break;
                         float tm[32], ts[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
@@ -266,7 +397,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 named_bar(1 + e, 128);
                 const int ht = ((warp - 2) & 3) * 32 + lane;   // 0..127 within the slice's 4 warps
                 if (ht < kBigNC && ht < myc) {
-                    const int col = c0 + e * kBigNC + ht;
+                    const int col = c0 + e * cw + ht;
                     float2 st = state[col];
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
@@ -287,5 +418,10 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tbase, 512);
+    if (CG == 2) {
+        cluster_sync_all();   // no CTA of the pair exits / frees TMEM while the other may still signal it
+        if (warp == 1) tmem_dealloc_cg2(tbase, 512);
+    } else if (warp == 1) {
+        tmem_dealloc(tbase, 512);
+    }
 }

@@ -105,7 +105,7 @@ def test_fused_c2_full_size():
     for seed in range(4):
         b = make_batch(8, 3, V=QV, d=QD, seed=100 + seed, device=DEV, W=W)
         acc, nxt, dd, _ = run(b)
-        ties += check(b, acc, nxt, dd, lnp_tol=1e-5, lse_tol=5e-6)
+        ties += check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)   # 16-MMA partials, DESIGN.md §6
 
 
 @pytest.mark.parametrize("B,g", [(8, "mixed:5"), (1, 0), (48, 0), (16, 2), (12, 3), (6, 5), (24, 1)])
@@ -114,7 +114,7 @@ def test_fused_shapes_full_size(B, g):
     if b.N > 48:
         pytest.skip("fused path is N <= 48")
     acc, nxt, dd, v = run(b, NJ_PATH_FUSED)
-    check(b, acc, nxt, dd, lnp_tol=1e-5, lse_tol=5e-6)
+    check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
 
 
 @pytest.mark.parametrize("V,d", [(1000, 64), (4096, 256), (777, 40), (16, 8)])
