@@ -318,9 +318,14 @@ def bench_nj(args, ws, rank, local):
         s1.record(stream)
         torch.cuda.synchronize()
         e_ms = s0.elapsed_time(s1)
-        h2d = b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.G * b.draft_probs.shape[1] * 4 + b.N * 4
+        # bytes that cross the host link per step: the copied hidden / tokens / uniforms,
+        # plus the draft-probability bytes the kernels read in place (zero copy):
+        # q_i(x_i) of every draft and the sample row of every rejected request
+        rej0 = per_batch[0][1]
+        h2d = (b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.N * 4 + b.G * 4 + rej0 * V_Q * 4)
         e2e = {"value": N * k_e2e * ws / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(2 * B * 4), "steps": k_e2e, "api": "nj_verify_host"}
+               "d2h_bytes_per_step": int(2 * B * 4), "steps": k_e2e, "api": "nj_verify_host",
+               "q_rows": "read in place from pinned host memory (NJ_OPT_Q_ZERO_COPY)"}
     if ws > 1:
         dist.barrier()
     if rank != 0:
@@ -496,9 +501,11 @@ def bench_c5(args, ws, rank, local):
     s1.record(stream)
     torch.cuda.synchronize()
     e_ms = njdist.max_over_ranks(s0.elapsed_time(s1), dev)
-    h2d = b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.G * b.draft_probs.shape[1] * 4 + b.N * 4
+    rej = int((acc.cpu().numpy() < b.gamma).sum())
+    h2d = b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.N * 4 + b.G * 4 + rej * (ve - vb) * 4
     e2e = {"value": b.N * k_e2e / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(2 * B * 4), "steps": k_e2e, "api": "nj_verify_host"}
+           "d2h_bytes_per_step": int(2 * B * 4), "steps": k_e2e, "api": "nj_verify_host",
+           "q_rows": "read in place from pinned host memory (NJ_OPT_Q_ZERO_COPY); bytes per rank"}
     v.close()
     comm.close()
     if ws > 1:

@@ -132,9 +132,11 @@ nj_status nj_verify(nj_ctx* ctx, void* stream,
 
 /* End-to-end variant: every per-step input and output is a HOST pointer
  * (pinned memory recommended); W_lm stays a resident device pointer (model
- * weight).  Copies the inputs into ctx staging buffers on `stream`, runs
- * nj_verify, copies accept_len / next_token back and synchronises `stream`
- * before returning.  ldq as above (host row pitch). */
+ * weight).  Copies hidden / draft_tokens / uniforms into ctx staging buffers
+ * on `stream`; draft_probs_h is read in place by the kernels when it is
+ * pinned and mapped (UVA; NJ_OPT_Q_ZERO_COPY), else copied; runs nj_verify,
+ * copies accept_len / next_token back and synchronises `stream` before
+ * returning.  ldq as above (host row pitch). */
 nj_status nj_verify_host(nj_ctx* ctx, void* stream,
                          const uint16_t* hidden_h, const uint16_t* W_lm,
                          const int32_t* draft_tokens_h,
@@ -157,8 +159,12 @@ typedef enum {
     NJ_OPT_PATH = 1,          /* value: nj_path                                  */
     NJ_OPT_CERTIFY = 2,       /* 1 (default): certified fp64 fallback on; 0 off  */
     NJ_OPT_FORCE_FALLBACK = 3,/* 1: recompute EVERY request in fp64 (tests)      */
-    NJ_OPT_PROFILE = 4        /* 1: bracket the dominant kernel of every nj_verify */
+    NJ_OPT_PROFILE = 4,       /* 1: bracket the dominant kernel of every nj_verify */
                               /*    with CUDA events (see nj_kernel_time)           */
+    NJ_OPT_Q_ZERO_COPY = 5    /* nj_verify_host: 1 (default) read a pinned, mapped */
+                              /*    draft_probs_h in place over the host link (only */
+                              /*    q_i(x_i) and rejected rows are touched); 0 copy */
+                              /*    all G rows to the device first                  */
 } nj_option;
 
 nj_status nj_set_option(nj_ctx* ctx, nj_option opt, int64_t value);

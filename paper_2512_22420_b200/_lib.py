@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libnj.so")
 
 NJ_OK, NJ_EINVAL, NJ_ESHAPE, NJ_ECUDA, NJ_ENCCL, NJ_ENOMEM, NJ_EUNSUPPORTED = range(7)
 NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_TWOPASS, NJ_PATH_STAGED = 0, 1, 2, 3
-NJ_OPT_PATH, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PROFILE = 1, 2, 3, 4
+NJ_OPT_PATH, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PROFILE, NJ_OPT_Q_ZERO_COPY = 1, 2, 3, 4, 5
 NJ_FLAG_FALLBACK, NJ_FLAG_ZERO_MASS, NJ_FLAG_CLAMP = 1, 2, 4
 
 # every symbol include/nj.h declares (checked by tests/test_abi.py)

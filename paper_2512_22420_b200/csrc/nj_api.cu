@@ -145,6 +145,7 @@ struct nj_ctx {
     int32_t *s_resid = nullptr, *s_qrow = nullptr;
     int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
     uint32_t* bar = nullptr;       // count, gen
+    int32_t* fb_done = nullptr;    // k_fb completion counter
     int32_t* scratch_i = nullptr;  // [MB]
     int32_t* s_row = nullptr;      // [MB] staged path: sample row of each request
     // vocab-sharded mode (nj_shard.cuh): rank / ranks, NCCL comm or nj_group member
@@ -161,6 +162,8 @@ struct nj_ctx {
     float *st_q = nullptr, *st_u = nullptr;
     int32_t *st_acc = nullptr, *st_next = nullptr;
     int64_t st_ldq = 0;
+    int q_zero_copy = 1;   // nj_verify_host: read mapped pinned q in place (NJ_OPT_Q_ZERO_COPY)
+    int q_remote = 0;      // the current call's q lives in host memory (no bulk q prefetch)
     // W tensor-map cache
     const void* w_cached = nullptr;
     CUtensorMap tmW128{}, tmW16{};
@@ -340,7 +343,7 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     fp.rows_cap = c->max_tiles * kTileV;
     const size_t ring = (size_t)S * stage2;
     const size_t all_q = align_up((size_t)pl.G * fp.rows_cap * 4, 16);
-    fp.q_prefetch = all_q <= ring ? 1 : 0;
+    fp.q_prefetch = (all_q <= ring && !c->q_remote) ? 1 : 0;
     const int nq = std::min(pl.B, pl.G);
     fp.q_bytes_cap = (int)(fp.q_prefetch ? all_q : align_up((size_t)nq * fp.rows_cap * 4, 16));
     const size_t tailb = 0;
@@ -527,6 +530,7 @@ FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const i
     f.fb_list = c->fb_list();
     f.req_flags = c->req_flags();
     f.fb_logits = c->fb_logits;
+    f.fb_done = c->fb_done;
     f.draft_tokens = tok;
     f.q = q;
     f.ldq = ldq;
@@ -556,10 +560,8 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t st, Args...
 }
 
 nj_status launch_fallback(nj_ctx* c, cudaStream_t st, const FbParams& f, const ReqMeta& m) {
-    NJ_CUDA(c, launch_pdl(k_fb_logits, dim3(c->num_sms * 2), dim3(256), st, f, m));
-    NJ_LAUNCHED(c, "k_fb_logits", st);
-    NJ_CUDA(c, launch_pdl(k_fb_decide, dim3(std::min(c->cfg.max_batch, c->num_sms)), dim3(256), st, f, m));
-    NJ_LAUNCHED(c, "k_fb_decide", st);
+    NJ_CUDA(c, launch_pdl(k_fb, dim3(c->num_sms * 2), dim3(256), st, f, m));
+    NJ_LAUNCHED(c, "k_fb", st);
     return NJ_OK;
 }
 
@@ -920,11 +922,12 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     A(s_qrow, (size_t)MB);
     A(fb_block, (size_t)1 + 2 * MB);
     A(bar, 2);
+    A(fb_done, 1);
     A(scratch_i, (size_t)MB);
     A(s_row, (size_t)MB);
 #undef A
     if (c->ncomm && (s = alloc_shard_ws(c)) != NJ_OK) { nj_destroy(c); return s; }
-    if (cudaMemset(c->bar, 0, 2 * sizeof(uint32_t)) != cudaSuccess ||
+    if (cudaMemset(c->bar, 0, 2 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(c->fb_done, 0, sizeof(int32_t)) != cudaSuccess ||
         cudaMemset(c->fb_block, 0, (1 + 2 * MB) * sizeof(int32_t)) != cudaSuccess) {
         nj_destroy(c);
         return set_err(nullptr, NJ_ECUDA, "cudaMemset failed");
@@ -973,6 +976,7 @@ nj_status nj_set_option(nj_ctx* c, nj_option opt, int64_t v) {
         case NJ_OPT_CERTIFY: c->certify = v != 0; return NJ_OK;
         case NJ_OPT_FORCE_FALLBACK: c->force_fb = v != 0; return NJ_OK;
         case NJ_OPT_PROFILE: c->profile = v != 0; return NJ_OK;
+        case NJ_OPT_Q_ZERO_COPY: c->q_zero_copy = v != 0; return NJ_OK;
     }
     return set_err(c, NJ_EINVAL, "unknown option %d", (int)opt);
 }
@@ -1016,7 +1020,7 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
     if (pl.path == NJ_PATH_FUSED) n = 1;
     else if (pl.path == NJ_PATH_STAGED) n = 4;   // GEMM, accept, mass, locate
     else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) : 0) + 4;   // gather+KA, KB, KC, KD1, KD2
-    if (c->certify) n += 2;
+    if (c->certify) n += 1;   // k_fb
     if (path_out) *path_out = pl.path;
     if (launches_out) *launches_out = n;
     return NJ_OK;
@@ -1206,12 +1210,27 @@ nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, cons
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     NJ_CUDA(c, cudaMemcpyAsync(c->st_hidden, hidden_h, (size_t)pl.N * c->cfg.d * 2, cudaMemcpyHostToDevice, st));
     NJ_CUDA(c, cudaMemcpyAsync(c->st_u, u_h, (size_t)pl.N * 4, cudaMemcpyHostToDevice, st));
+    // The draft rows q are read zero-copy when the host buffer is pinned and
+    // mapped (UVA): the path touches only q_i(x_i) and the sample row of each
+    // rejected request (<= B of the G rows), so copying all G x V floats would
+    // move ~G/R times the bytes the method reads.
+    const float* qd = c->st_q;
+    c->q_remote = 0;
     if (pl.G > 0) {
         NJ_CUDA(c, cudaMemcpyAsync(c->st_tok, tok_h, (size_t)pl.G * 4, cudaMemcpyHostToDevice, st));
-        NJ_CUDA(c, cudaMemcpyAsync(c->st_q, q_h, (size_t)pl.G * ldq * 4, cudaMemcpyHostToDevice, st));
+        cudaPointerAttributes at{};
+        if (c->q_zero_copy && cudaPointerGetAttributes(&at, q_h) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+            at.devicePointer) {
+            qd = static_cast<const float*>(at.devicePointer);
+            c->q_remote = 1;
+        } else {
+            (void)cudaGetLastError();
+            NJ_CUDA(c, cudaMemcpyAsync(c->st_q, q_h, (size_t)pl.G * ldq * 4, cudaMemcpyHostToDevice, st));
+        }
     }
-    s = nj_verify(c, stream, c->st_hidden, W_lm, c->st_tok, c->st_q, ldq, gamma, c->st_u, B, c->st_acc,
+    s = nj_verify(c, stream, c->st_hidden, W_lm, c->st_tok, qd, ldq, gamma, c->st_u, B, c->st_acc,
                   c->st_next, nullptr);
+    c->q_remote = 0;
     if (s != NJ_OK) return s;
     NJ_CUDA(c, cudaMemcpyAsync(acc_h, c->st_acc, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
     NJ_CUDA(c, cudaMemcpyAsync(next_h, c->st_next, (size_t)B * 4, cudaMemcpyDeviceToHost, st));

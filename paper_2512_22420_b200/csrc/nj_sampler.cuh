@@ -471,6 +471,7 @@ struct FbParams {
     const int32_t* fb_list;
     int32_t* req_flags;
     double* fb_logits;     // [N][V_local] (row index = packed row of the request)
+    int32_t* fb_done;      // k_fb completion counter (0 between calls)
     const int32_t* draft_tokens;
     const float* q;
     int64_t ldq;
@@ -495,10 +496,7 @@ __device__ __forceinline__ float bf16f(uint16_t h) { return __uint_as_float(((ui
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-__global__ void __launch_bounds__(256) k_fb_logits(const FbParams p, const ReqMeta m) {
-    pdl_wait();
-    const int nfb = __ldcg(p.fb_count);
-    if (nfb == 0) return;
+__device__ __forceinline__ void fb_logits_body(const FbParams& p, const ReqMeta& m, int nfb) {
     const int lane = (int)lane_id();
     const int gw = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     const int nw = gridDim.x * (blockDim.x / 32);
@@ -523,6 +521,13 @@ __global__ void __launch_bounds__(256) k_fb_logits(const FbParams p, const ReqMe
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_fb_logits(const FbParams p, const ReqMeta m) {
+    pdl_wait();
+    const int nfb = __ldcg(p.fb_count);
+    if (nfb == 0) return;
+    fb_logits_body(p, m, nfb);
 }
 
 template <typename T>
@@ -560,15 +565,13 @@ __device__ double row_lse_d(const LT* row, int V, double* sh) {
 
 // FB-B: block per queued request.  fp64 lse, acceptance, residual / bonus,
 // inverse CDF (block scan, ascending id) -- the plain definition.
-__global__ void __launch_bounds__(256) k_fb_decide(const FbParams p, const ReqMeta m) {
-    pdl_wait();
-    const int nfb = __ldcg(p.fb_count);
+__device__ __forceinline__ void fb_decide_body(const FbParams& p, const ReqMeta& m, int nfb, int k0, int kstep) {
     __shared__ double sh[32];
     __shared__ double lse[32];
     __shared__ int sn, st;
     __shared__ double sbase;
     const int V = p.V_local;
-    for (int k = blockIdx.x; k < nfb; k += gridDim.x) {
+    for (int k = k0; k < nfb; k += kstep) {
         const int b = __ldcg(&p.fb_list[k]);
         int gam, ro;
         const double* L = nullptr;
@@ -675,6 +678,30 @@ __global__ void __launch_bounds__(256) k_fb_decide(const FbParams p, const ReqMe
         }
         __syncthreads();
     }
+}
+
+__global__ void __launch_bounds__(256) k_fb_decide(const FbParams p, const ReqMeta m) {
+    pdl_wait();
+    fb_decide_body(p, m, __ldcg(p.fb_count), blockIdx.x, gridDim.x);
+}
+
+// FB (one launch): fp64 logits of the queued requests by every block, then the
+// last block to finish decides them all.  An empty queue costs one PDL launch
+// whose blocks exit at once (the common case).
+__global__ void __launch_bounds__(256) k_fb(const FbParams p, const ReqMeta m) {
+    pdl_wait();
+    const int nfb = __ldcg(p.fb_count);
+    if (nfb == 0) return;
+    fb_logits_body(p, m, nfb);
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (threadIdx.x == 0) last = atomicAdd(p.fb_done, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    fb_decide_body(p, m, nfb, 0, 1);
+    if (threadIdx.x == 0) *p.fb_done = 0;
 }
 
 }  // namespace nj

@@ -267,3 +267,21 @@ def test_uncertified_decisions_full_size(B, g):
     b = make_batch(B, g, V=QV, d=QD, seed=B * 3 + 1, device=DEV, W=w_full())
     acc, nxt, dd, v = run(b, certify=False)
     check(b, acc, nxt, dd, lnp_tol=2e-5)
+
+
+def test_verify_host_zero_copy_and_copy_paths_agree():
+    """nj_verify_host reads mapped pinned q in place (default) or copies it
+    (NJ_OPT_Q_ZERO_COPY=0); both equal the device-pointer call, on the fused,
+    staged and two-pass paths."""
+    from paper_2512_22420_b200 import NJ_OPT_Q_ZERO_COPY
+    for B, g in [(8, 3), (40, 2), (90, 3)]:
+        b = make_batch(B, g, V=4096, d=128, seed=B, device=DEV)
+        acc, nxt, _, v = run(b)
+        pin = lambda t: t.cpu().pin_memory()
+        hh, th, qh, uh = pin(b.hidden), pin(b.draft_tokens), pin(b.draft_probs), pin(b.uniforms)
+        for zc in (1, 0):
+            v.set_option(NJ_OPT_Q_ZERO_COPY, zc)
+            acc_h = torch.empty(B, dtype=torch.int32).pin_memory()
+            nxt_h = torch.empty(B, dtype=torch.int32).pin_memory()
+            v.verify_host(hh, b.W, th, qh, b.gamma, uh, acc_h, nxt_h)
+            assert (acc_h.numpy() == acc).all() and (nxt_h.numpy() == nxt).all(), (B, g, zc)
