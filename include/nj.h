@@ -150,7 +150,7 @@ typedef enum {
     NJ_PATH_FUSED = 1,   /* one persistent kernel, logits resident in TMEM       */
     NJ_PATH_TWOPASS = 2, /* stats GEMM over drafts, accept, sample-row GEMM,     */
                          /* sampler kernels                                      */
-    NJ_PATH_STAGED = 3   /* N <= 256: ONE GEMM pass over all N rows whose fp32   */
+    NJ_PATH_STAGED = 3   /* N <= 512: ONE GEMM pass over all N rows whose fp32   */
                          /* logits are staged in L2 (evict_last stores), accept, */
                          /* sampler kernels reading the B sample rows            */
 } nj_path;

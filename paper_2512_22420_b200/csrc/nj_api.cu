@@ -63,7 +63,7 @@ bool encode_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t d, int bo
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr int kStagedMaxN = kAccMaxRowG;   // staged path: rows of one GEMM pass (2 token chunks)
+constexpr int kStagedMaxN = kBigMaxRowG;   // staged path: rows of one GEMM pass (<= 2 token chunks of 256)
 
 inline int round16(int x) { return (x + 15) & ~15; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -257,7 +257,13 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
     const bool staged_ok = pl.N <= kStagedMaxN && c->logits_st != nullptr && !c->sharded();
     int path = c->path_opt;
     if (c->sharded() && path == NJ_PATH_AUTO) path = NJ_PATH_TWOPASS;   // the phased sharded driver
-    if (path == NJ_PATH_AUTO) path = fused_ok ? NJ_PATH_FUSED : staged_ok ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
+    // k_gemm_big's cost is ~per (vocab tile, token chunk) item whatever the chunk
+    // width (<= 256): staged (ceil(N/256) chunks in one pass) wins only when it
+    // needs fewer chunks than K-A + K-C (ceil(G/256) + ceil(B/256))
+    const auto nch = [](int r) { return (r + kBigMaxT - 1) / kBigMaxT; };
+    const bool staged_pays = pl.N <= kBigMaxT || nch(pl.N) < nch(pl.G) + nch(pl.B);
+    if (path == NJ_PATH_AUTO)
+        path = fused_ok ? NJ_PATH_FUSED : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
         return set_err(c, NJ_EUNSUPPORTED, "fused path needs N <= %d and TMEM room (N=%d)", kFusedMaxN, pl.N);
     if (path == NJ_PATH_STAGED && !staged_ok)
@@ -435,6 +441,7 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     if (R <= 0) return NJ_OK;
     if (c->gemm_acc) {
         if (rr) return set_err(c, NJ_EUNSUPPORTED, "NJ_GEMM=acc: no round-robin mode");
+        if (in.use_row_g && R > kAccMaxRowG) return set_err(c, NJ_EUNSUPPORTED, "NJ_GEMM=acc: staged rows <= %d", kAccMaxRowG);
         GemmAccParams gp{};
         gp.logits = in.logits; gp.ld_out = in.ld_out; gp.part_m = in.part_m; gp.part_s = in.part_s;
         gp.tok = in.tok; gp.dl = in.dl; gp.w_evict_first = in.w_evict_first; gp.use_row_g = in.use_row_g;
@@ -492,10 +499,10 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     size_t tail = 4 * 4 * kBigNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 4) * 8 + 8;
     int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
-    if (const char* e = getenv("NJ_BIG_S")) S = std::min(S, std::max(2, atoi(e)));
+    if (const char* e = getenv("NJ_BIG_S")) S = (gp.dbg & 4) ? std::min(64, atoi(e)) : std::min(S, std::max(2, atoi(e)));
     if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_big: not enough shared memory (R=%d)", R);
     gp.nstages = S;
-    const size_t smem = (size_t)S * stage + tail;
+    const size_t smem = ((gp.dbg & 4) ? 0 : (size_t)S * stage) + tail + ((gp.dbg & 4) ? (size_t)S * 16 : 0);
     if (CG == 2) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
@@ -1081,7 +1088,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         gp.part_m = c->part_m; gp.part_s = c->part_s;
         gp.tok = draft_tokens; gp.dl = c->dl;
         gp.use_row_g = 1;
-        gp.w_evict_first = 1;
+        gp.w_evict_first = pl.N <= kBigMaxT ? 1 : 0;   // two chunks re-read W tiles from L2
         if (const char* e = getenv("NJ_W_EVICT_FIRST")) gp.w_evict_first = atoi(e);
         for (int b = 0; b < pl.B; ++b)
             for (int r = pl.row_off[b]; r < pl.row_off[b + 1]; ++r)

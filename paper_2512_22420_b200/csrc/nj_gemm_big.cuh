@@ -38,7 +38,7 @@ constexpr int kBigEpiWarps = 16;
 constexpr int kBigThreads = (2 + kBigEpiWarps) * 32;   // warp 0 TMA, warp 1 MMA/TMEM, 2..17 epilogue
 constexpr int kBigMaxT = 256;                          // token chunk (MMA N) upper bound
 constexpr int kBigNC = 64;                             // columns per epilogue warp
-constexpr int kBigMaxRowG = 256;                       // staged path: rows mapped to draft indices
+constexpr int kBigMaxRowG = 512;                       // staged path: rows mapped to draft indices
 
 struct GemmBigParams {
     int32_t R, nchunks, chunk;           // rows, chunks, rows per chunk (multiple of 16, <= 256)
@@ -120,7 +120,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.nstages, GK = p.gk;
     const int bBytes = (p.chunk / CG) * 128;                          // this CTA's H box per k-block
-    const size_t stageBytes = (size_t)GK * (kTileBytesA + bBytes);
+    const size_t stageBytes = (p.dbg & 4) ? 0 : (size_t)GK * (kTileBytesA + bBytes);   // probe: no ring memory
     uint8_t* ring = smem;                                             // S x GK x (A 16 KB | B bBytes)
     float2* scratch = reinterpret_cast<float2*>(ring + (size_t)S * stageBytes);   // [4 e][4 q][64]
     float2* state = scratch + 4 * 4 * kBigNC;                                       // [R] (STATS)

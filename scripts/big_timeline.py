@@ -8,8 +8,9 @@ from synth.inputs import make_batch, make_weight
 lib = load(); lib.nj_debug_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
 dev = torch.device("cuda:0"); V, d = 152064, 3584
 W = make_weight(V, d, 0, dev)
-for B, g, extra in [(64, 3, {}), (64, 3, {"NJ_BIG_DBG": "15"}), (64, 3, {"NJ_BIG_DBG": "7"})]:
-    for k in ("NJ_BIG_DBG",):
+VARS = [(64, 3, {"NJ_BIG_DBG": "15", "NJ_BIG_S": str(S)}) for S in (2, 4, 8, 16, 32)] + [(64, 3, {"NJ_BIG_DBG": "15", "NJ_BIG_S": "16", "NJ_KS": "56"})]
+for B, g, extra in VARS:
+    for k in ("NJ_BIG_DBG", "NJ_BIG_S", "NJ_KS"):
         os.environ.pop(k, None)
     os.environ.update(extra)
     b = make_batch(B, g, V=V, d=d, seed=0, device=dev, W=W)
@@ -29,6 +30,5 @@ for B, g, extra in [(64, 3, {}), (64, 3, {"NJ_BIG_DBG": "15"}), (64, 3, {"NJ_BIG
     print("  mma stage interval ns:      median %.0f p90 %.0f max %.0f" % (np.median(dM), np.percentile(dM, 90), dM.max()))
     print("  epilogue group interval ns: median %.0f p90 %.0f max %.0f" % (np.median(dE), np.percentile(dE, 90), dE.max()))
     print("  mma start - producer start (same stage) ns: median %.0f" % np.median(M[:min(n, nm)] - P[:min(n, nm)]))
-    print("  first 70 mma intervals:", dM[:70].tolist())
-    print("  first 20 epi intervals:", dE[:20].tolist())
+    print("  first 30 mma intervals:", dM[:30].tolist())
     del v

@@ -187,16 +187,26 @@ def test_twopass_c3_large_batch_sampled():
 
 
 def test_twopass_above_staged_limit():
-    """N > 256 (AUTO picks two-pass): B=80, gamma=3 -> N=320, 3 token chunks."""
-    b = make_batch(80, 3, V=QV, d=QD, seed=31, device=DEV, W=w_full())
+    """N > 512 (AUTO picks two-pass): B=140, gamma=3 -> N=560, K-A over 420 rows in 2 chunks."""
+    b = make_batch(140, 3, V=QV, d=QD, seed=31, device=DEV, W=w_full())
     acc, nxt, dd, v = run(b)
     assert v.plan(b.gamma)[0] == NJ_PATH_TWOPASS
     check(b, acc, nxt, dd)
 
 
-# ----------------------------------------------------------------- staged path (48 < N <= 256)
+def test_staged_two_chunks_full_size():
+    """256 < N <= 512 with G > 256 (AUTO picks staged: one GEMM pass with two token
+    chunks instead of three chunk passes for K-A + K-C): B=100, gamma=3 -> N=400."""
+    b = make_batch(100, 3, V=QV, d=QD, seed=32, device=DEV, W=w_full())
+    acc, nxt, dd, v = run(b)
+    assert v.plan(b.gamma)[0] == NJ_PATH_STAGED
+    check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
+
+
+# ----------------------------------------------------------------- staged path (48 < N <= 512)
 @pytest.mark.parametrize("B,g,V,d", [(1, 3, 32, 16), (20, "mixed:5", 8192, 512), (40, "mixed:5", 8192, 512),
-                                     (64, 3, 1000, 64), (9, 5, 777, 40), (60, 0, 4096, 128)])
+                                     (64, 3, 1000, 64), (9, 5, 777, 40), (60, 0, 4096, 128),
+                                     (100, "mixed:5", 4096, 256)])
 def test_staged_small(B, g, V, d):
     for seed in range(2):
         b = make_batch(B, g, V=V, d=d, seed=seed + 3, device=DEV, q_vocab=max(1, V - 5))
@@ -208,8 +218,8 @@ def test_staged_small(B, g, V, d):
 def test_staged_full_size(B, g):
     """C3 points in the memory-bound band at the Qwen shape, every request vs the oracle."""
     b = make_batch(B, g, V=QV, d=QD, seed=B + 17, device=DEV, W=w_full())
-    if b.N > 256:
-        pytest.skip("staged path is N <= 256")
+    if b.N > 512:
+        pytest.skip("staged path is N <= 512")
     acc, nxt, dd, v = run(b)
     assert v.plan(b.gamma)[0] == (NJ_PATH_FUSED if b.N <= 48 else NJ_PATH_STAGED)
     check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
