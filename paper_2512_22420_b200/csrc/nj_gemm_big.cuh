@@ -267,17 +267,21 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 uint32_t dt = 0;
                 for (int kg = 0; kg < ngk; ++kg) {
                     const int ng = min(GK, p.num_kb - kg * GK);
+                    const bool tsm = p.ts && cta == 0 && mst < 1300;
+                    if (tsm) p.ts[4096 + 3 * mst] = globaltimer();
                     if (p.spin) mbar_wait_spin(&full[s], ph);
                     else mbar_wait(&full[s], ph);
-                    if (p.ts && cta == 0 && mst < 4096) p.ts[4096 + mst] = globaltimer();
-                    ++mst;
+                    if (tsm) p.ts[4096 + 3 * mst + 1] = globaltimer();
                     tc_fence_after();
                     uint8_t* st = ring + (size_t)s * stageBytes;
                     for (int g = 0; g < ng; ++g) {
                         if (kin == 0) {
                             const int buf = ngrp & 1;
+                            const bool tsa = p.ts && cta == 0 && ngrp < 2000;
+                            if (tsa) p.ts[12288 + 2 * ngrp] = globaltimer();
                             if (p.spin) mbar_wait_spin(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
                             else mbar_wait(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
+                            if (tsa) p.ts[12288 + 2 * ngrp + 1] = globaltimer();
                             tc_fence_after();
                             dt = tbase + (uint32_t)(buf * kBigMaxT);
                         }
@@ -302,6 +306,8 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                     if (p.dbg & 16) mbar_arrive(&empty[s]);   // probe (CG = 1, no MMAs): plain arrive
                     else if (CG == 2) mma_commit_mc2(&empty[s], 3);
                     else mma_commit(&empty[s]);
+                    if (tsm) p.ts[4096 + 3 * mst + 2] = globaltimer();
+                    ++mst;
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
@@ -330,6 +336,8 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
             for (int j = 0; j < kBigNC; ++j) acc[j] = 0.f;
             for (int g = 0; g < ngroups; ++g, ++ngrp) {
                 const int buf = ngrp & 1;
+                const bool tse = p.ts && cta == 0 && warp == 2 && lane == 0 && ngrp < 2048;
+                if (tse) p.ts[8192 + 2 * ngrp] = globaltimer();
                 if (p.sleep_ns > 0) mbar_wait_sleep(&afull[buf], (ngrp >> 1) & 1, (uint32_t)p.sleep_ns);
                 else if (p.spin & 2) mbar_wait_spin(&afull[buf], (ngrp >> 1) & 1);
                 else mbar_wait(&afull[buf], (ngrp >> 1) & 1);
@@ -357,7 +365,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (p.ts && cta == 0 && warp == 2 && lane == 0 && ngrp < 4096) p.ts[8192 + ngrp] = globaltimer();
+                if (tse) p.ts[8192 + 2 * ngrp + 1] = globaltimer();
                 if (lane == 0) {
                     if (CG == 2) mbar_arrive_cluster(aempty_cl[buf]);
                     else mbar_arrive(&aempty[buf]);
