@@ -206,6 +206,13 @@ nj_status nj_lmhead_logits_ks(nj_ctx* ctx, void* stream,
 nj_status nj_stream_test(nj_ctx* ctx, void* stream, const uint16_t* W, int32_t mode, int32_t group,
                          int32_t nstages, const uint16_t* H, int32_t hrows);
 
+/* tcgen05.mma issue microbenchmark (test-only): one CTA per SM,
+ * one thread issues `iters` groups of 4 MMAs (M = 128, N = n in 16..256, K =
+ * 16) from resident smem operands; mode 0: commit+wait at the end, 1: after
+ * every group, 2: commit every group without waiting.  cycles_out: device
+ * int64 [num_SMs], cycles per group per SM. */
+nj_status nj_mma_probe(nj_ctx* ctx, void* stream, int32_t n, int32_t iters, int32_t mode, int64_t* cycles_out);
+
 /* Sampler stage (BJ step 3, residual / bonus draw) on given fp32 logits:
  *   logits   [B, ld_l] fp32 device, one row per request over the full vocab V
  *   residual [B] int32 device: 1 -> w = max(0, p − q_row), 0 -> w = p

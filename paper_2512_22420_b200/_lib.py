@@ -32,7 +32,7 @@ EXPORTS = [
     "nj_observe", "nj_exploitation_score", "nj_prefill_cost_ms", "nj_bandit_state", "nj_bandit_arm",
     "nj_bandit_last_gamma", "nj_bandit_snapshot_json",
     "nj_shard_range", "nj_nccl_get_unique_id", "nj_nccl_comm_init", "nj_nccl_comm_destroy", "nj_group_create",
-    "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify",
+    "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify", "nj_mma_probe",
 ]
 NJ_NCCL_ID_BYTES = 128
 
@@ -99,6 +99,7 @@ def load():
         "nj_group_member": ([P, I32], P),
         "nj_group_last_error": ([P], ctypes.c_char_p),
         "nj_group_verify": ([P, P, P, P, P, P, I64, P, P, I32, P, P, P], I32),
+        "nj_mma_probe": ([P, P, I32, I32, I32, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

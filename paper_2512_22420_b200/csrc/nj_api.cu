@@ -24,6 +24,7 @@
 #include "nj_probe_ks.cuh"
 #include "nj_stream_test.cuh"
 #include "nj_shard.cuh"
+#include "nj_mma_probe.cuh"
 
 #include <dlfcn.h>
 
@@ -1497,6 +1498,17 @@ const char* nj_group_last_error(const nj_group* g) {
     for (nj_ctx* c : g->mem)
         if (!c->err.empty()) return c->err.c_str();
     return "";
+}
+
+
+nj_status nj_mma_probe(nj_ctx* c, void* stream, int32_t n, int32_t iters, int32_t mode, int64_t* cycles_out) {
+    if (!c || !cycles_out || n < 16 || n > 256 || n % 16 || iters < 1) return NJ_EINVAL;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t smem = kTileBytesA + 256 * 128 + 64;
+    NJ_CUDA(c, cudaFuncSetAttribute(k_mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_mma_probe<<<c->num_sms, 128, smem, st>>>(n, iters, mode, reinterpret_cast<long long*>(cycles_out));
+    NJ_LAUNCHED(c, "k_mma_probe", st);
+    return NJ_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,57 @@
+// nj_mma_probe.cuh — test-only microbenchmark of the single-thread tcgen05.mma
+// issue loop (DESIGN.md §5 "what bounds k_gemm_big"): one CTA per SM, the
+// operand tiles stay resident in shared memory (no TMA), one thread issues
+// `iters` groups of 4 MMAs (M = 128, N = n, K = 16 each; one 64-deep
+// k-block) into one TMEM accumulator, optionally committing to an mbarrier
+// after every group and waiting for it (`mode` 1), committing without waiting
+// (2, as the ring does), or only at the end (0).
+// Reports clock64 cycles per group in out[blockIdx.x].
+#pragma once
+#include "nj_gemm.cuh"
+
+namespace nj {
+
+__global__ void __launch_bounds__(128, 1) k_mma_probe(int n, int iters, int mode, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sA = smem;                       // 16 KB: 128 x 64 bf16 (contents irrelevant)
+    uint8_t* sB = smem + kTileBytesA;         // n x 128 B
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 256 * 128);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    for (int i = threadIdx.x; i < (kTileBytesA + 256 * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    if (threadIdx.x == 0) { mbar_init(bar, 1); fence_barrier_init(); }
+    if (warp_id() == 0) tmem_alloc(slot, 256);
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = *slot;
+    if (threadIdx.x == 32) {
+        const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)n);
+        const uint64_t ad = sdesc_sw128(sA), bd = sdesc_sw128(sB);
+        uint32_t ph = 0;
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_bf16(tbase, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+            if (mode == 1) {
+                mma_commit(bar);
+                mbar_wait(bar, ph);
+                ph ^= 1;
+            } else if (mode == 2) {
+                mma_commit(bar);   // like the ring's per-stage commit, not waited for
+            }
+        }
+        if (mode != 2) {
+            mma_commit(bar);
+            mbar_wait(bar, ph);
+        } else {
+            tc_fence_before();   // (mode 2: the barrier phase count is not tracked)
+        }
+        out[blockIdx.x] = (clock64() - t0) / iters;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp_id() == 0) tmem_dealloc(tbase, 256);
+}
+
+}  // namespace nj
