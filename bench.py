@@ -244,6 +244,44 @@ def bench_nj(args, ws, rank, local):
     ms = e0.elapsed_time(e1)
     kms, kn = v.kernel_time(reset=True)
     v.set_option(NJ_OPT_PROFILE, 0)
+    ms_eager = ms
+    graph_ok = False
+    if not args.no_graph:
+        # the same steps replayed from CUDA graphs (one per rotating batch; nj_verify does
+        # no host synchronisation, so a call is capturable): no per-launch host overhead
+        try:
+            graphs = []
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                for j in range(nb):
+                    step(j)          # warm the capture stream
+                cap.synchronize()
+                for j in range(nb):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=cap):
+                        step(j)
+                    graphs.append(g)
+            stream.wait_stream(cap)
+            for i in range(args.warmup):
+                graphs[i % nb].replay()
+            torch.cuda.synchronize()
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clk:
+                g0.record(stream)
+                for i in range(args.steps):
+                    graphs[i % nb].replay()
+                g1.record(stream)
+                torch.cuda.synchronize()
+            if ws > 1:
+                dist.barrier()
+            ms = g0.elapsed_time(g1)
+            graph_ok = True
+        except Exception as e:   # graph capture unavailable: keep the eager timing
+            print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
     # accepted tokens in the timed steps (outputs of the last nb steps are representative: same batches)
     acc_tok, rejected = 0, 0
     per_batch = []
@@ -340,7 +378,9 @@ def bench_nj(args, ws, rank, local):
                        "d": D_Q, "V": V_Q, "global_batch": B * ws,
                        "path": PATH_NAMES[p_used],
                        "parallelism": f"request-sharded x{ws} (no data-path collective)",
-                       "l2": "inputs larger than L2: W_lm (1.09 GB) streamed from HBM every step"},
+                       "l2": "inputs larger than L2: W_lm (1.09 GB) streamed from HBM every step",
+                       "launch": "CUDA graph replay per step" if graph_ok else "eager launches",
+                       "ms_per_step_eager": ms_eager / args.steps},
             "accepted_tokens_per_s": acc_tok * ws / (t_max / 1e3),
             "realised_beta_tokens_per_request": acc_tok / (args.steps * B),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
@@ -598,6 +638,7 @@ def main():
     ap.add_argument("--path", default=None, choices=[None] + PATH_NAMES)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager nj_verify launches only")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--sweep", action="store_true", help="C3 grid: one JSON line per (B, gamma) point")
     ap.add_argument("--sweep-B", default="1,2,4,8,16,32,48,64,96,128,192,256")
