@@ -481,6 +481,11 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     gp.gk = (gp.nchunks == 1 && gp.chunk <= 128) ? 2 : 1;
     if (const char* e = getenv("NJ_BIG_GK")) gp.gk = std::max(1, atoi(e));
     gp.ks = std::max(gp.gk, (c->gemm_ks + gp.gk - 1) / gp.gk * gp.gk);
+    // as many accumulator buffers as TMEM holds: small chunks let the MMAs run
+    // further ahead of the epilogue's per-item output
+    gp.bstride = std::max(32, (gp.chunk + 31) & ~31);
+    gp.nbuf = std::max(2, std::min(kBigMaxBuf, 512 / gp.bstride));
+    if (const char* e = getenv("NJ_BIG_NBUF")) gp.nbuf = std::max(2, std::min(gp.nbuf, atoi(e)));
     gp.pf = c->gemm_pf;
     gp.dbg = 0;
     if (const char* e = getenv("NJ_BIG_DBG")) gp.dbg = atoi(e);
@@ -498,7 +503,7 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
         return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
     const size_t stage = (size_t)gp.gk * (kTileBytesA + (size_t)(gp.chunk / CG) * 128);
     size_t tail = 4 * 4 * kBigNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
-    tail = align_up(tail, 8) + (2 * 8 + 4) * 8 + 8;
+    tail = align_up(tail, 8) + (2 * 8 + 2 * kBigMaxBuf) * 8 + 8;
     int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
     if (const char* e = getenv("NJ_BIG_S")) S = (gp.dbg & 4) ? std::min(64, atoi(e)) : std::min(S, std::max(2, atoi(e)));
     if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_big: not enough shared memory (R=%d)", R);

@@ -38,13 +38,15 @@ constexpr int kBigEpiWarps = 16;
 constexpr int kBigThreads = (2 + kBigEpiWarps) * 32;   // warp 0 TMA, warp 1 MMA/TMEM, 2..17 epilogue
 constexpr int kBigMaxT = 256;                          // token chunk (MMA N) upper bound
 constexpr int kBigNC = 64;                             // columns per epilogue warp
-constexpr int kBigMaxRowG = 512;                       // staged path: rows mapped to draft indices
+constexpr int kBigMaxRowG = 512;
+constexpr int kBigMaxBuf = 8;                          // accumulator buffers (512 TMEM columns / chunk)                       // staged path: rows mapped to draft indices
 
 struct GemmBigParams {
     int32_t R, nchunks, chunk;           // rows, chunks, rows per chunk (multiple of 16, <= 256)
     int32_t V_local, U, num_kb, nstages, v_begin;
     int32_t gk;                          // k-blocks per TMA ring stage (1, 2 or 4)
     int32_t ks;                          // k-blocks per accumulator restart (multiple of gk)
+    int32_t nbuf, bstride;               // accumulator buffers (2..8) and their TMEM column stride
     int32_t rr;                          // 1: round-robin (tile, chunk) items over global 128-row tiles
     int32_t ntiles_g;                    // global 128-row tiles (rr mode)
     float* logits;                       // WRITE: [R][ld_out] fp32
@@ -129,9 +131,10 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         (reinterpret_cast<uintptr_t>(stok + (CAPTURE ? p.R : 0)) + 7) & ~uintptr_t(7));
     uint64_t* full = bars;
     uint64_t* empty = bars + S;
-    uint64_t* afull = bars + 2 * S;    // [2] accumulator buffers
-    uint64_t* aempty = afull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+    uint64_t* afull = bars + 2 * S;    // [kBigMaxBuf] accumulator buffers
+    uint64_t* aempty = afull + kBigMaxBuf;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kBigMaxBuf);
+    const int NBUF = p.nbuf;            // accumulator buffers of p.bstride TMEM columns
 
     const int warp = (int)warp_id(), lane = (int)lane_id();
     const int grid = gridDim.x, cta = blockIdx.x;
@@ -157,7 +160,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         tma_prefetch_desc(&tmW16);
         tma_prefetch_desc(&tmH);
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int g = 0; g < 2; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kBigEpiWarps * CG); }
+        for (int g = 0; g < NBUF; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kBigEpiWarps * CG); }
         fence_barrier_init();
         fence_proxy_async();
     }
@@ -256,7 +259,9 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
             // ------------------------------------------------ MMA issuer (leader CTA)
             int s = 0;
             uint32_t ph = 0;
-            int ngrp = 0;   // accumulator groups issued (buffer ngrp & 1, phase (ngrp >> 1) & 1)
+            int ngrp = 0;   // accumulator groups issued
+            int abuf = 0;   // accumulator buffer of the current group and its phase
+            uint32_t aph = 0;
             int mst = 0;
             int row0, trows, row0L, trowsL, trowsP, c;
             for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
@@ -276,14 +281,13 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                     uint8_t* st = ring + (size_t)s * stageBytes;
                     for (int g = 0; g < ng; ++g) {
                         if (kin == 0) {
-                            const int buf = ngrp & 1;
                             const bool tsa = p.ts && cta == 0 && ngrp < 2000;
                             if (tsa) p.ts[12288 + 2 * ngrp] = globaltimer();
-                            if (p.spin) mbar_wait_spin(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
-                            else mbar_wait(&aempty[buf], ((ngrp >> 1) & 1) ^ 1);
+                            if (p.spin) mbar_wait_spin(&aempty[abuf], aph ^ 1);
+                            else mbar_wait(&aempty[abuf], aph ^ 1);
                             if (tsa) p.ts[12288 + 2 * ngrp + 1] = globaltimer();
                             tc_fence_after();
-                            dt = tbase + (uint32_t)(buf * kBigMaxT);
+                            dt = tbase + (uint32_t)(abuf * p.bstride);
                         }
                         const uint64_t ad = sdesc_sw128(st + (size_t)g * kTileBytesA);
                         const uint64_t bd = sdesc_sw128(st + (size_t)GK * kTileBytesA + (size_t)g * bBytes);
@@ -296,10 +300,11 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                         }
                         const int kb = kg * GK + g;
                         if (++kin == p.ks || kb == p.num_kb - 1) {
-                            if (p.dbg & 16) mbar_arrive(&afull[ngrp & 1]);
-                            else if (CG == 2) mma_commit_mc2(&afull[ngrp & 1], 3);
-                            else mma_commit(&afull[ngrp & 1]);
+                            if (p.dbg & 16) mbar_arrive(&afull[abuf]);
+                            else if (CG == 2) mma_commit_mc2(&afull[abuf], 3);
+                            else mma_commit(&afull[abuf]);
                             ++ngrp;
+                            if (++abuf == NBUF) { abuf = 0; aph ^= 1; }
                             kin = 0;
                         }
                     }
@@ -323,9 +328,11 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         const int vr = q * 32 + lane;
         const uint64_t pol_keep = policy_evict_last();   // staged logits stay in L2 for the sampler
         const int ngroups = (p.num_kb + p.ks - 1) / p.ks;
-        uint32_t aempty_cl[2] = {0u, 0u};
-        if (CG == 2) { aempty_cl[0] = mapa_shared(&aempty[0], 0); aempty_cl[1] = mapa_shared(&aempty[1], 0); }
-        int ngrp = 0;
+        uint32_t aempty_cl[kBigMaxBuf];
+        if (CG == 2)
+            for (int g = 0; g < NBUF; ++g) aempty_cl[g] = mapa_shared(&aempty[g], 0);
+        int ngrp = 0, ebuf = 0;
+        uint32_t eph = 0;
         int row0, trows, row0L, trowsL, trowsP, c;
         for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
             const int c0 = c * p.chunk;
@@ -335,14 +342,15 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
 #pragma unroll
             for (int j = 0; j < kBigNC; ++j) acc[j] = 0.f;
             for (int g = 0; g < ngroups; ++g, ++ngrp) {
-                const int buf = ngrp & 1;
+                const int buf = ebuf;
                 const bool tse = p.ts && cta == 0 && warp == 2 && lane == 0 && ngrp < 2048;
                 if (tse) p.ts[8192 + 2 * ngrp] = globaltimer();
-                if (p.sleep_ns > 0) mbar_wait_sleep(&afull[buf], (ngrp >> 1) & 1, (uint32_t)p.sleep_ns);
-                else if (p.spin & 2) mbar_wait_spin(&afull[buf], (ngrp >> 1) & 1);
-                else mbar_wait(&afull[buf], (ngrp >> 1) & 1);
+                if (p.sleep_ns > 0) mbar_wait_sleep(&afull[buf], eph, (uint32_t)p.sleep_ns);
+                else if (p.spin & 2) mbar_wait_spin(&afull[buf], eph);
+                else mbar_wait(&afull[buf], eph);
+                if (++ebuf == NBUF) { ebuf = 0; eph ^= 1; }
                 tc_fence_after();
-                const uint32_t ta = lane_base + (uint32_t)(buf * kBigMaxT);
+                const uint32_t ta = lane_base + (uint32_t)(buf * p.bstride);
                 if (p.dbg & 2) {
                 } else if (myc > 32) {
                     float v[32];
