@@ -295,3 +295,22 @@ def test_verify_host_zero_copy_and_copy_paths_agree():
             nxt_h = torch.empty(B, dtype=torch.int32).pin_memory()
             v.verify_host(hh, b.W, th, qh, b.gamma, uh, acc_h, nxt_h)
             assert (acc_h.numpy() == acc).all() and (nxt_h.numpy() == nxt).all(), (B, g, zc)
+
+
+@pytest.mark.parametrize("B,g,V,d", [(1024, 5, 4096, 256), (1024, "mixed:15", 2048, 64), (300, 15, 1024, 64)])
+def test_maximum_sizes(B, g, V, d):
+    """max_batch = 1024 (kMaxB), gamma up to 15: K-A spans several launches
+    (G > 1536 rows) that share one partial layout."""
+    b = make_batch(B, g, V=V, d=d, seed=B % 97, device=DEV)
+    acc, nxt, dd, v = run(b, gamma_max=15)
+    check(b, acc, nxt, dd)
+
+
+def test_degenerate_inputs():
+    """B = 1 with gamma = 0 at V = 1 (the only token), d = 8 (one 16-byte row)."""
+    b = make_batch(1, 0, V=1, d=8, seed=0, device=DEV)
+    acc, nxt, dd, v = run(b, gamma_max=1)
+    assert acc[0] == 0 and nxt[0] == 0
+    b = make_batch(3, 2, V=16, d=8, seed=1, device=DEV)
+    acc, nxt, dd, v = run(b)
+    check(b, acc, nxt, dd)

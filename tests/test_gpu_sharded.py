@@ -121,3 +121,10 @@ def test_nccl_single_rank():
         v.close()
     finally:
         comm.close()
+
+
+def test_group_large_batch_multi_launch():
+    """G = 2000 draft rows: the sharded K-A spans two launches on every shard."""
+    b = make_batch(400, 5, V=2048, d=64, seed=77, device=DEV)
+    acc, nxt, dd = run_group(b, 4)
+    check(b, acc, nxt, dd)
