@@ -139,6 +139,7 @@ struct nj_ctx {
     std::vector<void*> allocs;
     float *part_m = nullptr, *part_s = nullptr, *part2_m = nullptr, *part2_s = nullptr;
     double* dl = nullptr;
+    double* row_lse = nullptr;   // [max(Nmax, Gmax)] k_lse_rows output
     double *wpart = nullptr, *s_lse = nullptr, *cmass = nullptr, *fb_logits = nullptr, *lse_tmp = nullptr;
     uint16_t *hd = nullptr, *hs = nullptr;
     float* logits_s = nullptr;
@@ -318,8 +319,11 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     fp.kpd = 1;
     fp.sacc = 1;
     if (spare >= 2 * NPAD) {
-        fp.ngroups = 2;
-        fp.nbuf = 2;
+        // as many one-partial groups as the spare TMEM holds: the MMAs run that
+        // many stages ahead of the epilogue's per-tile work
+        fp.ngroups = std::max(2, std::min(8, spare / NPAD));
+        if (const char* e = getenv("NJ_FGROUPS")) fp.ngroups = std::max(2, std::min(fp.ngroups, atoi(e)));
+        fp.nbuf = fp.ngroups;
     } else {
         fp.ngroups = 0;
         fp.nbuf = std::max(1, std::min(8, spare / NPAD));
@@ -329,6 +333,7 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     if (const char* e = getenv("NJ_SACC")) fp.sacc = atoi(e);
     if (!fp.sacc && fp.ngroups > 0) {   // one partial per k-block: GK partial slots per group
         GK = std::max(1, std::min(4, spare / (2 * NPAD)));
+        fp.ngroups = 2;
         fp.nbuf = 2 * GK;
     }
     if (const char* e = getenv("NJ_KGROUP")) GK = std::max(1, atoi(e));
@@ -922,6 +927,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     A(part2_m, (size_t)MB * gp_);
     A(part2_s, (size_t)MB * gp_);
     A(dl, (size_t)c->Gmax);
+    A(row_lse, (size_t)std::max(c->Nmax, c->Gmax));
     A(wpart, (size_t)MB * g);
     A(s_lse, (size_t)MB);
     A(lse_tmp, (size_t)MB);
@@ -1031,8 +1037,8 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
         return NJ_OK;
     }
     if (pl.path == NJ_PATH_FUSED) n = 1;
-    else if (pl.path == NJ_PATH_STAGED) n = 4;   // GEMM, accept, mass, locate
-    else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) : 0) + 4;   // gather+KA, KB, KC, KD1, KD2
+    else if (pl.path == NJ_PATH_STAGED) n = 5;   // GEMM, row lse, accept, mass, locate
+    else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 4;   // gather+KA, row lse, KB, KC, KD1, KD2
     if (c->certify) n += 1;   // k_fb
     if (path_out) *path_out = pl.path;
     if (launches_out) *launches_out = n;
@@ -1113,6 +1119,9 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
         ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc;
         ap.staged = 1; ap.s_row = c->s_row;
+        k_lse_rows<<<(pl.N + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.N, c->row_lse);
+        NJ_LAUNCHED(c, "k_lse_rows", st);
+        ap.pre_lse = c->row_lse;
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
         NJ_LAUNCHED(c, "k_accept", st);
         MassParams mp{};
@@ -1164,6 +1173,11 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         ap.fb_count = c->fb_count(); ap.fb_list = c->fb_list(); ap.req_flags = c->req_flags();
         ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
         ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc;
+        if (pl.G > 0) {
+            k_lse_rows<<<(pl.G + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.G, c->row_lse);
+            NJ_LAUNCHED(c, "k_lse_rows", st);
+            ap.pre_lse = c->row_lse;
+        }
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
         NJ_LAUNCHED(c, "k_accept", st);
         // K-C: sample-row GEMM -> fp32 logits [B, V_local] + stats (bonus-row lse)

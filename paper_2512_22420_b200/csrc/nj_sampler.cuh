@@ -111,7 +111,14 @@ struct AcceptParams {
     // vocab-sharded mode (nj_shard.cuh): merged X1 entries [nranks][xld][2]
     const double* xr1;
     int32_t nranks, xld;
+    // lse of every partial row, precomputed by k_lse_rows (NULL: merge here)
+    const double* pre_lse;
 };
+
+// lse of partial rows [0, n) from the per-CTA partials, one warp per row (all
+// rows in parallel; k_accept then only reads them)
+__global__ void k_lse_rows(const float* __restrict__ pm, const float* __restrict__ ps, int pld, int grid, int n,
+                           double* __restrict__ out);
 
 __device__ __forceinline__ double xmerge_lse(const double* xr, int nranks, int ld, int g, double& dl);
 
@@ -128,7 +135,11 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
         const int g = g0 + i;
         double lse, dlv;
         if (p.xr1) lse = xmerge_lse(p.xr1, p.nranks, p.xld, g, dlv);
-        else { lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid); dlv = __ldcg(&p.dl[g]); }
+        else {
+            const int pr = p.staged ? ro + i : g;
+            lse = p.pre_lse ? __ldcg(&p.pre_lse[pr]) : warp_lse(p.part_m, p.part_s, p.pld, pr, p.grid);
+            dlv = __ldcg(&p.dl[g]);
+        }
         const double pd = exp(dlv - lse);
         const double qx = (double)p.q[(int64_t)g * p.ldq + p.draft_tokens[g]];
         const double uq = (double)p.u[ro + i] * qx;
@@ -144,14 +155,19 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
         const int g = g0 + i;
         double lse, dlv;
         if (p.xr1) lse = xmerge_lse(p.xr1, p.nranks, p.xld, g, dlv);
-        else { lse = warp_lse(p.part_m, p.part_s, p.pld, p.staged ? ro + i : g, p.grid); dlv = __ldcg(&p.dl[g]); }
+        else {
+            const int pr = p.staged ? ro + i : g;
+            lse = p.pre_lse ? __ldcg(&p.pre_lse[pr]) : warp_lse(p.part_m, p.part_s, p.pld, pr, p.grid);
+            dlv = __ldcg(&p.dl[g]);
+        }
         if (lane == 0) {
             if (p.dbg_lse) p.dbg_lse[ro + i] = (float)lse;
             p.dbg_pdraft[g] = (float)exp(dlv - lse);
         }
     }
     if (p.staged) {
-        if (n == gam) lse_n = warp_lse(p.part_m, p.part_s, p.pld, ro + gam, p.grid);   // bonus row
+        if (n == gam)   // bonus row
+            lse_n = p.pre_lse ? __ldcg(&p.pre_lse[ro + gam]) : warp_lse(p.part_m, p.part_s, p.pld, ro + gam, p.grid);
     } else {
         copy_row(p.hs + (int64_t)b * p.d, p.hidden + (int64_t)(ro + n) * p.d, p.d, lane, 32);
     }
@@ -163,6 +179,14 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
         p.s_lse[b] = lse_n;
         if (p.certify && (flag || p.force_fallback)) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
     }
+}
+
+__global__ void k_lse_rows(const float* __restrict__ pm, const float* __restrict__ ps, int pld, int grid, int n,
+                           double* __restrict__ out) {
+    const int r = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
+    if (r >= n) return;
+    const double l = warp_lse(pm, ps, pld, r, grid);
+    if (lane_id() == 0) out[r] = l;
 }
 
 // lse of each request's logits row [B, ld] (stage-isolated sampler), fp64 merge
@@ -276,22 +300,48 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p) {
     const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
     const float* lrow = logits_row(p, b);
     __shared__ float wt[kSubTiles][8];
+    // all 16 (or 32) loads of the chunk issued before any use, then the same
+    // weight expression as chunk_weight (k_locate recomputes it bit-identically)
     float w[kSubTiles];
+    const int x0 = c * kChunk + (int)threadIdx.x;
 #pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, lrow, c, s, lsef, resid, qrow);
+    for (int s = 0; s < kSubTiles; ++s) {
+        const int x = x0 + s * kSampThreads;
+        w[s] = x < p.V_local ? __ldcg(&lrow[x]) : -INFINITY;
+    }
+    if (resid) {
+        float qv[kSubTiles];
+#pragma unroll
+        for (int s = 0; s < kSubTiles; ++s) {
+            const int x = x0 + s * kSampThreads;
+            qv[s] = x < p.V_local ? __ldg(&qrow[x]) : 0.f;
+        }
+#pragma unroll
+        for (int s = 0; s < kSubTiles; ++s) w[s] = fmaxf(__expf(w[s] - lsef) - qv[s], 0.f);
+    } else {
+#pragma unroll
+        for (int s = 0; s < kSubTiles; ++s) w[s] = __expf(w[s] - lsef);
+    }
 #pragma unroll
     for (int s = 0; s < kSubTiles; ++s) {
         float inc;
         subtile_scan(w[s], inc, wt[s]);
     }
     __syncthreads();
+    // sub-tile totals in parallel (same left-to-right fp64 order as k_locate),
+    // then the chunk total over the 16 sub-tiles
+    __shared__ double sst[kSubTiles];
+    if (threadIdx.x < kSubTiles) {
+        double st = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
+        sst[threadIdx.x] = st;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
         double acc = 0.0;
-        for (int s = 0; s < kSubTiles; ++s) {
-            double st = 0.0;
-            for (int k = 0; k < 8; ++k) st = st + (double)wt[s][k];
-            acc = acc + st;
-        }
+#pragma unroll
+        for (int s = 0; s < kSubTiles; ++s) acc = acc + sst[s];
         p.cmass[(int64_t)b * p.nchunks + c] = acc;
     }
 }
@@ -311,11 +361,20 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     const float uf = p.stage_mode ? p.u[b] : p.u[m.row_off[b] + gam];
     __shared__ int s_own;
     __shared__ double s_scale;
+    // the request's chunk masses -> smem with one parallel load (thread 0's
+    // fixed-order scans below then run on smem, not on dependent global loads)
+    constexpr int kMaxSmemChunks = 64;
+    __shared__ double scm[kMaxSmemChunks];
+    const bool cm_smem = p.nchunks <= kMaxSmemChunks;
+    if (cm_smem)
+        for (int c = threadIdx.x; c < p.nchunks; c += blockDim.x) scm[c] = __ldcg(&p.cmass[(int64_t)b * p.nchunks + c]);
+    __syncthreads();
+    const double* cm = cm_smem ? scm : p.cmass + (int64_t)b * p.nchunks;
     if (threadIdx.x == 0) {
         double P = 0.0, Pc = 0.0;
         int csel = -1, lastpos = -1;
         double W = 0.0;
-        for (int c = 0; c < p.nchunks; ++c) W = W + p.cmass[(int64_t)b * p.nchunks + c];
+        for (int c = 0; c < p.nchunks; ++c) W = W + cm[c];
         double T = (double)uf * W;
         int own = 1, zero_g = 0, clamp_g = 0;
         double scale = 1.0;   // local mass units -> natural (p) units
@@ -360,7 +419,7 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
         s_own = own;
         s_scale = scale;
         for (int c = 0; c < p.nchunks; ++c) {
-            const double wc = p.cmass[(int64_t)b * p.nchunks + c];
+            const double wc = cm[c];
             if (wc > 0.0) lastpos = c;
             if (csel < 0 && T < P + wc) { csel = c; Pc = P; }
             P = P + wc;
@@ -401,14 +460,21 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     for (int s = 0; s < kSubTiles; ++s) subtile_scan(w[s], inc[s], wt[s]);
     __syncthreads();
     __shared__ double spre[kSubTiles + 1];
+    __shared__ double sst[kSubTiles];
     __shared__ int ssel;
+    if (threadIdx.x < kSubTiles) {   // sub-tile totals in parallel (k_mass's order)
+        double st = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
+        sst[threadIdx.x] = st;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
         double acc = 0.0;
         int sel = -1, lastpos = -1;
         for (int s = 0; s < kSubTiles; ++s) {
             spre[s] = acc;
-            double st = 0.0;
-            for (int k = 0; k < 8; ++k) st = st + (double)wt[s][k];
+            const double st = sst[s];
             if (st > 0.0) lastpos = s;
             acc = acc + st;
             if (sel < 0 && tp < acc) sel = s;
