@@ -111,6 +111,7 @@ struct nj_ctx {
     int gemm_cg = 0;    // k_gemm_big CTA group: 0 auto, 1 single CTA, 2 CTA pair (NJ_CG)
     int gemm_pf = 0;    // k_gemm_big: W k-blocks prefetched into L2 ahead of the ring (NJ_PF)
     int gemm_maxt = 256;  // k_gemm_big: max token chunk (NJ_BIG_MAXT)
+    int gemm_teams = -1;  // k_gemm_big: two alternating epilogue teams (NJ_TEAMS; -1 auto)
     int U = 0;          // 16-row vocab units
     int max_tiles = 0;  // max 128-row tiles per CTA
     int nchunks = 0;    // sampler chunks
@@ -458,9 +459,15 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     }
     GemmBigParams gp = in;
     gp.R = R;
-    // CTA pair (cta_group::2) unless forced off or the token chunk is tiny
     const int CG = c->gemm_cg == 2 ? 2 : 1;
+    // two epilogue teams (alternate items) need chunks of <= 128 columns: 2 teams x
+    // 2 buffers x 128 TMEM columns
+    // (on by default only when the chunks are that narrow anyway: halving 256-wide
+    // chunks doubles the per-item costs, which outweighs the overlap)
     gp.nchunks = (R + c->gemm_maxt - 1) / c->gemm_maxt;
+    const bool narrow = (R + gp.nchunks - 1) / gp.nchunks <= 128;
+    gp.teams = (CG == 1 && (c->gemm_teams == 1 || (c->gemm_teams < 0 && narrow))) ? 2 : 1;
+    if (gp.teams == 2) gp.nchunks = (R + std::min(128, c->gemm_maxt) - 1) / std::min(128, c->gemm_maxt);
     gp.chunk = (R + gp.nchunks - 1) / gp.nchunks;
     gp.chunk = CG == 2 ? (gp.chunk + 31) & ~31 : round16(gp.chunk);   // pair: each CTA a multiple-of-16 half
     gp.V_local = c->V_local;
@@ -490,6 +497,7 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     // further ahead of the epilogue's per-item output
     gp.bstride = std::max(32, (gp.chunk + 31) & ~31);
     gp.nbuf = std::max(2, std::min(kBigMaxBuf, 512 / gp.bstride));
+    if (gp.teams == 2) gp.nbuf &= ~1;   // an even split between the teams
     if (const char* e = getenv("NJ_BIG_NBUF")) gp.nbuf = std::max(2, std::min(gp.nbuf, atoi(e)));
     gp.pf = c->gemm_pf;
     gp.dbg = 0;
@@ -507,7 +515,8 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     if (!encode_2d(&tmH, h, R, c->cfg.d, gp.chunk / CG))
         return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
     const size_t stage = (size_t)gp.gk * (kTileBytesA + (size_t)(gp.chunk / CG) * 128);
-    size_t tail = 4 * 4 * kBigNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
+    size_t tail = 4 * 4 * kBigNC * sizeof(float2) + (STATS ? (size_t)gp.teams * R * 8 : 0) +
+                  (CAPTURE ? (size_t)R * 4 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 2 * kBigMaxBuf) * 8 + 8;
     int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
     if (const char* e = getenv("NJ_BIG_S")) S = (gp.dbg & 4) ? std::min(64, atoi(e)) : std::min(S, std::max(2, atoi(e)));
@@ -920,6 +929,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     if (const char* e = getenv("NJ_CG")) c->gemm_cg = atoi(e);
     if (const char* e = getenv("NJ_PF")) c->gemm_pf = std::max(0, atoi(e));
     if (const char* e = getenv("NJ_BIG_MAXT")) c->gemm_maxt = std::min(256, std::max(32, atoi(e)));
+    if (const char* e = getenv("NJ_TEAMS")) c->gemm_teams = atoi(e) != 0;
     const size_t g = (size_t)c->grid, gp_ = (size_t)c->pld;
 #define A(ptr, n) if ((s = alloc(c, &c->ptr, (n))) != NJ_OK) { nj_destroy(c); return s; }
     A(part_m, (size_t)c->Nmax * gp_);

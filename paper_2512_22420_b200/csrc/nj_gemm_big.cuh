@@ -47,6 +47,9 @@ struct GemmBigParams {
     int32_t gk;                          // k-blocks per TMA ring stage (1, 2 or 4)
     int32_t ks;                          // k-blocks per accumulator restart (multiple of gk)
     int32_t nbuf, bstride;               // accumulator buffers (2..8) and their TMEM column stride
+    int32_t teams;                       // 2: two epilogue teams of 8 warps take alternate items
+                                         //    (buffers split between them), so one team's per-item
+                                         //    output overlaps the other's drains; 1: one team of 16
     int32_t rr;                          // 1: round-robin (tile, chunk) items over global 128-row tiles
     int32_t ntiles_g;                    // global 128-row tiles (rr mode)
     float* logits;                       // WRITE: [R][ld_out] fp32
@@ -126,7 +129,8 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
     uint8_t* ring = smem;                                             // S x GK x (A 16 KB | B bBytes)
     float2* scratch = reinterpret_cast<float2*>(ring + (size_t)S * stageBytes);   // [4 e][4 q][64]
     float2* state = scratch + 4 * 4 * kBigNC;                                       // [R] (STATS)
-    int32_t* stok = reinterpret_cast<int32_t*>(state + (STATS ? p.R : 0));         // [R] (CAPTURE)
+    const int TEAMS = p.teams;
+    int32_t* stok = reinterpret_cast<int32_t*>(state + (STATS ? TEAMS * p.R : 0));  // [R] (CAPTURE)
     uint64_t* bars = reinterpret_cast<uint64_t*>(
         (reinterpret_cast<uintptr_t>(stok + (CAPTURE ? p.R : 0)) + 7) & ~uintptr_t(7));
     uint64_t* full = bars;
@@ -160,7 +164,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         tma_prefetch_desc(&tmW16);
         tma_prefetch_desc(&tmH);
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int g = 0; g < NBUF; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kBigEpiWarps * CG); }
+        for (int g = 0; g < NBUF; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kBigEpiWarps / TEAMS * CG); }
         fence_barrier_init();
         fence_proxy_async();
     }
@@ -169,7 +173,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         else tmem_alloc(tmem_slot, 512);
     }
     if (STATS)
-        for (int i = threadIdx.x; i < p.R; i += kBigThreads) state[i] = make_float2(-INFINITY, 0.f);
+        for (int i = threadIdx.x; i < TEAMS * p.R; i += kBigThreads) state[i] = make_float2(-INFINITY, 0.f);
     if (CAPTURE)
         for (int i = threadIdx.x; i < p.R; i += kBigThreads) {
             if (p.use_row_g) stok[i] = p.row_g[i] >= 0 ? p.tok[p.row_g[i]] - p.v_begin : -1;
@@ -260,11 +264,16 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
             int s = 0;
             uint32_t ph = 0;
             int ngrp = 0;   // accumulator groups issued
-            int abuf = 0;   // accumulator buffer of the current group and its phase
+            // accumulator buffer (within the item's team) of the current group and its phase
+            const int NBT = NBUF / TEAMS;
+            int tbuf[2] = {0, 0};
+            uint32_t tph[2] = {0u, 0u};
+            int abuf = 0;
             uint32_t aph = 0;
             int mst = 0;
             int row0, trows, row0L, trowsL, trowsP, c;
             for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
+                const int team = it % TEAMS;
                 const int ncol = min(p.chunk, p.R - c * p.chunk);
                 const uint32_t nmma = CG == 2 ? (uint32_t)p.chunk : (uint32_t)((ncol + 15) & ~15);
                 const uint32_t idesc = idesc_bf16_f32(128 * CG, nmma);
@@ -281,6 +290,8 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                     uint8_t* st = ring + (size_t)s * stageBytes;
                     for (int g = 0; g < ng; ++g) {
                         if (kin == 0) {
+                            abuf = team * NBT + tbuf[team];
+                            aph = tph[team];
                             const bool tsa = p.ts && cta == 0 && ngrp < 2000;
                             if (tsa) p.ts[12288 + 2 * ngrp] = globaltimer();
                             if (p.spin) mbar_wait_spin(&aempty[abuf], aph ^ 1);
@@ -304,7 +315,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                             else if (CG == 2) mma_commit_mc2(&afull[abuf], 3);
                             else mma_commit(&afull[abuf]);
                             ++ngrp;
-                            if (++abuf == NBUF) { abuf = 0; aph ^= 1; }
+                            if (++tbuf[team] == NBT) { tbuf[team] = 0; tph[team] ^= 1; }
                             kin = 0;
                         }
                     }
@@ -320,10 +331,15 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
     } else {
         // ------------------------------------------------ epilogue (16 warps per CTA)
         const int q = warp & 3;             // TMEM lane quadrant this warp may access
-        const int e = (warp - 2) >> 2;      // 64-column slice
-        // column slice per warp: the chunk's columns spread over the 4 warps of a
-        // lane quadrant (16..64 columns), so small chunks still drain with all 16 warps
-        const int cw = min(kBigNC, max(16, ((p.chunk + 3) / 4 + 15) & ~15));
+        const int team = (warp - 2) / (kBigEpiWarps / TEAMS);
+        const int wi = (warp - 2) - team * (kBigEpiWarps / TEAMS);   // warp index within the team
+        const int EPT = 4 / TEAMS;          // column slices per team
+        const int e = wi >> 2;              // column slice of this warp
+        // column slice per warp: the chunk's columns spread over the team's warps of a
+        // lane quadrant (16..64 columns), so small chunks still drain with all warps
+        const int cw = min(kBigNC, max(16, ((p.chunk + EPT - 1) / EPT + 15) & ~15));
+        const int NBT = NBUF / TEAMS;       // this team's accumulator buffers
+        float2* tstate = state + (STATS ? team * p.R : 0);
         const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(e * cw);
         const int vr = q * 32 + lane;
         const uint64_t pol_keep = policy_evict_last();   // staged logits stay in L2 for the sampler
@@ -334,7 +350,7 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         int ngrp = 0, ebuf = 0;
         uint32_t eph = 0;
         int row0, trows, row0L, trowsL, trowsP, c;
-        for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
+        for (int it = team; next_item(it, row0, trows, row0L, trowsL, trowsP, c); it += TEAMS) {
             const int c0 = c * p.chunk;
             const int ncol = min(p.chunk, p.R - c0);
             const int myc = min(cw, ncol - e * cw);   // columns of this warp's slice that exist (may be <= 0)
@@ -342,13 +358,13 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
 #pragma unroll
             for (int j = 0; j < kBigNC; ++j) acc[j] = 0.f;
             for (int g = 0; g < ngroups; ++g, ++ngrp) {
-                const int buf = ebuf;
+                const int buf = team * NBT + ebuf;
                 const bool tse = p.ts && cta == 0 && warp == 2 && lane == 0 && ngrp < 2048;
                 if (tse) p.ts[8192 + 2 * ngrp] = globaltimer();
                 if (p.sleep_ns > 0) mbar_wait_sleep(&afull[buf], eph, (uint32_t)p.sleep_ns);
                 else if (p.spin & 2) mbar_wait_spin(&afull[buf], eph);
                 else mbar_wait(&afull[buf], eph);
-                if (++ebuf == NBUF) { ebuf = 0; eph ^= 1; }
+                if (++ebuf == NBT) { ebuf = 0; eph ^= 1; }
                 tc_fence_after();
                 const uint32_t ta = lane_base + (uint32_t)(buf * p.bstride);
                 if (p.dbg & 2) {
@@ -407,30 +423,33 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                         }
                         float wm, ws;
                         warp_scatter_ms<32>(tm, ts, wm, ws);
-                        scratch[(e * 4 + q) * kBigNC + hh * 32 + col_of_lane<32>(lane)] = make_float2(wm, ws);
+                        scratch[((team * EPT + e) * 4 + q) * kBigNC + hh * 32 + col_of_lane<32>(lane)] =
+                            make_float2(wm, ws);
                     }
                 }
-                named_bar(1 + e, 128);
-                const int ht = ((warp - 2) & 3) * 32 + lane;   // 0..127 within the slice's 4 warps
+                named_bar(1 + team * EPT + e, 128);
+                const int ht = (wi & 3) * 32 + lane;   // 0..127 within the slice's 4 warps
                 if (ht < kBigNC && ht < myc) {
                     const int col = c0 + e * cw + ht;
-                    float2 st = state[col];
+                    float2 st = tstate[col];
 #pragma unroll
                     for (int w = 0; w < 4; ++w) {
-                        const float2 o = scratch[(e * 4 + w) * kBigNC + ht];
+                        const float2 o = scratch[((team * EPT + e) * 4 + w) * kBigNC + ht];
                         ms_merge(st.x, st.y, o.x, o.y);
                     }
-                    state[col] = st;
+                    tstate[col] = st;
                 }
-                named_bar(1 + e, 128);
+                named_bar(1 + team * EPT + e, 128);
             }
         }
     }
     __syncthreads();
     if (STATS)
         for (int i = threadIdx.x; i < p.R; i += kBigThreads) {
-            p.part_m[(int64_t)i * p.part_ld + cta] = state[i].x;
-            p.part_s[(int64_t)i * p.part_ld + cta] = state[i].y;
+            float2 st = state[i];
+            if (TEAMS == 2) ms_merge(st.x, st.y, state[p.R + i].x, state[p.R + i].y);
+            p.part_m[(int64_t)i * p.part_ld + cta] = st.x;
+            p.part_s[(int64_t)i * p.part_ld + cta] = st.y;
         }
     tc_fence_before();
     __syncthreads();
