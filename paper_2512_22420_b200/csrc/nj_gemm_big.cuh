@@ -45,7 +45,8 @@ struct GemmBigParams {
     int32_t R, nchunks, chunk;           // rows, chunks, rows per chunk (multiple of 16, <= 256)
     int32_t V_local, U, num_kb, nstages, v_begin;
     int32_t gk;                          // k-blocks per TMA ring stage (1, 2 or 4)
-    int32_t ks;                          // k-blocks per accumulator restart (multiple of gk)
+    int32_t ks;                          // k-blocks per accumulator restart (multiple of gk; caller's
+                                         // nonzero value overrides the ctx default)
     int32_t nbuf, bstride;               // accumulator buffers (2..8) and their TMEM column stride
     int32_t teams;                       // 2: two epilogue teams of 8 warps take alternate items
                                          //    (buffers split between them), so one team's per-item

@@ -113,6 +113,7 @@ struct AcceptParams {
     int32_t nranks, xld;
     // lse of every partial row, precomputed by k_lse_rows (NULL: merge here)
     const double* pre_lse;
+    int32_t lse_sample_from_c;
 };
 
 // lse of partial rows [0, n) from the per-CTA partials, one warp per row (all
@@ -176,7 +177,9 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
         p.accept_len[b] = n;
         p.s_resid[b] = n < gam;
         p.s_qrow[b] = g0 + n;
-        p.s_lse[b] = lse_n;
+        // lse_sample_from_c: the sample row's lse comes from K-C's own statistics
+        // (the two-pass path's accurate sample-row GEMM), not from K-A's
+        p.s_lse[b] = p.lse_sample_from_c ? __longlong_as_double(0x7ff8000000000000ll) : lse_n;
         if (p.certify && (flag || p.force_fallback)) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 0);
     }
 }
