@@ -492,10 +492,11 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     // several launches writing one partial layout share the first launch's grid
     // (CTAs without items write (-inf, 0) partials)
     if (grid_force > 0) grid = CG == 2 ? (grid_force + 1) & ~1 : grid_force;
-    gp.gk = (gp.nchunks == 1 && gp.chunk <= 128) ? 2 : 1;
+    // ring stages of 3 k-blocks for chunks <= 128 columns (one barrier round trip per
+    // 48 KB of W: the per-stage loop cost, not bandwidth, bounds narrow chunks), 1 above
+    gp.gk = gp.chunk <= 128 ? 3 : 1;
     if (const char* e = getenv("NJ_BIG_GK")) gp.gk = std::max(1, atoi(e));
-    const int ks_req = in.ks > 0 ? in.ks : c->gemm_ks;
-    gp.ks = std::max(gp.gk, (ks_req + gp.gk - 1) / gp.gk * gp.gk);
+    gp.ks = in.ks > 0 ? in.ks : c->gemm_ks;   // accumulator groups are counted per k-block, not per stage
     // as many accumulator buffers as TMEM holds: small chunks let the MMAs run
     // further ahead of the epilogue's per-item output
     gp.bstride = std::max(32, (gp.chunk + 31) & ~31);
