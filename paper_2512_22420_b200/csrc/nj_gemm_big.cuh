@@ -67,7 +67,7 @@ struct GemmBigParams {
     unsigned long long* ts;              // debug timeline of CTA 0 (NJ_PHASE_TS): [0,4K) producer stage
                                          // starts, [4K,8K) MMA stage starts, [8K,12K) epilogue group ends
     int32_t dbg;                         // bottleneck probes (NJ_BIG_DBG): 1 no MMAs, 2 no TMEM drain,
-                                         // 4 no TMA loads, 8 no per-item epilogue output
+                                         // 4 no TMA loads, 8 no per-item epilogue output, 32 no logits stores
                                          // (results are garbage; timing only)
     int32_t use_row_g;                   // staged path: row r is draft row_g[r] (-1: bonus row)
     int32_t row_g[kBigMaxRowG];
@@ -175,6 +175,12 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
     }
     if (STATS)
         for (int i = threadIdx.x; i < TEAMS * p.R; i += kBigThreads) state[i] = make_float2(-INFINITY, 0.f);
+    // one token chunk: every item of this CTA covers the same columns, so each
+    // epilogue warp keeps its columns' running (m, s) in its own scratch slots
+    // across items (no per-item barriers); the quadrants merge once at the end
+    const bool one_chunk = p.nchunks == 1;
+    if (STATS && one_chunk)
+        for (int i = threadIdx.x; i < 4 * 4 * kBigNC; i += kBigThreads) scratch[i] = make_float2(-INFINITY, 0.f);
     if (CAPTURE)
         for (int i = threadIdx.x; i < p.R; i += kBigThreads) {
             if (p.use_row_g) stok[i] = p.row_g[i] >= 0 ? p.tok[p.row_g[i]] - p.v_begin : -1;
@@ -399,15 +405,36 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
             if (p.dbg & 8) continue;   // probe: no per-item output work
             const bool valid = vr < trows;
             const int xl = row0 + vr;
+            if (WRITE && !(p.dbg & 32)) {
 #pragma unroll
-            for (int j = 0; j < kBigNC; ++j) {
-                if (j < myc) {
-                    const int row = c0 + e * cw + j;
-                    if (WRITE && valid) st_evict_last(&p.logits[(int64_t)row * p.ld_out + xl], acc[j], pol_keep);
-                    if (CAPTURE && valid && stok[row] == xl) p.dl[p.use_row_g ? p.row_g[row] : row] = (double)acc[j];
+                for (int j = 0; j < kBigNC; ++j)
+                    if (j < myc && valid)
+                        st_evict_last(&p.logits[(int64_t)(c0 + e * cw + j) * p.ld_out + xl], acc[j], pol_keep);
+            }
+            if (CAPTURE && !(p.dbg & 128)) {
+                // which of this slice's rows draw their draft token from this tile: lanes
+                // test 2 rows each, a ballot gives the (rare: ~R/V_tiles per item) hits,
+                // the thread holding vocab row x - row0 writes that column's logit
+                const int rbase = c0 + e * cw;
+                const int ta = lane < myc ? stok[rbase + lane] - row0 : -1;
+                const int tb = lane + 32 < myc ? stok[rbase + lane + 32] - row0 : -1;
+                unsigned ma = __ballot_sync(0xffffffffu, ta >= 0 && ta < trows);
+                unsigned mb = __ballot_sync(0xffffffffu, tb >= 0 && tb < trows);
+                while (ma | mb) {
+                    const int j = ma ? __ffs(ma) - 1 : 32 + __ffs(mb) - 1;
+                    if (j < 32) ma &= ma - 1; else mb &= mb - 1;
+                    const int tv = __shfl_sync(0xffffffffu, j < 32 ? ta : tb, j & 31);
+                    if (tv == vr) {
+                        float val = 0.f;
+#pragma unroll
+                        for (int jj = 0; jj < kBigNC; ++jj)
+                            if (jj == j) val = acc[jj];
+                        const int row = rbase + j;
+                        p.dl[p.use_row_g ? p.row_g[row] : row] = (double)val;
+                    }
                 }
             }
-            if (STATS) {
+            if (STATS && !(p.dbg & 64)) {
                 // two reduce-scatters of 32 columns: lane l then owns column
                 // col_of_lane<32>(l) of each half -> scratch[e][q][col]; the 4
                 // quadrant warps of slice e merge them into the row state
@@ -424,10 +451,17 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                         }
                         float wm, ws;
                         warp_scatter_ms<32>(tm, ts, wm, ws);
-                        scratch[((team * EPT + e) * 4 + q) * kBigNC + hh * 32 + col_of_lane<32>(lane)] =
-                            make_float2(wm, ws);
+                        float2& sc = scratch[((team * EPT + e) * 4 + q) * kBigNC + hh * 32 + col_of_lane<32>(lane)];
+                        if (one_chunk) {
+                            float2 r = sc;
+                            ms_merge(r.x, r.y, wm, ws);
+                            sc = r;
+                        } else {
+                            sc = make_float2(wm, ws);
+                        }
                     }
                 }
+                if (one_chunk) continue;
                 named_bar(1 + team * EPT + e, 128);
                 const int ht = (wi & 3) * 32 + lane;   // 0..127 within the slice's 4 warps
                 if (ht < kBigNC && ht < myc) {
@@ -445,6 +479,22 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
         }
     }
     __syncthreads();
+    if (STATS && one_chunk) {   // merge the warps' running pairs: column i = slice e, offset ht
+        const int EPT = 4 / TEAMS;
+        const int cw = min(kBigNC, max(16, ((p.chunk + EPT - 1) / EPT + 15) & ~15));
+        for (int i = threadIdx.x; i < p.R; i += kBigThreads) {
+            const int e = i / cw, ht = i - e * cw;
+            for (int t = 0; t < TEAMS; ++t) {
+                float2 st = state[t * p.R + i];
+                for (int w = 0; w < 4; ++w) {
+                    const float2 o = scratch[((t * EPT + e) * 4 + w) * kBigNC + ht];
+                    ms_merge(st.x, st.y, o.x, o.y);
+                }
+                state[t * p.R + i] = st;
+            }
+        }
+        __syncthreads();
+    }
     if (STATS)
         for (int i = threadIdx.x; i < p.R; i += kBigThreads) {
             float2 st = state[i];
