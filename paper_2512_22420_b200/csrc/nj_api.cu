@@ -494,8 +494,8 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     if (grid_force > 0) grid = CG == 2 ? (grid_force + 1) & ~1 : grid_force;
     // ring stages of several k-blocks: the single-thread producer / MMA loops cost
     // ~600 cycles per stage, so a stage must carry more MMA work than
-    // that -- 3 k-blocks for chunks <= 128 columns, 2 above (96 KB stages, S = 2)
-    gp.gk = gp.chunk <= 128 ? 3 : 2;
+    // that -- 4 / 3 / 2 k-blocks for chunks of <= 64 / <= 128 / more columns (~96 KB stages)
+    gp.gk = gp.chunk <= 64 ? 4 : gp.chunk <= 128 ? 3 : 2;
     if (const char* e = getenv("NJ_BIG_GK")) gp.gk = std::max(1, atoi(e));
     gp.ks = in.ks > 0 ? in.ks : c->gemm_ks;   // accumulator groups are counted per k-block, not per stage
     // as many accumulator buffers as TMEM holds: small chunks let the MMAs run
