@@ -550,6 +550,13 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     return NJ_OK;
 }
 
+// k_mass CTAs per request: ~6 resident CTAs per SM in total, each looping over
+// its request's chunks (one dependent-load prologue per CTA instead of per chunk)
+int mass_split(const nj_ctx* c, int B) {
+    const int want = (c->num_sms * 6 + B - 1) / B;
+    return std::max(1, std::min(c->nchunks, want));
+}
+
 FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const int32_t* tok, const float* q,
                    int64_t ldq, const float* u, int32_t* acc, int32_t* nxt, const nj_debug* dbg) {
     FbParams f{};
@@ -779,7 +786,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = a.certify; mp.eps_draw = c->eps_draw;
         mp.xr2 = c->xr2; mp.nranks = c->nranks; mp.rank = c->rank; mp.xflags = c->x3 + pl.B;
-        k_mass<<<dim3(c->nchunks, pl.B), kSampThreads, 0, st>>>(mp);
+        k_mass<<<dim3(mass_split(c, pl.B), pl.B), kSampThreads, 0, st>>>(mp);
         NJ_LAUNCHED(c, "k_mass", st);
         k_xpack2<<<(pl.B + 7) / 8, 256, 0, st>>>(mp, pl.B, c->xs2);
         NJ_LAUNCHED(c, "k_xpack2", st);
@@ -1151,7 +1158,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = certify; mp.eps_draw = c->eps_draw;
-        k_mass<<<dim3(c->nchunks, pl.B), kSampThreads, 0, st>>>(mp);
+        k_mass<<<dim3(mass_split(c, pl.B), pl.B), kSampThreads, 0, st>>>(mp);
         NJ_LAUNCHED(c, "k_mass", st);
         k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
         NJ_LAUNCHED(c, "k_locate", st);
@@ -1218,7 +1225,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = certify; mp.eps_draw = c->eps_draw;
-        k_mass<<<dim3(c->nchunks, pl.B), kSampThreads, 0, st>>>(mp);
+        k_mass<<<dim3(mass_split(c, pl.B), pl.B), kSampThreads, 0, st>>>(mp);
         NJ_LAUNCHED(c, "k_mass", st);
         k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
         NJ_LAUNCHED(c, "k_locate", st);
@@ -1376,7 +1383,7 @@ nj_status nj_sample_from_logits(nj_ctx* c, void* stream, const float* logits, in
     mp.certify = c->certify; mp.eps_draw = 4e-6f;
     ReqMeta meta;
     meta.B = B;
-    k_mass<<<dim3(c->nchunks, B), kSampThreads, 0, st>>>(mp);
+    k_mass<<<dim3(mass_split(c, B), B), kSampThreads, 0, st>>>(mp);
     NJ_LAUNCHED(c, "k_mass", st);
     k_locate<<<B, kSampThreads, 0, st>>>(mp, meta);
     NJ_LAUNCHED(c, "k_locate", st);

@@ -295,57 +295,63 @@ __device__ __forceinline__ void subtile_scan(float w, float& inc, float* wt_sh) 
 }
 
 // K-D1: grid (nchunks, B).  Chunk masses.
+// K-D1: grid (nsplit, B); CTA (k, b) takes chunks k, k + nsplit, ... of request
+// b (one prologue per CTA; the next chunk's loads are issued before the current
+// chunk's scans so every thread keeps a chunk of loads in flight).
 __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p) {
-    const int c = blockIdx.x, b = blockIdx.y;
+    const int b = blockIdx.y;
     const double lse = sample_lse(p, b);
     const float lsef = (float)lse;
     const bool resid = p.s_resid[b] != 0;
     const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
     const float* lrow = logits_row(p, b);
     __shared__ float wt[kSubTiles][8];
-    // all 16 (or 32) loads of the chunk issued before any use, then the same
-    // weight expression as chunk_weight (k_locate recomputes it bit-identically)
-    float w[kSubTiles];
-    const int x0 = c * kChunk + (int)threadIdx.x;
-#pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) {
-        const int x = x0 + s * kSampThreads;
-        w[s] = x < p.V_local ? __ldcg(&lrow[x]) : -INFINITY;
-    }
-    if (resid) {
-        float qv[kSubTiles];
+    __shared__ double sst[kSubTiles];
+    // the same weight expression as chunk_weight (k_locate recomputes it bit-identically)
+    auto load = [&](int c, float (&l)[kSubTiles], float (&qv)[kSubTiles]) {
+        const int x0 = c * kChunk + (int)threadIdx.x;
 #pragma unroll
         for (int s = 0; s < kSubTiles; ++s) {
             const int x = x0 + s * kSampThreads;
-            qv[s] = x < p.V_local ? __ldg(&qrow[x]) : 0.f;
+            l[s] = x < p.V_local ? __ldcg(&lrow[x]) : -INFINITY;
         }
+        if (resid) {
 #pragma unroll
-        for (int s = 0; s < kSubTiles; ++s) w[s] = fmaxf(__expf(w[s] - lsef) - qv[s], 0.f);
-    } else {
+            for (int s = 0; s < kSubTiles; ++s) {
+                const int x = x0 + s * kSampThreads;
+                qv[s] = x < p.V_local ? __ldg(&qrow[x]) : 0.f;
+            }
+        }
+    };
+    float l[kSubTiles], qv[kSubTiles];
+    int c = blockIdx.x;
+    if (c < p.nchunks) load(c, l, qv);
+    for (; c < p.nchunks; c += gridDim.x) {
+        float w[kSubTiles];
 #pragma unroll
-        for (int s = 0; s < kSubTiles; ++s) w[s] = __expf(w[s] - lsef);
-    }
+        for (int s = 0; s < kSubTiles; ++s) w[s] = resid ? fmaxf(__expf(l[s] - lsef) - qv[s], 0.f) : __expf(l[s] - lsef);
+        if (c + (int)gridDim.x < p.nchunks) load(c + gridDim.x, l, qv);   // next chunk in flight
 #pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) {
-        float inc;
-        subtile_scan(w[s], inc, wt[s]);
-    }
-    __syncthreads();
-    // sub-tile totals in parallel (same left-to-right fp64 order as k_locate),
-    // then the chunk total over the 16 sub-tiles
-    __shared__ double sst[kSubTiles];
-    if (threadIdx.x < kSubTiles) {
-        double st = 0.0;
+        for (int s = 0; s < kSubTiles; ++s) {
+            float inc;
+            subtile_scan(w[s], inc, wt[s]);
+        }
+        __syncthreads();
+        // sub-tile totals in parallel (same left-to-right fp64 order as k_locate),
+        // then the chunk total over the 16 sub-tiles
+        if (threadIdx.x < kSubTiles) {
+            double st = 0.0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
-        sst[threadIdx.x] = st;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double acc = 0.0;
+            for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
+            sst[threadIdx.x] = st;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double acc = 0.0;
 #pragma unroll
-        for (int s = 0; s < kSubTiles; ++s) acc = acc + sst[s];
-        p.cmass[(int64_t)b * p.nchunks + c] = acc;
+            for (int s = 0; s < kSubTiles; ++s) acc = acc + sst[s];
+            p.cmass[(int64_t)b * p.nchunks + c] = acc;
+        }
     }
 }
 

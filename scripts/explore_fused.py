@@ -8,11 +8,11 @@ from synth.inputs import make_batch, make_weight
 import oracle
 dev = torch.device("cuda:0"); V, d = 152064, 3584
 W = make_weight(V, d, 0, dev)
-KN = ["NJ_SACC", "NJ_KPD", "NJ_KGROUP", "NJ_FGROUPS"]
-for (B, g) in [(8, 3), (4, 5), (8, 1), (16, 2)]:
+KN = ["NJ_SACC", "NJ_KPD", "NJ_KGROUP", "NJ_FGROUPS", "NJ_GRID"]
+for (B, g) in [(8, 3), (1, 0)]:
     b = make_batch(B, g, V=V, d=d, seed=11, device=dev, W=W)
     ref = None
-    for var in [{}, {"NJ_KGROUP": "3"}, {"NJ_KGROUP": "2"}]:
+    for var in [{}, {"NJ_GRID": "148"}, {"NJ_GRID": "144"}, {"NJ_GRID": "140"}]:
         for k in KN: os.environ.pop(k, None)
         os.environ.update(var)
         v = Verifier(d, V, max_batch=B, gamma_max=5); v.set_option(NJ_OPT_PATH, 1)
