@@ -509,6 +509,8 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     if (const char* e = getenv("NJ_BIG_DBG")) gp.dbg = atoi(e);
     gp.spin = 0;
     if (const char* e = getenv("NJ_SPIN")) gp.spin = atoi(e);
+    gp.stats_mode = 1;
+    if (const char* e = getenv("NJ_STATS")) gp.stats_mode = atoi(e);
     gp.sleep_ns = 0;
     if (const char* e = getenv("NJ_SLEEP")) gp.sleep_ns = atoi(e);
     gp.ts = nullptr;

@@ -97,6 +97,101 @@ __device__ __forceinline__ void warp_scatter_ms(float (&m)[NCP], float (&s)[NCP]
     so = s[0];
 }
 
+// The same reduce-scatter for 32 columns with every level a template
+// instantiation, so all register-array indices are compile-time constants
+// (the loop form above can leave m / s in local memory).  Lane l ends with
+// column col_of_lane<32>(l) == l.
+template <int H>
+__device__ __forceinline__ void scatter_ms_level(float (&m)[32], float (&s)[32], bool up) {
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+        const float sm_m = up ? m[j] : m[H + j];
+        const float sm_s = up ? s[j] : s[H + j];
+        float km = up ? m[H + j] : m[j];
+        float ks = up ? s[H + j] : s[j];
+        const float rm = __shfl_xor_sync(0xffffffffu, sm_m, H);
+        const float rs = __shfl_xor_sync(0xffffffffu, sm_s, H);
+        ms_merge(km, ks, rm, rs);
+        m[j] = km;
+        s[j] = ks;
+    }
+}
+// 16 columns over 32 lanes: lanes l and l ^ 1 both end with column l >> 1.
+template <int H>
+__device__ __forceinline__ void scatter_ms16_level(float (&m)[16], float (&s)[16], bool up) {
+#pragma unroll
+    for (int j = 0; j < H / 2; ++j) {
+        const float sm_m = up ? m[j] : m[H / 2 + j];
+        const float sm_s = up ? s[j] : s[H / 2 + j];
+        float km = up ? m[H / 2 + j] : m[j];
+        float ks = up ? s[H / 2 + j] : s[j];
+        const float rm = __shfl_xor_sync(0xffffffffu, sm_m, H);
+        const float rs = __shfl_xor_sync(0xffffffffu, sm_s, H);
+        ms_merge(km, ks, rm, rs);
+        m[j] = km;
+        s[j] = ks;
+    }
+}
+__device__ __forceinline__ void warp_scatter_ms16(float (&m)[16], float (&s)[16], float& mo, float& so) {
+    const int l = (int)lane_id();
+    scatter_ms16_level<16>(m, s, (l & 16) != 0);
+    scatter_ms16_level<8>(m, s, (l & 8) != 0);
+    scatter_ms16_level<4>(m, s, (l & 4) != 0);
+    scatter_ms16_level<2>(m, s, (l & 2) != 0);
+    const float rm = __shfl_xor_sync(0xffffffffu, m[0], 1);
+    const float rs = __shfl_xor_sync(0xffffffffu, s[0], 1);
+    ms_merge(m[0], s[0], rm, rs);
+    mo = m[0];
+    so = s[0];
+}
+// Plain-op version of scatter_ms16_level / warp_scatter_ms16 (lanes l, l ^ 1 end
+// with op over column l >> 1).
+template <int H, typename Op>
+__device__ __forceinline__ void scatter16_level(float (&v)[16], bool up, Op op) {
+#pragma unroll
+    for (int j = 0; j < H / 2; ++j) {
+        const float send = up ? v[j] : v[H / 2 + j];
+        const float keep = up ? v[H / 2 + j] : v[j];
+        v[j] = op(keep, __shfl_xor_sync(0xffffffffu, send, H));
+    }
+}
+template <typename Op>
+__device__ __forceinline__ float warp_scatter16(float (&v)[16], Op op) {
+    const int l = (int)lane_id();
+    scatter16_level<16>(v, (l & 16) != 0, op);
+    scatter16_level<8>(v, (l & 8) != 0, op);
+    scatter16_level<4>(v, (l & 4) != 0, op);
+    scatter16_level<2>(v, (l & 2) != 0, op);
+    return op(v[0], __shfl_xor_sync(0xffffffffu, v[0], 1));
+}
+// Column (max, sum e^{x - max}) of 16 columns with ONE exponential per element:
+// max reduce-scatter, the 16 column maxima broadcast back (lane 2j holds column
+// j), e^{x - max_j} summed by a second reduce-scatter.  x: -inf = invalid;
+// lanes l, l ^ 1 end with column l >> 1.
+__device__ __forceinline__ void warp_colstats16(const float (&x)[16], float& mo, float& so) {
+    float t[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) t[j] = x[j];
+    const float cm = warp_scatter16(t, [](float a, float b) { return fmaxf(a, b); });
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const float mj = __shfl_sync(0xffffffffu, cm, 2 * j);
+        t[j] = x[j] == -INFINITY ? 0.f : __expf(x[j] - mj);
+    }
+    mo = cm;
+    so = warp_scatter16(t, [](float a, float b) { return a + b; });
+}
+__device__ __forceinline__ void warp_scatter_ms32(float (&m)[32], float (&s)[32], float& mo, float& so) {
+    const int l = (int)lane_id();
+    scatter_ms_level<16>(m, s, (l & 16) != 0);
+    scatter_ms_level<8>(m, s, (l & 8) != 0);
+    scatter_ms_level<4>(m, s, (l & 4) != 0);
+    scatter_ms_level<2>(m, s, (l & 2) != 0);
+    scatter_ms_level<1>(m, s, (l & 1) != 0);
+    mo = m[0];
+    so = s[0];
+}
+
 constexpr int kFusedThreads = 384;   // warps 0-3 control, 4-11 epilogue (2 per TMEM lane quadrant)
 
 // residual / bonus weight of one vocab entry (BJ step 3); the lse shift is

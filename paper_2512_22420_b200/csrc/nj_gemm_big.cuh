@@ -63,6 +63,7 @@ struct GemmBigParams {
     int32_t w_evict_first;
     int32_t pf;                          // W k-blocks prefetched into L2 ahead of the TMA ring (0: off)
     int32_t spin;                        // 1: producer / MMA threads poll (test_wait); 2: epilogue too
+    int32_t stats_mode;                  // 1: column stats with one exponential per element
     int32_t sleep_ns;                    // epilogue accumulator waits: nanosleep backoff (0: try_wait)
     unsigned long long* ts;              // debug timeline of CTA 0 (NJ_PHASE_TS): [0,4K) producer stage
                                          // starts, [4K,8K) MMA stage starts, [8K,12K) epilogue group ends
@@ -403,6 +404,8 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 }
             }
             if (p.dbg & 8) continue;   // probe: no per-item output work
+            const bool tsi = p.ts && cta == 0 && warp == 2 && lane == 0 && it < 500;
+            if (tsi) p.ts[14336 + 4 * it] = globaltimer();
             const bool valid = vr < trows;
             const int xl = row0 + vr;
             if (WRITE && !(p.dbg & 32)) {
@@ -434,33 +437,42 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                     }
                 }
             }
+            if (tsi) p.ts[14336 + 4 * it + 1] = globaltimer();
             if (STATS && !(p.dbg & 64)) {
-                // two reduce-scatters of 32 columns: lane l then owns column
-                // col_of_lane<32>(l) of each half -> scratch[e][q][col]; the 4
-                // quadrant warps of slice e merge them into the row state
+                // per 16-column quarter: column (max, sum e^{x - max}) over the warp's
+                // 32 vocab rows with one exponential per element (the epilogue is
+                // MUFU-bound here); lanes 2j hold column j ->
+                // scratch[team, e][q][col]; the slice's 4 quadrant warps merge them
+                // into the row state (per item, or once at the end for one chunk)
                 if (myc > 0) {
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        if (hh * 32 >= myc) break;
-                        float tm[32], ts[32];
+                    for (int hh = 0; hh < 4; ++hh) {   // four 16-column quarters (fewer live registers)
+                        if (hh * 16 >= myc) break;
+                        float tm[16];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const bool ok = valid && hh * 32 + j < myc;
-                            tm[j] = ok ? acc[hh * 32 + j] : -INFINITY;
-                            ts[j] = ok ? 1.f : 0.f;
-                        }
+                        for (int j = 0; j < 16; ++j) tm[j] = (valid && hh * 16 + j < myc) ? acc[hh * 16 + j] : -INFINITY;
                         float wm, ws;
-                        warp_scatter_ms<32>(tm, ts, wm, ws);
-                        float2& sc = scratch[((team * EPT + e) * 4 + q) * kBigNC + hh * 32 + col_of_lane<32>(lane)];
-                        if (one_chunk) {
-                            float2 r = sc;
-                            ms_merge(r.x, r.y, wm, ws);
-                            sc = r;
+                        if (p.stats_mode) {
+                            warp_colstats16(tm, wm, ws);
                         } else {
-                            sc = make_float2(wm, ws);
+                            float ts[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) ts[j] = tm[j] == -INFINITY ? 0.f : 1.f;
+                            warp_scatter_ms16(tm, ts, wm, ws);
+                        }
+                        if (!(lane & 1)) {
+                            float2& sc = scratch[((team * EPT + e) * 4 + q) * kBigNC + hh * 16 + (lane >> 1)];
+                            if (one_chunk) {
+                                float2 r = sc;
+                                ms_merge(r.x, r.y, wm, ws);
+                                sc = r;
+                            } else {
+                                sc = make_float2(wm, ws);
+                            }
                         }
                     }
                 }
+                if (tsi) p.ts[14336 + 4 * it + 2] = globaltimer();
                 if (one_chunk) continue;
                 named_bar(1 + team * EPT + e, 128);
                 const int ht = (wi & 3) * 32 + lane;   // 0..127 within the slice's 4 warps

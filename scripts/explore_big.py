@@ -6,10 +6,10 @@ from paper_2512_22420_b200 import NJ_OPT_CERTIFY, NJ_OPT_PROFILE, Verifier
 from synth.inputs import make_batch, make_weight
 dev = torch.device("cuda:0"); V, d = 152064, 3584
 W = make_weight(V, d, 0, dev)
-KNOBS = ["NJ_CG", "NJ_PF", "NJ_BIG_S", "NJ_BIG_GK", "NJ_BIG_MAXT", "NJ_KS", "NJ_BIG_DBG", "NJ_SPIN", "NJ_SLEEP", "NJ_BIG_NBUF", "NJ_TEAMS", "NJ_KS_KA", "NJ_W_EVICT_FIRST"]
-variants = [{}, {"NJ_BIG_GK": "2"}, {"NJ_BIG_GK": "4"}, {"NJ_PF": "4"}, {"NJ_KS": "6"}]
+KNOBS = ["NJ_CG", "NJ_PF", "NJ_BIG_S", "NJ_BIG_GK", "NJ_BIG_MAXT", "NJ_KS", "NJ_BIG_DBG", "NJ_SPIN", "NJ_SLEEP", "NJ_BIG_NBUF", "NJ_TEAMS", "NJ_KS_KA", "NJ_W_EVICT_FIRST", "NJ_STATS"]
+variants = [{}, {"NJ_STATS": "0"}, {}, {"NJ_STATS": "0"}]
 out = {}
-for (B, g) in [(16, 3), (32, 3), (64, 3), (256, 5)]:
+for (B, g) in [(16, 3), (64, 3), (256, 5)]:
     b = make_batch(B, g, V=V, d=d, seed=5, device=dev, W=W)
     for var in variants:
         for k in KNOBS:
