@@ -514,6 +514,37 @@ def bench_c5(args, ws, rank, local):
     ms = e0.elapsed_time(e1)
     kms, kn = v.kernel_time(reset=True)
     v.set_option(NJ_OPT_PROFILE, 0)
+    ms_eager = ms
+    graph_ok = False
+    if not args.no_graph:
+        # one step (kernels + NCCL collectives on the stream) replayed from a CUDA graph
+        try:
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                step()
+                cap.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=cap):
+                    step()
+            stream.wait_stream(cap)
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clk:
+                g0.record(stream)
+                for _ in range(args.steps):
+                    graph.replay()
+                g1.record(stream)
+                torch.cuda.synchronize()
+            ms = g0.elapsed_time(g1)
+            graph_ok = True
+        except Exception as e:
+            print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
     t_max = njdist.max_over_ranks(ms, dev)
     toks = int((acc + 1).sum().item())
     hbm, tf_burst, _, peak_src = load_peaks()
@@ -561,7 +592,9 @@ def bench_c5(args, ws, rank, local):
                        "V": V_Q, "V_per_rank_max": max(shard_range(V_Q, ws, r)[1] - shard_range(V_Q, ws, r)[0]
                                                       for r in range(ws)),
                        "parallelism": f"vocab-sharded x{ws} (NCCL allgather x2 + allreduce-MAX per step)",
-                       "l2": "inputs larger than L2 at G <= 4; W shard streamed every step"},
+                       "l2": "inputs larger than L2 at G <= 4; W shard streamed every step",
+                       "launch": "CUDA graph replay per step" if graph_ok else "eager launches",
+                       "ms_per_step_eager": ms_eager / args.steps},
             "accepted_tokens_per_s": toks * args.steps / (t_max / 1e3),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": int(launches * args.steps)}
