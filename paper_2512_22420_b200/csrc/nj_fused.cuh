@@ -97,25 +97,6 @@ __device__ __forceinline__ void warp_scatter_ms(float (&m)[NCP], float (&s)[NCP]
     so = s[0];
 }
 
-// The same reduce-scatter for 32 columns with every level a template
-// instantiation, so all register-array indices are compile-time constants
-// (the loop form above can leave m / s in local memory).  Lane l ends with
-// column col_of_lane<32>(l) == l.
-template <int H>
-__device__ __forceinline__ void scatter_ms_level(float (&m)[32], float (&s)[32], bool up) {
-#pragma unroll
-    for (int j = 0; j < H; ++j) {
-        const float sm_m = up ? m[j] : m[H + j];
-        const float sm_s = up ? s[j] : s[H + j];
-        float km = up ? m[H + j] : m[j];
-        float ks = up ? s[H + j] : s[j];
-        const float rm = __shfl_xor_sync(0xffffffffu, sm_m, H);
-        const float rs = __shfl_xor_sync(0xffffffffu, sm_s, H);
-        ms_merge(km, ks, rm, rs);
-        m[j] = km;
-        s[j] = ks;
-    }
-}
 // 16 columns over 32 lanes: lanes l and l ^ 1 both end with column l >> 1.
 template <int H>
 __device__ __forceinline__ void scatter_ms16_level(float (&m)[16], float (&s)[16], bool up) {
@@ -181,17 +162,6 @@ __device__ __forceinline__ void warp_colstats16(const float (&x)[16], float& mo,
     mo = cm;
     so = warp_scatter16(t, [](float a, float b) { return a + b; });
 }
-__device__ __forceinline__ void warp_scatter_ms32(float (&m)[32], float (&s)[32], float& mo, float& so) {
-    const int l = (int)lane_id();
-    scatter_ms_level<16>(m, s, (l & 16) != 0);
-    scatter_ms_level<8>(m, s, (l & 8) != 0);
-    scatter_ms_level<4>(m, s, (l & 4) != 0);
-    scatter_ms_level<2>(m, s, (l & 2) != 0);
-    scatter_ms_level<1>(m, s, (l & 1) != 0);
-    mo = m[0];
-    so = s[0];
-}
-
 constexpr int kFusedThreads = 384;   // warps 0-3 control, 4-11 epilogue (2 per TMEM lane quadrant)
 
 // residual / bonus weight of one vocab entry (BJ step 3); the lse shift is

@@ -9,7 +9,7 @@ from synth.inputs import make_batch, make_weight
 lib = load(); lib.nj_debug_phase_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
 dev = torch.device("cuda:0"); V, d = 152064, 3584
 W = make_weight(V, d, 0, dev)
-for B, g, extra in [(64, 3, {}), (256, 5, {}), (16, 3, {}), (64, 3, {"NJ_KS": "8"})]:
+for B, g, extra in [(64, 3, {}), (16, 3, {})]:
     for k in ("NJ_KS",):
         os.environ.pop(k, None)
     os.environ.update(extra)
