@@ -440,8 +440,8 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
             if (tsi) p.ts[14336 + 4 * it + 1] = globaltimer();
             if (STATS && !(p.dbg & 64)) {
                 // per 16-column quarter: column (max, sum e^{x - max}) over the warp's
-                // 32 vocab rows with one exponential per element (the epilogue is
-                // MUFU-bound here); lanes 2j hold column j ->
+                // 32 vocab rows with one exponential per element;
+                // lanes 2j hold column j ->
                 // scratch[team, e][q][col]; the slice's 4 quadrant warps merge them
                 // into the row state (per item, or once at the end for one chunk)
                 if (myc > 0) {
