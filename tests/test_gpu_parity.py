@@ -314,3 +314,29 @@ def test_degenerate_inputs():
     b = make_batch(3, 2, V=16, d=8, seed=1, device=DEV)
     acc, nxt, dd, v = run(b)
     check(b, acc, nxt, dd)
+
+
+@pytest.mark.parametrize("B,g", [(8, 3), (48, 3), (150, 3)])
+def test_cuda_graph_capture_replay(B, g):
+    """nj_verify performs no host synchronisation, so one call is capturable in a
+    CUDA graph (bench.py times graph replays): replay == eager on every path."""
+    V, d = 4096, 128
+    b = make_batch(B, g, V=V, d=d, seed=B, device=DEV)
+    acc0, nxt0, _, v = run(b)
+    acc = torch.full((B,), -7, dtype=torch.int32, device=DEV)
+    nxt = torch.full((B,), -7, dtype=torch.int32, device=DEV)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        v.verify(b.hidden, b.W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+        s.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            v.verify(b.hidden, b.W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+    torch.cuda.current_stream().wait_stream(s)
+    acc.fill_(-7)
+    nxt.fill_(-7)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert (acc.cpu().numpy() == acc0).all() and (nxt.cpu().numpy() == nxt0).all()
