@@ -667,7 +667,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="nj", choices=["nj", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS) + ["c4", "c5"])
+    ap.add_argument("--config", default="c2", choices=sorted(set(CONFIGS) | {"c4", "c5"}))
     ap.add_argument("--path", default=None, choices=[None] + PATH_NAMES)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -151,6 +151,8 @@ struct nj_ctx {
     int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
     uint32_t* bar = nullptr;       // count, gen
     int32_t* fb_done = nullptr;    // k_fb completion counter
+    int mass_nst = 2;                 // k_mass cp.async ring stages (NJ_MASS_NST: 2..4; 2 = 3 CTAs / SM)
+    int mass_occ = 1;                 // resident k_mass CTAs per SM at mass_nst
     int32_t* scratch_i = nullptr;  // [MB]
     int32_t* s_row = nullptr;      // [MB] staged path: sample row of each request
     // vocab-sharded mode (nj_shard.cuh): rank / ranks, NCCL comm or nj_group member
@@ -552,11 +554,23 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     return NJ_OK;
 }
 
-// k_mass CTAs per request: ~6 resident CTAs per SM in total, each looping over
-// its request's chunks (one dependent-load prologue per CTA instead of per chunk)
-int mass_split(const nj_ctx* c, int B) {
-    const int want = (c->num_sms * 6 + B - 1) / B;
-    return std::max(1, std::min(c->nchunks, want));
+// K-D: [k_sample_lse when some sample-row lse is still NaN] + k_mass over a
+// grid of num_sms x resident CTAs taking (request, chunk) items round-robin.
+nj_status launch_mass(nj_ctx* c, cudaStream_t st, const MassParams& mp, int B, bool need_lse) {
+    if (B <= 0) return NJ_OK;
+    if (need_lse) {
+        k_sample_lse<<<(B + 7) / 8, 256, 0, st>>>(mp, B, const_cast<double*>(mp.s_lse));   // ctx-owned s_lse
+        NJ_LAUNCHED(c, "k_sample_lse", st);
+    }
+    const int total = B * c->nchunks;
+    const int grid = std::max(1, std::min(total, c->num_sms * c->mass_occ));
+    if (const char* e = getenv("NJ_MASS_PROBE")) const_cast<MassParams&>(mp).probe = atoi(e);
+    const size_t sm = mass_smem(c->mass_nst, B);
+    if (c->mass_nst == 2) k_mass<2><<<grid, kSampThreads, sm, st>>>(mp, B);
+    else if (c->mass_nst == 4) k_mass<4><<<grid, kSampThreads, sm, st>>>(mp, B);
+    else k_mass<3><<<grid, kSampThreads, sm, st>>>(mp, B);
+    NJ_LAUNCHED(c, "k_mass", st);
+    return NJ_OK;
 }
 
 FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const int32_t* tok, const float* q,
@@ -788,8 +802,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = a.certify; mp.eps_draw = c->eps_draw;
         mp.xr2 = c->xr2; mp.nranks = c->nranks; mp.rank = c->rank; mp.xflags = c->x3 + pl.B;
-        k_mass<<<dim3(mass_split(c, pl.B), pl.B), kSampThreads, 0, st>>>(mp);
-        NJ_LAUNCHED(c, "k_mass", st);
+        if ((s = launch_mass(c, st, mp, pl.B, true)) != NJ_OK) return s;
         k_xpack2<<<(pl.B + 7) / 8, 256, 0, st>>>(mp, pl.B, c->xs2);
         NJ_LAUNCHED(c, "k_xpack2", st);
         NJ_CUDA(c, cudaMemsetAsync(c->x3, 0, 2 * (size_t)pl.B * sizeof(int32_t), st));
@@ -992,10 +1005,19 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_gemm_big<false, true, true, 2>);
     e = e ? e : set_smem_attr(k_gemm_big<true, true, false, 2>);
     e = e ? e : set_smem_attr(k_gemm_big<true, true, true, 2>);
+    if (const char* ev = getenv("NJ_MASS_NST")) c->mass_nst = std::min(4, std::max(2, atoi(ev)));
+    e = e ? e : cudaFuncSetAttribute(k_mass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(2, c->cfg.max_batch));
+    e = e ? e : cudaFuncSetAttribute(k_mass<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(3, c->cfg.max_batch));
+    e = e ? e : cudaFuncSetAttribute(k_mass<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(4, c->cfg.max_batch));
+    e = e ? e : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                    &c->mass_occ, c->mass_nst == 2 ? k_mass<2> : c->mass_nst == 4 ? k_mass<4> : k_mass<3>, kSampThreads,
+                    mass_smem(c->mass_nst, c->cfg.max_batch));
     if (e != cudaSuccess) {
         nj_destroy(c);
         return set_err(nullptr, NJ_ECUDA, "cudaFuncSetAttribute failed: %s", cudaGetErrorString(e));
     }
+    if (const char* ev = getenv("NJ_MASS_OCC")) c->mass_occ = std::max(1, atoi(ev));
+    c->mass_occ = std::max(1, c->mass_occ);
     *out = c;
     return NJ_OK;
 }
@@ -1160,8 +1182,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = certify; mp.eps_draw = c->eps_draw;
-        k_mass<<<dim3(mass_split(c, pl.B), pl.B), kSampThreads, 0, st>>>(mp);
-        NJ_LAUNCHED(c, "k_mass", st);
+        if ((s = launch_mass(c, st, mp, pl.B, false)) != NJ_OK) return s;
         k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
         NJ_LAUNCHED(c, "k_locate", st);
     } else {
@@ -1227,8 +1248,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = certify; mp.eps_draw = c->eps_draw;
-        k_mass<<<dim3(mass_split(c, pl.B), pl.B), kSampThreads, 0, st>>>(mp);
-        NJ_LAUNCHED(c, "k_mass", st);
+        if ((s = launch_mass(c, st, mp, pl.B, true)) != NJ_OK) return s;
         k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
         NJ_LAUNCHED(c, "k_locate", st);
     }
@@ -1385,8 +1405,7 @@ nj_status nj_sample_from_logits(nj_ctx* c, void* stream, const float* logits, in
     mp.certify = c->certify; mp.eps_draw = 4e-6f;
     ReqMeta meta;
     meta.B = B;
-    k_mass<<<dim3(mass_split(c, B), B), kSampThreads, 0, st>>>(mp);
-    NJ_LAUNCHED(c, "k_mass", st);
+    if (nj_status s2 = launch_mass(c, st, mp, B, false)) return s2;
     k_locate<<<B, kSampThreads, 0, st>>>(mp, meta);
     NJ_LAUNCHED(c, "k_locate", st);
     if (c->certify) {

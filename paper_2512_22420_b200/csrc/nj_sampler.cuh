@@ -254,6 +254,7 @@ struct MassParams {
     const double* xr2;
     int32_t nranks, rank;
     int32_t* xflags;
+    int32_t probe;         // k_mass timing probes (NJ_MASS_PROBE; 0 in normal runs): 1 no copies, 2 no scans, 4 no totals
 };
 
 __device__ __forceinline__ void flag_draw(const MassParams& p, int b, int32_t bits) {
@@ -294,48 +295,127 @@ __device__ __forceinline__ void subtile_scan(float w, float& inc, float* wt_sh) 
     if (lane_id() == 31) wt_sh[warp_id()] = inc;
 }
 
-// K-D1: grid (nchunks, B).  Chunk masses.
-// K-D1: grid (nsplit, B); CTA (k, b) takes chunks k, k + nsplit, ... of request
-// b (one prologue per CTA; the next chunk's loads are issued before the current
-// chunk's scans so every thread keeps a chunk of loads in flight).
-__global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p) {
-    const int b = blockIdx.y;
-    const double lse = sample_lse(p, b);
-    const float lsef = (float)lse;
-    const bool resid = p.s_resid[b] != 0;
-    const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
-    const float* lrow = logits_row(p, b);
+// Sample-row lse of every request whose s_lse is NaN (bonus rows / the
+// two-pass path's K-C statistics), merged once per request so that k_mass's
+// items and k_locate read one value.  Warp per request.
+__global__ void k_sample_lse(const MassParams p, int B, double* s_lse) {   // s_lse == p.s_lse
+    const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
+    if (b >= B) return;
+    if (!isnan(__ldcg(&p.s_lse[b]))) return;
+    const double v = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
+    if (lane_id() == 0) s_lse[b] = v;
+}
+
+// K-D1: chunk masses.  Items (request b, chunk c), request-major, are taken
+// round-robin by a grid of num_sms x resident CTAs (every CTA sees a mix of
+// residual items, which read logits + q, and bonus items, which read logits
+// only).  Each CTA streams its items through a ring of NST shared-memory
+// stages with cp.async (16-byte copies where the rows are 16-byte aligned),
+// NST - 1 items in flight while it scans the current one, so the bytes in
+// flight per SM do not depend on the register budget.  Needs s_lse non-NaN
+// (k_sample_lse).  The per-item arithmetic (and so cmass) is the same
+// expression and order as k_locate's recomputation.
+__device__ __forceinline__ void mass_copy_chunk(float* dst, const float* src, int n) {
+    if (n == kChunk && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+        for (int k = 0; k < kChunk / 4 / kSampThreads; ++k) {
+            const int f = k * kSampThreads + (int)threadIdx.x;
+            cp_async16(dst + 4 * f, src + 4 * f);
+        }
+    } else if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        for (int f = threadIdx.x; 4 * f < n; f += kSampThreads) {
+            if (4 * f + 4 <= n) cp_async16(dst + 4 * f, src + 4 * f);
+            else
+                for (int e = 4 * f; e < n; ++e) cp_async4(dst + e, src + e);
+        }
+    } else {
+        for (int x = threadIdx.x; x < n; x += kSampThreads) cp_async4(dst + x, src + x);
+    }
+}
+
+template <int NST>
+__global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B) {
+    extern __shared__ __align__(16) float ring[];   // NST x {logits[kChunk], q[kChunk]}, then the request table
     __shared__ float wt[kSubTiles][8];
     __shared__ double sst[kSubTiles];
-    // the same weight expression as chunk_weight (k_locate recomputes it bit-identically)
-    auto load = [&](int c, float (&l)[kSubTiles], float (&qv)[kSubTiles]) {
-        const int x0 = c * kChunk + (int)threadIdx.x;
-#pragma unroll
-        for (int s = 0; s < kSubTiles; ++s) {
-            const int x = x0 + s * kSampThreads;
-            l[s] = x < p.V_local ? __ldcg(&lrow[x]) : -INFINITY;
+    // per-request scalars staged once per CTA: the item loop then has no
+    // dependent global load (each would cost a DRAM latency per item)
+    int* t_qrow = reinterpret_cast<int*>(ring + (size_t)NST * 2 * kChunk);   // -1: bonus row (no q)
+    float* t_lsef = reinterpret_cast<float*>(t_qrow + B);
+    for (int b = threadIdx.x; b < B; b += kSampThreads) {
+        t_qrow[b] = p.s_resid[b] ? p.s_qrow[b] : -1;
+        t_lsef[b] = (float)__ldcg(&p.s_lse[b]);
+    }
+    __syncthreads();
+    const int total = B * p.nchunks;
+    const int G = gridDim.x;
+    auto issue = [&](int it, int slot) {
+        if (it < total && !(p.probe & 1)) {
+            const int b = it / p.nchunks, c = it - b * p.nchunks;
+            const int x0 = c * kChunk, n = min(kChunk, p.V_local - x0);
+            float* d = ring + (size_t)slot * 2 * kChunk;
+            mass_copy_chunk(d, logits_row(p, b) + x0, n);
+            const int qr = t_qrow[b];
+            if (qr >= 0) mass_copy_chunk(d + kChunk, p.q + (int64_t)qr * p.ldq + p.v_begin + x0, n);
         }
-        if (resid) {
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) issue(blockIdx.x + s * G, s);
+    int j = 0;
+    for (int it = blockIdx.x; it < total; it += G, ++j) {
+        cp_async_wait<NST - 2>();
+        __syncthreads();   // item j's stage is visible; stage (j - 1) % NST is free
+        issue(it + (NST - 1) * G, (j + NST - 1) % NST);
+        const int b = it / p.nchunks, c = it - b * p.nchunks;
+        const int slot = j % NST;
+        const bool resid = t_qrow[b] >= 0;
+        const float lsef = t_lsef[b];
+        const float* sl = ring + (size_t)slot * 2 * kChunk;
+        const float* sq = sl + kChunk;
+        const int x0 = c * kChunk + (int)threadIdx.x;
+        float v[kSubTiles];
+        if (x0 - (int)threadIdx.x + kChunk <= p.V_local) {   // whole chunk in range
 #pragma unroll
             for (int s = 0; s < kSubTiles; ++s) {
-                const int x = x0 + s * kSampThreads;
-                qv[s] = x < p.V_local ? __ldg(&qrow[x]) : 0.f;
+                const int o = s * kSampThreads + (int)threadIdx.x;
+                const float e = __expf(sl[o] - lsef);
+                v[s] = resid ? fmaxf(e - sq[o], 0.f) : e;
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < kSubTiles; ++s) {
+                const int o = s * kSampThreads + (int)threadIdx.x;
+                const bool in = x0 + s * kSampThreads < p.V_local;
+                const float l = in ? sl[o] : -INFINITY;
+                v[s] = resid ? fmaxf(__expf(l - lsef) - (in ? sq[o] : 0.f), 0.f) : __expf(l - lsef);
             }
         }
-    };
-    float l[kSubTiles], qv[kSubTiles];
-    int c = blockIdx.x;
-    if (c < p.nchunks) load(c, l, qv);
-    for (; c < p.nchunks; c += gridDim.x) {
-        float w[kSubTiles];
+        if (!(p.probe & 2)) {
+            // The 16 warp totals by a reduce-scatter over lane bits 0, 1, 2, 3
+            // (each step halves the set a lane keeps) and a final xor-16 step:
+            // every total is the aligned binary tree over lanes 0..31, which is
+            // exactly the lane-31 value of warp_incl_scan (k_locate's sub-tile
+            // totals; fp32 addition is commutative), in 16 shuffles, not 80.
+            const uint32_t lane = lane_id();
 #pragma unroll
-        for (int s = 0; s < kSubTiles; ++s) w[s] = resid ? fmaxf(__expf(l[s] - lsef) - qv[s], 0.f) : __expf(l[s] - lsef);
-        if (c + (int)gridDim.x < p.nchunks) load(c + gridDim.x, l, qv);   // next chunk in flight
+            for (int m = 1, n = kSubTiles / 2; m <= 8; m <<= 1, n >>= 1) {
+                const bool hi = (lane & (uint32_t)m) != 0;
 #pragma unroll
-        for (int s = 0; s < kSubTiles; ++s) {
-            float inc;
-            subtile_scan(w[s], inc, wt[s]);
+                for (int k = 0; k < n; ++k) {
+                    const float keep = hi ? v[k + n] : v[k];
+                    const float send = hi ? v[k] : v[k + n];
+                    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                }
+            }
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
+            // lane bits (0, 1, 2, 3) chose halves (8, 4, 2, 1) of the sub-tile index
+            const int s = ((lane & 1) << 3) | ((lane & 2) << 1) | ((lane & 4) >> 1) | ((lane & 8) >> 3);
+            if (lane < 16) wt[s][warp_id()] = v[0];
+        } else if (v[0] == 1234.5f) {
+            wt[0][0] = v[1];
         }
+        if (p.probe & 4) continue;
         __syncthreads();
         // sub-tile totals in parallel (same left-to-right fp64 order as k_locate),
         // then the chunk total over the 16 sub-tiles
@@ -353,7 +433,9 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p) {
             p.cmass[(int64_t)b * p.nchunks + c] = acc;
         }
     }
+    cp_async_wait_all();
 }
+constexpr size_t mass_smem(int nst, int B) { return (size_t)nst * 2 * kChunk * sizeof(float) + (size_t)B * 8; }
 
 // K-D2: block per request.  Locate chunk -> sub-tile -> token.
 __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, const ReqMeta m) {
