@@ -288,12 +288,6 @@ __device__ __forceinline__ float chunk_weight(const MassParams& p, const float* 
     return resid ? fmaxf(pe - __ldg(&qrow[x]), 0.f) : pe;
 }
 
-// sub-tile total in fixed order: warp inclusive scans (fp32), warps summed
-// left-associatively in fp64.  wt[8] gets the warp totals.
-__device__ __forceinline__ void subtile_scan(float w, float& inc, float* wt_sh) {
-    inc = warp_incl_scan(w);
-    if (lane_id() == 31) wt_sh[warp_id()] = inc;
-}
 
 // Sample-row lse of every request whose s_lse is NaN (bonus rows / the
 // two-pass path's K-C statistics), merged once per request so that k_mass's
@@ -304,6 +298,30 @@ __global__ void k_sample_lse(const MassParams p, int B, double* s_lse) {   // s_
     if (!isnan(__ldcg(&p.s_lse[b]))) return;
     const double v = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
     if (lane_id() == 0) s_lse[b] = v;
+}
+
+// The 16 sub-tile warp totals of a thread's v[0..15] (destroyed) by a
+// reduce-scatter over lane bits 0, 1, 2, 3 (each step halves the set a lane
+// keeps) and a final xor-16 step: every total is the aligned binary tree over
+// lanes 0..31, which is exactly the lane-31 value of warp_incl_scan (fp32
+// addition is commutative; tests/test_reduction_order.py), in 16 shuffles
+// instead of 16 scans' 80.  wt[s][warp] gets sub-tile s's total.
+__device__ __forceinline__ void warp_totals16(float (&v)[kSubTiles], float (*wt)[8]) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int m = 1, n = kSubTiles / 2; m <= 8; m <<= 1, n >>= 1) {
+        const bool hi = (lane & (uint32_t)m) != 0;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+            const float keep = hi ? v[k + n] : v[k];
+            const float send = hi ? v[k] : v[k + n];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
+    // lane bits (0, 1, 2, 3) chose halves (8, 4, 2, 1) of the sub-tile index
+    const int s = ((lane & 1) << 3) | ((lane & 2) << 1) | ((lane & 4) >> 1) | ((lane & 8) >> 3);
+    if (lane < 16) wt[s][warp_id()] = v[0];
 }
 
 // K-D1: chunk masses.  Items (request b, chunk c), request-major, are taken
@@ -392,26 +410,7 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
             }
         }
         if (!(p.probe & 2)) {
-            // The 16 warp totals by a reduce-scatter over lane bits 0, 1, 2, 3
-            // (each step halves the set a lane keeps) and a final xor-16 step:
-            // every total is the aligned binary tree over lanes 0..31, which is
-            // exactly the lane-31 value of warp_incl_scan (k_locate's sub-tile
-            // totals; fp32 addition is commutative), in 16 shuffles, not 80.
-            const uint32_t lane = lane_id();
-#pragma unroll
-            for (int m = 1, n = kSubTiles / 2; m <= 8; m <<= 1, n >>= 1) {
-                const bool hi = (lane & (uint32_t)m) != 0;
-#pragma unroll
-                for (int k = 0; k < n; ++k) {
-                    const float keep = hi ? v[k + n] : v[k];
-                    const float send = hi ? v[k] : v[k + n];
-                    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-                }
-            }
-            v[0] += __shfl_xor_sync(0xffffffffu, v[0], 16);
-            // lane bits (0, 1, 2, 3) chose halves (8, 4, 2, 1) of the sub-tile index
-            const int s = ((lane & 1) << 3) | ((lane & 2) << 1) | ((lane & 4) >> 1) | ((lane & 8) >> 3);
-            if (lane < 16) wt[s][warp_id()] = v[0];
+            warp_totals16(v, wt);
         } else if (v[0] == 1234.5f) {
             wt[0][0] = v[1];
         }
@@ -544,11 +543,10 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     }
     const int c = shi[0];
     const double tp = sh[0];
-    float w[kSubTiles], inc[kSubTiles];
+    float w[kSubTiles], v[kSubTiles];
 #pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) w[s] = chunk_weight(p, lrow, c, s, lsef, resid, qrow);
-#pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) subtile_scan(w[s], inc[s], wt[s]);
+    for (int s = 0; s < kSubTiles; ++s) v[s] = w[s] = chunk_weight(p, lrow, c, s, lsef, resid, qrow);
+    warp_totals16(v, wt);   // k_mass's totals, bit for bit
     __syncthreads();
     __shared__ double spre[kSubTiles + 1];
     __shared__ double sst[kSubTiles];
@@ -578,10 +576,11 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     int s = ssel;
     const bool clamped = s < 0;
     if (clamped) s = -1 - s;
-    float ws = 0.f, is = 0.f;
+    float ws = 0.f;
 #pragma unroll
     for (int k = 0; k < kSubTiles; ++k)
-        if (k == s) { ws = w[k]; is = inc[k]; }
+        if (k == s) ws = w[k];
+    const float is = warp_incl_scan(ws);   // the located sub-tile's prefix only
     float ex = __shfl_up_sync(0xffffffffu, is, 1);
     if (lane_id() == 0) ex = 0.f;
     double Sq = 0.0;
