@@ -8,6 +8,8 @@ Bar (BASELINE.json north_star; R11/R12):
     tighter regression bound this build actually meets (DESIGN.md "accuracy");
   * sampler stage on given fp32 logits: W_b within 1e-5 relative.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 import torch
@@ -340,3 +342,19 @@ def test_cuda_graph_capture_replay(B, g):
         graph.replay()
     torch.cuda.synchronize()
     assert (acc.cpu().numpy() == acc0).all() and (nxt.cpu().numpy() == nxt0).all()
+
+
+@pytest.mark.parametrize("path", [NJ_PATH_FUSED, NJ_PATH_STAGED, NJ_PATH_TWOPASS])
+def test_strided_misaligned_draft_probs(path):
+    """q rows with pitch ldq = V + 3 floats (rows not 16-byte aligned: k_mass takes
+    its 4-byte cp.async path, the fused kernel its scalar q copies) give the same
+    decisions as contiguous q (the oracle's)."""
+    for V, d, B, g in [(QV, QD, 12, 3), (4099, 64, 10, "mixed:3")]:
+        W = w_full() if V == QV else None
+        b = make_batch(B, g, V=V, d=d, seed=V + B, device=DEV, W=W)
+        wide = torch.zeros(max(b.G, 1), V + 3, device=DEV)
+        wide[: b.G, :V] = b.draft_probs
+        b_strided = dataclasses.replace(b, draft_probs=wide[: b.G, :V])
+        assert b_strided.draft_probs.stride(0) == V + 3
+        acc, nxt, dd, _ = run(b_strided, path)
+        check(b, acc, nxt, dd)
