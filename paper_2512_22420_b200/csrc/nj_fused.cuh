@@ -553,15 +553,25 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
     }
     __syncthreads();
     NJ_STAMP(5);
-    // (d) the rejected requests' q slices [r0, r0+rows) -> smem (unless prefetched)
-    if (p.q_prefetch) cp_async_wait_all();
-    for (int b = 0; b < B && !p.q_prefetch; ++b) {
-        const int s = qslot[b];
-        if (s < 0) continue;
-        const float* src = p.q + (int64_t)req[b].qrow * p.ldq + p.v_begin + r0;
-        float* dst = qsl + (size_t)s * rows_cap;
-        for (int x = threadIdx.x; x < rows; x += kFusedThreads) dst[x] = __ldg(&src[x]);
+    // (d) the rejected requests' q slices [r0, r0+rows) -> smem (unless prefetched):
+    //     every slice's async copies in flight at once (q may be host memory read
+    //     in place, where a load-store loop would pay one link latency per request)
+    if (!p.q_prefetch) {
+        for (int b = 0; b < B; ++b) {
+            const int s = qslot[b];
+            if (s < 0) continue;
+            const float* src = p.q + (int64_t)req[b].qrow * p.ldq + p.v_begin + r0;
+            float* dst = qsl + (size_t)s * rows_cap;
+            if (p.q_vec16) {
+                const int n4 = (rows + 3) >> 2;
+                for (int i = threadIdx.x; i < n4; i += kFusedThreads) cp_async16(dst + 4 * i, src + 4 * i);
+            } else {
+                for (int x = threadIdx.x; x < rows; x += kFusedThreads) cp_async4(dst + x, src + x);
+            }
+        }
+        cp_async_commit();
     }
+    cp_async_wait_all();
     __syncthreads();
     NJ_STAMP(6);
 
