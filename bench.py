@@ -603,6 +603,139 @@ def bench_c5(args, ws, rank, local):
         dist.destroy_process_group()
 
 
+def bench_propose(args, ws, rank, local):
+    """the draft-side proposal step (nj_propose) at a
+    0.5B-style draft head (d = 896, V = 151936), B = 64 positions per step:
+    draft LM head -> q rows -> inverse-CDF draws.  Metric: proposed tokens/s.
+    Replicas only (each rank proposes for its own requests, no exchange)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2512_22420_b200 import NJ_OPT_PROFILE, Verifier
+    from paper_2512_22420_b200 import dist as njdist
+    from synth.inputs import make_batch, make_weight
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    DV, DD, B = 151936, 896, 64
+    W = make_weight(DV, DD, args.seed + 9, dev)
+    b = make_batch(B, 0, V=DV, d=DD, seed=args.seed + rank, device=dev, W=W)
+    v = Verifier(DD, DV, max_batch=B, gamma_max=1, device=local)
+    tok = torch.empty(B, dtype=torch.int32, device=dev)
+    q = torch.empty(B, DV, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        v.propose(b.hidden, W, b.uniforms, tok, q)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    v.set_option(NJ_OPT_PROFILE, 1)
+    v.kernel_time(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_eager = e0.elapsed_time(e1)
+    kms, kn = v.kernel_time(reset=True)
+    v.set_option(NJ_OPT_PROFILE, 0)
+    ms, graph_ok = ms_eager, False
+    clk = None
+    if not args.no_graph:
+        try:
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                step()
+                cap.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=cap):
+                    step()
+            stream.wait_stream(cap)
+            for _ in range(args.warmup):
+                graph.replay()
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clk:
+                g0.record(stream)
+                for _ in range(args.steps):
+                    graph.replay()
+                g1.record(stream)
+                torch.cuda.synchronize()
+            ms, graph_ok = g0.elapsed_time(g1), True
+        except Exception as e:
+            print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
+    t_max = njdist.max_over_ranks(ms, dev) if ws > 1 else ms
+    hbm, _, _, peak_src = load_peaks()
+    kern_ms = kms / max(kn, 1)
+    byts = 2 * DV * DD + 2 * B * DD + 4 * B * DV   # W once, hidden, fp32 logits written
+    roof = {"kernel": "k_gemm_big<logits,stats> (draft LM head)", "bound": "hbm",
+            "achieved": byts / (kern_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": byts / (kern_ms / 1e3) / 1e9 / hbm, "algorithmic_bytes_per_launch": byts,
+            "peak_source": peak_src, "kernel_ms_avg": kern_ms,
+            "kernel_share_of_step": kms / ms_eager if ms_eager > 0 else None, "traffic": None}
+    # end to end: pinned host hidden / uniforms in, tokens out (q stays on the device for nj_verify)
+    hh, uh = b.hidden.cpu().pin_memory(), b.uniforms.cpu().pin_memory()
+    th = torch.empty(B, dtype=torch.int32).pin_memory()
+    hd, ud = torch.empty_like(b.hidden), torch.empty_like(b.uniforms)
+    k_e2e = max(5, min(args.steps, 30))
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s0.record(stream)
+    for _ in range(k_e2e):
+        hd.copy_(hh, non_blocking=True)
+        ud.copy_(uh, non_blocking=True)
+        v.propose(hd, W, ud, tok, q)
+        th.copy_(tok, non_blocking=True)
+        stream.synchronize()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = s0.elapsed_time(s1)
+    e2e = {"value": B * k_e2e / (e_ms / 1e3), "unit": "proposed tokens/s", "h2d_bytes_per_step": int(B * DD * 2 + B * 4),
+           "d2h_bytes_per_step": int(B * 4), "steps": k_e2e, "api": "nj_propose (torch pinned copies around it)"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        n = b.to_numpy()
+        k = 2
+        runs, t0 = 0, time.perf_counter()
+        while True:
+            oracle.propose(n["hidden_bits"][:k], n["W_bits"], n["uniforms"][:k])
+            runs += 1
+            if time.perf_counter() - t0 > min(args.cpu_budget, 10.0) or runs >= 20:
+                break
+        dt = time.perf_counter() - t0
+        cpu = {"value": k * runs / dt, "unit": "proposed tokens/s", "cores": oracle.max_threads(), "kind": "oracle",
+               "sample": f"{runs} run(s) of {k} of the {B} positions, {dt:.1f} s"}
+    v.close()
+    if ws > 1:
+        dist.barrier()
+        if rank != 0:
+            dist.destroy_process_group()
+            return
+    line = {"metric": "proposed tokens/s (draft LM head + softmax + inverse-CDF draw)",
+            "value": B * ws * args.steps / (t_max / 1e3), "unit": "proposed tokens/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "draft_propose_0.5b_head", "B": B, "d": DD, "V": DV,
+                       "parallelism": f"replicas x{ws}", "l2": "inputs larger than L2 (W 272 MB streamed every step)",
+                       "launch": "CUDA graph replay per step" if graph_ok else "eager launches",
+                       "ms_per_step_eager": ms_eager / args.steps},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary() if clk else None,
+            "gpu_launches": 4 * args.steps}
+    emit(line)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 PATH_NAMES = ["auto", "fused", "twopass", "staged"]
 
 
@@ -667,7 +800,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="nj", choices=["nj", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(set(CONFIGS) | {"c4", "c5"}))
+    ap.add_argument("--config", default="c2", choices=sorted(set(CONFIGS) | {"c4", "c5", "propose"}))
     ap.add_argument("--path", default=None, choices=[None] + PATH_NAMES)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -690,6 +823,9 @@ def main():
         return
     if args.config == "c5" and args.impl != "reference":
         bench_c5(args, ws, rank, local)
+        return
+    if args.config == "propose" and args.impl != "reference":
+        bench_propose(args, ws, rank, local)
         return
     if args.impl == "reference":
         bench_reference(args, ws, rank)

@@ -227,6 +227,28 @@ nj_status nj_sample_from_logits(nj_ctx* ctx, void* stream,
                                 const float* u, int32_t B,
                                 int32_t* next_token, double* mass);
 
+/* Draft-side proposal step (PAPER.md:23 — the draft
+ * model proposes x_i ~ q_i, which the target then verifies): for B draft
+ * positions with final hidden states h_b of the DRAFT model,
+ *   l_b(x) = Σ_k W[x,k]·h_b[k]   (x < V; the draft LM head, e.g. d = 896,
+ *                                 V = 151936 for a 0.5B-style draft)
+ *   q_b(x) = exp(l_b(x) − lse_b),  lse_b = log Σ_x exp l_b(x)
+ *   x_b    = min{x : Σ_{y≤x} q_b(y) > u_b·Σ_y q_b(y)}   (inverse CDF, R5)
+ * Arguments (device pointers unless noted; the ctx is created with the draft's
+ * d and V, unsharded):
+ *   hidden  [B, d] bf16 row-major, 16-byte aligned
+ *   W_lm    [V, d] bf16 row-major (the draft LM head)
+ *   u       [B] fp32 in [0, 1): the draw's uniform per position
+ *   tokens  [B] int32 out: x_b
+ *   q_out   [B, ldq] fp32 out (ldq >= V): q_b, exactly the fp32 weights the
+ *           draw summed (so q_b(x_b) > 0) — the draft_probs rows nj_verify takes
+ * Same tcgen05 LM-head GEMM (accumulator restarted every 4 k-blocks, §6) and
+ * sampler kernels as nj_verify's staged / two-pass paths.  The draw is not
+ * certified (R16).  Errors: NJ_EINVAL (NULL), NJ_ESHAPE (B outside
+ * [1, max_batch], ldq < V), NJ_EUNSUPPORTED (sharded ctx). */
+nj_status nj_propose(nj_ctx* ctx, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
+                     const float* u, int32_t B, int32_t* tokens, float* q_out, int64_t ldq);
+
 /* ------------------------------------------------------ vocab-sharded mode */
 /* BJ config 5 / SURVEY §8a row a7, §8e: the LM head split along V over G
  * ranks (one process per GPU).  Rank r owns the contiguous, 128-row aligned

@@ -148,6 +148,21 @@ def verify(hidden_bits, W_bits, draft_tokens, draft_probs, gamma, uniforms,
     return out
 
 
+def propose(hidden_bits, W_bits, uniforms, tie_eps: float = TIE_EPS, nthreads: int = 0) -> dict:
+    """Draft-side proposal step (the
+    draft proposes x ~ q): q_b = softmax(l_b) of the draft LM head and x_b the
+    inverse-CDF draw of q_b with uniform u_b.  Written as the definition's two
+    pinned pieces: the fp64 logits (step 1) and verification with gamma = 0,
+    which draws from p_0 = softmax(l_0) (test_gamma0_is_inverse_cdf_of_p).
+    Returns tokens, q (fp64 [B, V]), lse and the draw's tie mask."""
+    L = logits(hidden_bits, W_bits, nthreads=nthreads)
+    B, V = L.shape
+    r = verify(hidden_bits, W_bits, np.zeros(0, np.int32), np.zeros((0, V), np.float32),
+               np.zeros(B, np.int32), uniforms, tie_eps=tie_eps, nthreads=nthreads)
+    q = np.exp(L - r["lse"][:, None])
+    return {"tokens": r["next_token"], "q": q, "lse": r["lse"], "tie": r["tie"]}
+
+
 def sample_from_logits(logits32, residual, q, u, tie_eps: float = TIE_EPS,
                        nthreads: int = 0) -> dict:
     """Stage-isolated sampler oracle on fp32 logits (R11(ii))."""

@@ -33,6 +33,7 @@ EXPORTS = [
     "nj_bandit_last_gamma", "nj_bandit_snapshot_json",
     "nj_shard_range", "nj_nccl_get_unique_id", "nj_nccl_comm_init", "nj_nccl_comm_destroy", "nj_group_create",
     "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify", "nj_mma_probe",
+    "nj_propose",
 ]
 NJ_NCCL_ID_BYTES = 128
 
@@ -80,6 +81,7 @@ def load():
         "nj_lmhead_logits": ([P, P, P, P, P, I32, P, I64], I32),
         "nj_lmhead_logits_ks": ([P, P, P, P, P, I32, P, I64, I32], I32),
         "nj_sample_from_logits": ([P, P, P, I64, P, P, I64, P, I32, P, P], I32),
+        "nj_propose": ([P, P, P, P, P, I32, P, P, I64], I32),
         "nj_bandit_create": ([I32, I32, U64, P, I32, P, I32, P, ctypes.POINTER(P)], I32),
         "nj_bandit_destroy": ([P], None),
         "nj_select_gamma": ([P, I32, I32], I32),
@@ -196,6 +198,13 @@ class Verifier:
     def lmhead_logits_ks(self, hidden, W, rows, out64, ks: int, stream=None):
         self._check(self._lib.nj_lmhead_logits_ks(self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(rows),
                                                   int(rows.shape[0]), _ptr(out64), int(out64.stride(0)), int(ks)))
+
+    def propose(self, hidden, W, u, tokens, q_out, stream=None):
+        """nj_propose: draft LM head + softmax + inverse-CDF draw (include/nj.h):
+        tokens[b] ~ q_out[b] = softmax(W @ hidden[b]) with uniform u[b]."""
+        self._check(self._lib.nj_propose(
+            self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(u), int(hidden.shape[0]), _ptr(tokens),
+            _ptr(q_out), int(q_out.stride(0))))
 
     def sample_from_logits(self, logits, residual, q, u, next_token, mass=None, stream=None):
         self._check(self._lib.nj_sample_from_logits(

@@ -1312,6 +1312,49 @@ nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, cons
     return NJ_OK;
 }
 
+nj_status nj_propose(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm, const float* u,
+                     int32_t B, int32_t* tokens, float* q_out, int64_t ldq) {
+    if (!c) return NJ_EINVAL;
+    if (!hidden || !W_lm || !u || !tokens || !q_out) return set_err(c, NJ_EINVAL, "NULL device pointer");
+    if (B < 1 || B > c->cfg.max_batch) return set_err(c, NJ_ESHAPE, "B=%d outside [1, max_batch=%d]", B, c->cfg.max_batch);
+    if (ldq < c->V_local) return set_err(c, NJ_ESHAPE, "ldq=%lld < V", (long long)ldq);
+    if (c->V_local != c->cfg.V || c->ncomm) return set_err(c, NJ_EUNSUPPORTED, "nj_propose is unsharded only");
+    if ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(W_lm)) & 15)
+        return set_err(c, NJ_ESHAPE, "hidden / W_lm must be 16-byte aligned");
+    nj_status s;
+    if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // draft LM head: fp32 logits straight into q_out + per-CTA (max, sum) partials
+    int grid = c->grid;
+    {
+        GemmBigParams gp{};
+        gp.logits = q_out; gp.ld_out = ldq;
+        gp.part_m = c->part2_m; gp.part_s = c->part2_s;
+        const bool rr = B > kBigMaxT && !c->gemm_acc;
+        std::pair<cudaEvent_t, cudaEvent_t> ev;
+        if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
+        if ((s = launch_lmhead<true, true, false>(c, st, hidden, B, gp, rr, &grid)) != NJ_OK) return s;
+        if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
+    }
+    k_lse_rows<<<(B + 7) / 8, 256, 0, st>>>(c->part2_m, c->part2_s, c->pld, grid, B, c->row_lse);
+    NJ_LAUNCHED(c, "k_lse_rows", st);
+    NJ_CUDA(c, cudaMemsetAsync(c->s_resid, 0, (size_t)B * sizeof(int32_t), st));   // every row: w = q
+    MassParams mp{};
+    mp.logits = q_out; mp.ld = ldq; mp.V_local = c->V_local; mp.v_begin = 0; mp.nchunks = c->nchunks;
+    mp.s_resid = c->s_resid; mp.s_qrow = c->scratch_i; mp.s_lse = c->row_lse;
+    mp.q = q_out; mp.ldq = ldq; mp.u = u; mp.stage_mode = 1; mp.cmass = c->cmass;
+    mp.next_token = tokens;
+    mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
+    mp.certify = 0; mp.eps_draw = 0.f;
+    mp.w_inplace = 1;   // k_mass leaves q = exp(l - lse) in q_out; k_locate reads it
+    if ((s = launch_mass(c, st, mp, B, false)) != NJ_OK) return s;
+    ReqMeta meta;
+    meta.B = B;
+    k_locate<<<B, kSampThreads, 0, st>>>(mp, meta);
+    NJ_LAUNCHED(c, "k_locate", st);
+    return NJ_OK;
+}
+
 nj_status nj_lmhead_logits(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
                            const int32_t* rows, int32_t n_rows, float* logits, int64_t ld_out) {
     if (!c) return NJ_EINVAL;

@@ -254,6 +254,9 @@ struct MassParams {
     const double* xr2;
     int32_t nranks, rank;
     int32_t* xflags;
+    // nj_propose: k_mass writes each bonus row's weights exp(l - lse) over its
+    // logits in place (the q rows), and k_locate then reads them as weights
+    int32_t w_inplace;
     int32_t probe;         // k_mass timing probes (NJ_MASS_PROBE; 0 in normal runs): 1 no copies, 2 no scans, 4 no totals
 };
 
@@ -284,7 +287,7 @@ __device__ __forceinline__ float chunk_weight(const MassParams& p, const float* 
                                               bool resid, const float* qrow) {
     const int x = c * kChunk + s * kSampThreads + (int)threadIdx.x;
     if (x >= p.V_local) return 0.f;
-    const float pe = __expf(__ldcg(&lrow[x]) - lsef);
+    const float pe = p.w_inplace ? __ldcg(&lrow[x]) : __expf(__ldcg(&lrow[x]) - lsef);
     return resid ? fmaxf(pe - __ldg(&qrow[x]), 0.f) : pe;
 }
 
@@ -407,6 +410,14 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
                 const bool in = x0 + s * kSampThreads < p.V_local;
                 const float l = in ? sl[o] : -INFINITY;
                 v[s] = resid ? fmaxf(__expf(l - lsef) - (in ? sq[o] : 0.f), 0.f) : __expf(l - lsef);
+            }
+        }
+        if (p.w_inplace && !resid) {   // nj_propose: q = the draw's weights, over the logits
+            float* wrow = const_cast<float*>(logits_row(p, b)) + c * kChunk;
+#pragma unroll
+            for (int s = 0; s < kSubTiles; ++s) {
+                const int o = s * kSampThreads + (int)threadIdx.x;
+                if (x0 + s * kSampThreads < p.V_local) wrow[o] = v[s];
             }
         }
         if (!(p.probe & 2)) {

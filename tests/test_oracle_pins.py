@@ -263,3 +263,29 @@ def test_sample_from_logits_matches_definition():
         assert abs(r["mass"][b] - w.sum()) < 1e-12
         if not r["tie"][b]:
             assert r["next_token"][b] == t
+
+
+def test_propose_draws_from_softmax_and_q_sums_to_one():
+    """oracle.propose (draft proposal): q rows are
+    probability vectors (sum 1 to 1e-12), equal to the fp64 softmax of the
+    logits, and the token is the inverse-CDF draw of q -- checked with
+    np.searchsorted on the cumulative q (an independent routine); a one-hot
+    logit row (one huge logit) draws its token for every u."""
+    b = make_batch(24, 0, V=700, d=32, seed=5)
+    n = _np(b)
+    r = oracle.propose(n["hidden_bits"], n["W_bits"], n["uniforms"])
+    assert np.allclose(r["q"].sum(axis=1), 1.0, atol=1e-12, rtol=0)
+    for i in range(24):
+        c = np.cumsum(r["q"][i])
+        t = int(np.searchsorted(c, float(n["uniforms"][i]) * c[-1], side="right"))
+        if not r["tie"][i]:
+            assert r["tokens"][i] == t
+    # peaked row: a hidden state aligned with one W row dominates
+    W = np.zeros((16, 8), np.float32); W[np.arange(16), np.arange(16) % 8] = 0.01
+    W[11] = 0.0; W[11, 3] = 64.0
+    h = np.zeros((3, 8), np.float32); h[:, 3] = 4.0
+    u = np.array([0.25, 0.5, 0.999], np.float32)
+    import torch
+    bf = lambda a: torch.tensor(a, dtype=torch.bfloat16)
+    rp = oracle.propose(bf(h), bf(W), u)
+    assert (rp["tokens"] == 11).all()
