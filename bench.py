@@ -736,6 +736,149 @@ def bench_propose(args, ws, rank, local):
         dist.destroy_process_group()
 
 
+def bench_greedy(args, ws, rank, local):
+    """greedy verification (argmax target,
+    nj_verify_greedy) at the Qwen shape, B = 8 (config greedy_c2) or B = 256,
+    gamma = 5 (greedy_b256g5).  Metric: verified positions/s.  Replicas only."""
+    import numpy as np
+    import torch
+
+    import oracle
+    from paper_2512_22420_b200 import NJ_OPT_PROFILE, Verifier
+    from paper_2512_22420_b200 import dist as njdist
+    from synth.inputs import make_batch, make_weight
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    B, g = (8, 3) if args.config == "greedy_c2" else (256, 5)
+    W = make_weight(V_Q, D_Q, args.seed, dev)
+    b = make_batch(B, g, V=V_Q, d=D_Q, seed=args.seed + rank, device=dev, W=W)
+    v = Verifier(D_Q, V_Q, max_batch=B, gamma_max=5, device=local)
+    acc = torch.empty(B, dtype=torch.int32, device=dev)
+    nxt = torch.empty(B, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    nblk = -(-b.N // 512)
+
+    def step():
+        v.verify_greedy(b.hidden, W, b.draft_tokens, b.gamma, acc, nxt)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    v.set_option(NJ_OPT_PROFILE, 1)
+    v.kernel_time(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_eager = e0.elapsed_time(e1)
+    kms, kn = v.kernel_time(reset=True)
+    v.set_option(NJ_OPT_PROFILE, 0)
+    ms, graph_ok, clk = ms_eager, False, None
+    if not args.no_graph:
+        try:
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.stream(cap):
+                step()
+                cap.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=cap):
+                    step()
+            stream.wait_stream(cap)
+            for _ in range(args.warmup):
+                graph.replay()
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clk:
+                g0.record(stream)
+                for _ in range(args.steps):
+                    graph.replay()
+                g1.record(stream)
+                torch.cuda.synchronize()
+            ms, graph_ok = g0.elapsed_time(g1), True
+        except Exception as e:
+            print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
+    t_max = njdist.max_over_ranks(ms, dev) if ws > 1 else ms
+    hbm, tf_burst, _, peak_src = load_peaks()
+    kern_ms = kms / max(kn, 1)
+    R = b.N / nblk
+    ridge = tf_burst * 1e12 / (hbm * 1e9)
+    if R < ridge:
+        byts = 2 * V_Q * D_Q + 2 * R * D_Q + 4 * R * V_Q
+        roof = {"kernel": "k_gemm_big<logits,stats> (all rows)", "bound": "hbm", "achieved": byts / (kern_ms / 1e3) / 1e9,
+                "peak": hbm, "unit": "GB/s", "frac": byts / (kern_ms / 1e3) / 1e9 / hbm,
+                "algorithmic_bytes_per_launch": byts}
+    else:
+        fl = 2.0 * R * V_Q * D_Q
+        roof = {"kernel": "k_gemm_big<logits,stats> (all rows)", "bound": "tensor",
+                "achieved": fl / (kern_ms / 1e3) / 1e12, "peak": tf_burst, "unit": "TFLOP/s",
+                "frac": fl / (kern_ms / 1e3) / 1e12 / tf_burst, "algorithmic_flops_per_launch": fl}
+    roof.update({"peak_source": peak_src, "kernel_ms_avg": kern_ms,
+                 "kernel_share_of_step": kms / ms_eager if ms_eager > 0 else None, "traffic": None, "rows": R})
+    # end to end: pinned host hidden + draft tokens in, accept_len / next_token out
+    hh, th = b.hidden.cpu().pin_memory(), b.draft_tokens.cpu().pin_memory()
+    hd, td = torch.empty_like(b.hidden), torch.empty_like(b.draft_tokens)
+    ah = torch.empty(B, dtype=torch.int32).pin_memory()
+    nh = torch.empty(B, dtype=torch.int32).pin_memory()
+    k_e2e = max(5, min(args.steps, 30))
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(k_e2e):
+        hd.copy_(hh, non_blocking=True)
+        td.copy_(th, non_blocking=True)
+        v.verify_greedy(hd, W, td, b.gamma, acc, nxt)
+        ah.copy_(acc, non_blocking=True)
+        nh.copy_(nxt, non_blocking=True)
+        stream.synchronize()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = s0.elapsed_time(s1)
+    e2e = {"value": b.N * k_e2e / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(hh.numel() * 2 + th.numel() * 4),
+           "d2h_bytes_per_step": int(2 * B * 4), "steps": k_e2e, "api": "nj_verify_greedy (torch pinned copies around it)"}
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        n = b.to_numpy()
+        k = min(B, 4)
+        nr, nd = int((n["gamma"][:k] + 1).sum()), int(n["gamma"][:k].sum())
+        runs, t0 = 0, time.perf_counter()
+        while True:
+            oracle.verify_greedy(n["hidden_bits"][:nr], n["W_bits"], n["draft_tokens"][:nd], n["gamma"][:k])
+            runs += 1
+            if time.perf_counter() - t0 > min(args.cpu_budget, 10.0) or runs >= 20:
+                break
+        dt = time.perf_counter() - t0
+        cpu = {"value": nr * runs / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+               "sample": f"{runs} run(s) of {k} of the {B} requests ({nr} positions), {dt:.1f} s"}
+    v.close()
+    if ws > 1:
+        dist.barrier()
+        if rank != 0:
+            dist.destroy_process_group()
+            return
+    line = {"metric": "verified positions/s (greedy target)", "value": b.N * ws * args.steps / (t_max / 1e3),
+            "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"qwen7b_greedy_B{B}_g{g}", "B": B, "gamma": g, "N_per_step": b.N, "d": D_Q,
+                       "V": V_Q, "parallelism": f"replicas x{ws}", "gemm_blocks": nblk,
+                       "l2": "inputs larger than L2 (W 1.09 GB streamed per block)",
+                       "launch": "CUDA graph replay per step" if graph_ok else "eager launches",
+                       "ms_per_step_eager": ms_eager / args.steps},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary() if clk else None,
+            "gpu_launches": (2 * nblk + 1) * args.steps}
+    emit(line)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 PATH_NAMES = ["auto", "fused", "twopass", "staged"]
 
 
@@ -800,7 +943,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="nj", choices=["nj", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(set(CONFIGS) | {"c4", "c5", "propose"}))
+    ap.add_argument("--config", default="c2", choices=sorted(set(CONFIGS) | {"c4", "c5", "propose", "greedy_c2", "greedy_b256g5"}))
     ap.add_argument("--path", default=None, choices=[None] + PATH_NAMES)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -823,6 +966,9 @@ def main():
         return
     if args.config == "c5" and args.impl != "reference":
         bench_c5(args, ws, rank, local)
+        return
+    if args.config.startswith("greedy") and args.impl != "reference":
+        bench_greedy(args, ws, rank, local)
         return
     if args.config == "propose" and args.impl != "reference":
         bench_propose(args, ws, rank, local)

@@ -249,6 +249,22 @@ nj_status nj_sample_from_logits(nj_ctx* ctx, void* stream,
 nj_status nj_propose(nj_ctx* ctx, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
                      const float* u, int32_t B, int32_t* tokens, float* q_out, int64_t ldq);
 
+/* Greedy verification (the target distribution is
+ * the argmax of its logits, temperature -> 0; the paper is silent on sampling
+ * settings).  With p_i = one-hot at a_i = argmax_x l_i(x) (ties ->
+ * lowest id), Leviathan's test u·q_i(x_i) < p_i(x_i) accepts
+ * x_i iff x_i == a_i for any u in [0,1) and q_i(x_i) <= 1, and the residual
+ * max(0, p_n − q_n) of the first rejected row is one-hot at a_n, so:
+ *   accept_len[b] = first i < γ_b with draft x_i != a_i (else γ_b)
+ *   next_token[b] = a_{n_b}  (the target's argmax at the first unmatched slot)
+ * draft_probs and uniforms are not needed.  Layout of hidden / draft_tokens /
+ * gamma_per_req as nj_verify.  Every row goes through the LM-head GEMM
+ * (fp32 logits of <= 512 rows at a time) and a row argmax.  Errors as
+ * nj_verify; NJ_EUNSUPPORTED on a vocab-sharded ctx. */
+nj_status nj_verify_greedy(nj_ctx* ctx, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
+                           const int32_t* draft_tokens, const int32_t* gamma_per_req, int32_t B,
+                           int32_t* accept_len, int32_t* next_token);
+
 /* ------------------------------------------------------ vocab-sharded mode */
 /* BJ config 5 / SURVEY §8a row a7, §8e: the LM head split along V over G
  * ranks (one process per GPU).  Rank r owns the contiguous, 128-row aligned

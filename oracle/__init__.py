@@ -148,6 +148,37 @@ def verify(hidden_bits, W_bits, draft_tokens, draft_probs, gamma, uniforms,
     return out
 
 
+def verify_greedy(hidden_bits, W_bits, draft_tokens, gamma, tie_gap: float = 1e-4, nthreads: int = 0) -> dict:
+    """Verification against the argmax target (the
+    temperature -> 0 limit of PAPER.md:23's sampled verification): a_j =
+    argmax_x l_j(x) in fp64 (ties -> lowest id); request b accepts its drafts
+    up to the first x_i != a_i and emits a_n.  ``tie`` marks requests whose
+    decision consulted a row with top-2 logit gap <= tie_gap (where fp32
+    logits may order the top two differently)."""
+    L = logits(hidden_bits, W_bits, nthreads=nthreads)
+    a = L.argmax(axis=1)
+    top2 = np.sort(L, axis=1)[:, -2:] if L.shape[1] > 1 else np.concatenate([L - np.inf, L], axis=1)
+    gap = top2[:, 1] - top2[:, 0]
+    g = np.asarray(gamma, np.int64)
+    x = np.asarray(draft_tokens, np.int64).reshape(-1)
+    B = g.shape[0]
+    acc = np.empty(B, np.int32)
+    nxt = np.empty(B, np.int32)
+    tie = np.zeros(B, bool)
+    ro = 0
+    for b in range(B):
+        g0 = ro - b
+        n = int(g[b])
+        for i in range(int(g[b])):
+            if x[g0 + i] != a[ro + i]:
+                n = i
+                break
+        acc[b], nxt[b] = n, a[ro + n]
+        tie[b] = bool((gap[ro:ro + n + 1] <= tie_gap).any())
+        ro += int(g[b]) + 1
+    return {"accept_len": acc, "next_token": nxt, "argmax": a, "gap": gap, "tie": tie}
+
+
 def propose(hidden_bits, W_bits, uniforms, tie_eps: float = TIE_EPS, nthreads: int = 0) -> dict:
     """Draft-side proposal step (the
     draft proposes x ~ q): q_b = softmax(l_b) of the draft LM head and x_b the

@@ -33,7 +33,7 @@ EXPORTS = [
     "nj_bandit_last_gamma", "nj_bandit_snapshot_json",
     "nj_shard_range", "nj_nccl_get_unique_id", "nj_nccl_comm_init", "nj_nccl_comm_destroy", "nj_group_create",
     "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify", "nj_mma_probe",
-    "nj_propose",
+    "nj_propose", "nj_verify_greedy",
 ]
 NJ_NCCL_ID_BYTES = 128
 
@@ -82,6 +82,7 @@ def load():
         "nj_lmhead_logits_ks": ([P, P, P, P, P, I32, P, I64, I32], I32),
         "nj_sample_from_logits": ([P, P, P, I64, P, P, I64, P, I32, P, P], I32),
         "nj_propose": ([P, P, P, P, P, I32, P, P, I64], I32),
+        "nj_verify_greedy": ([P, P, P, P, P, P, I32, P, P], I32),
         "nj_bandit_create": ([I32, I32, U64, P, I32, P, I32, P, ctypes.POINTER(P)], I32),
         "nj_bandit_destroy": ([P], None),
         "nj_select_gamma": ([P, I32, I32], I32),
@@ -198,6 +199,13 @@ class Verifier:
     def lmhead_logits_ks(self, hidden, W, rows, out64, ks: int, stream=None):
         self._check(self._lib.nj_lmhead_logits_ks(self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(rows),
                                                   int(rows.shape[0]), _ptr(out64), int(out64.stride(0)), int(ks)))
+
+    def verify_greedy(self, hidden, W, draft_tokens, gamma, accept_len, next_token, stream=None):
+        """nj_verify_greedy: verification against the argmax target (include/nj.h)."""
+        g = np.ascontiguousarray(np.asarray(gamma, dtype=np.int32))
+        self._check(self._lib.nj_verify_greedy(
+            self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(draft_tokens), g.ctypes.data, g.shape[0],
+            _ptr(accept_len), _ptr(next_token)))
 
     def propose(self, hidden, W, u, tokens, q_out, stream=None):
         """nj_propose: draft LM head + softmax + inverse-CDF draw (include/nj.h):

@@ -151,6 +151,7 @@ struct nj_ctx {
     int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
     uint32_t* bar = nullptr;       // count, gen
     int32_t* fb_done = nullptr;    // k_fb completion counter
+    int32_t* amax = nullptr;         // nj_verify_greedy: argmax per row [Nmax]
     int mass_nst = 2;                 // k_mass cp.async ring stages (NJ_MASS_NST: 2..4; 2 = 3 CTAs / SM)
     int mass_occ = 1;                 // resident k_mass CTAs per SM at mass_nst
     int32_t* scratch_i = nullptr;  // [MB]
@@ -982,6 +983,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     A(fb_done, 1);
     A(scratch_i, (size_t)MB);
     A(s_row, (size_t)MB);
+    A(amax, (size_t)c->Nmax);
 #undef A
     if (c->ncomm && (s = alloc_shard_ws(c)) != NJ_OK) { nj_destroy(c); return s; }
     if (cudaMemset(c->bar, 0, 2 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(c->fb_done, 0, sizeof(int32_t)) != cudaSuccess ||
@@ -1309,6 +1311,44 @@ nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, cons
     NJ_CUDA(c, cudaMemcpyAsync(acc_h, c->st_acc, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
     NJ_CUDA(c, cudaMemcpyAsync(next_h, c->st_next, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
     NJ_CUDA(c, cudaStreamSynchronize(st));
+    return NJ_OK;
+}
+
+nj_status nj_verify_greedy(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
+                           const int32_t* draft_tokens, const int32_t* gamma_per_req, int32_t B, int32_t* accept_len,
+                           int32_t* next_token) {
+    if (!c) return NJ_EINVAL;
+    Plan pl;
+    nj_status s = make_plan(c, gamma_per_req, B, pl);
+    if (s != NJ_OK) return s;
+    if (!hidden || !W_lm || !accept_len || !next_token || (pl.G > 0 && !draft_tokens))
+        return set_err(c, NJ_EINVAL, "NULL device pointer");
+    if (c->V_local != c->cfg.V || c->ncomm || !c->logits_st)
+        return set_err(c, NJ_EUNSUPPORTED, "nj_verify_greedy is unsharded only");
+    if ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(W_lm)) & 15)
+        return set_err(c, NJ_ESHAPE, "hidden / W_lm must be 16-byte aligned");
+    if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // all N rows through the LM-head GEMM in blocks of the staged logits buffer
+    // (one W stream per block), fp32 logits -> row argmax
+    const int cap = std::min(c->Nmax, kStagedMaxN);
+    for (int r0 = 0; r0 < pl.N; r0 += cap) {
+        const int R = std::min(cap, pl.N - r0);
+        GemmBigParams gp{};
+        gp.logits = c->logits_st; gp.ld_out = c->V_local;
+        gp.part_m = c->part_m; gp.part_s = c->part_s;   // statistics unused
+        int grid = c->grid;
+        std::pair<cudaEvent_t, cudaEvent_t> ev;
+        if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
+        if ((s = launch_lmhead<true, true, false>(c, st, hidden + (size_t)r0 * c->cfg.d, R, gp, false, &grid)) != NJ_OK)
+            return s;
+        if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
+        k_argmax_rows<<<R, 256, 0, st>>>(c->logits_st, c->V_local, c->V_local, c->amax + r0);
+        NJ_LAUNCHED(c, "k_argmax_rows", st);
+    }
+    const ReqMeta meta = make_meta(pl);
+    k_greedy_decide<<<(B + 127) / 128, 128, 0, st>>>(meta, draft_tokens, c->amax, accept_len, next_token);
+    NJ_LAUNCHED(c, "k_greedy_decide", st);
     return NJ_OK;
 }
 

@@ -447,6 +447,50 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
 }
 constexpr size_t mass_smem(int nst, int B) { return (size_t)nst * 2 * kChunk * sizeof(float) + (size_t)B * 8; }
 
+// nj_verify_greedy: argmax over the vocabulary of
+// each fp32 logits row (ties -> lowest id).  Block per row.
+__global__ void __launch_bounds__(256) k_argmax_rows(const float* __restrict__ logits, int64_t ld, int V,
+                                                      int32_t* __restrict__ out) {
+    const float* row = logits + (int64_t)blockIdx.x * ld;
+    float m = -INFINITY;
+    int mi = 0x7fffffff;
+    for (int x = threadIdx.x; x < V; x += blockDim.x) {
+        const float v = __ldcs(&row[x]);
+        if (v > m) { m = v; mi = x; }   // ascending x per thread: first maximum kept
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, mi, o);
+        if (m2 > m || (m2 == m && i2 < mi)) { m = m2; mi = i2; }
+    }
+    __shared__ float sm[8];
+    __shared__ int si[8];
+    if (lane_id() == 0) { sm[warp_id()] = m; si[warp_id()] = mi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x / 32); ++w)
+            if (sm[w] > m || (sm[w] == m && si[w] < mi)) { m = sm[w]; mi = si[w]; }
+        out[blockIdx.x] = mi == 0x7fffffff ? 0 : mi;
+    }
+}
+
+// Greedy target (p_i = one-hot at a_i = argmax l_i): Leviathan's test
+// u q(x) < p(x) accepts x_i iff x_i == a_i; the residual max(0, p - q) of the
+// first rejected row n is one-hot at a_n, and the bonus row gives a_gamma, so
+// next_token = a_n in every case.  Thread per request.
+__global__ void k_greedy_decide(const ReqMeta m, const int32_t* __restrict__ draft_tokens,
+                                const int32_t* __restrict__ amax, int32_t* accept_len, int32_t* next_token) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= m.B) return;
+    const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
+    int n = gam;
+    for (int i = 0; i < gam; ++i)
+        if (draft_tokens[g0 + i] != amax[ro + i]) { n = i; break; }
+    accept_len[b] = n;
+    next_token[b] = amax[ro + n];
+}
+
 // K-D2: block per request.  Locate chunk -> sub-tile -> token.
 __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, const ReqMeta m) {
     const int b = blockIdx.x;

@@ -289,3 +289,29 @@ def test_propose_draws_from_softmax_and_q_sums_to_one():
     bf = lambda a: torch.tensor(a, dtype=torch.bfloat16)
     rp = oracle.propose(bf(h), bf(W), u)
     assert (rp["tokens"] == 11).all()
+
+
+def test_greedy_is_zero_temperature_limit():
+    """oracle.verify_greedy equals the (pinned) sampled verification of the same
+    batch with W scaled by 2^16 -- exact in bf16 and in the fp64 logits, so the
+    target softmax is one-hot to < e^-6 wherever the top-2 gap exceeds 1e-4
+    (the greedy tie band)."""
+    import torch
+    b = make_batch(30, "mixed:5", V=300, d=32, seed=13)
+    n = _np(b)
+    Ws = (b.W.float() * 65536.0).to(torch.bfloat16)
+    assert torch.equal(Ws.float(), b.W.float() * 65536.0)
+    r_s = oracle.verify(n["hidden_bits"], oracle.bf16_bits(Ws), n["draft_tokens"], n["draft_probs"], n["gamma"],
+                        n["uniforms"])
+    r_g = oracle.verify_greedy(n["hidden_bits"], n["W_bits"], n["draft_tokens"], n["gamma"])
+    ok = ~r_g["tie"]
+    assert ok.sum() >= 25
+    assert (r_s["accept_len"][ok] == r_g["accept_len"][ok]).all()
+    assert (r_s["next_token"][ok] == r_g["next_token"][ok]).all()
+    # and a draft that copies the argmax is accepted in full
+    L = oracle.logits(n["hidden_bits"], n["W_bits"])
+    g = n["gamma"]
+    ro = np.concatenate([[0], np.cumsum(g + 1)])
+    x = np.concatenate([L[ro[b]:ro[b] + g[b]].argmax(axis=1) for b in range(len(g))]).astype(np.int32)
+    r2 = oracle.verify_greedy(n["hidden_bits"], n["W_bits"], x, g)
+    assert (r2["accept_len"] == g).all()
