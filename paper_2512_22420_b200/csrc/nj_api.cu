@@ -151,7 +151,7 @@ struct nj_ctx {
     int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
     uint32_t* bar = nullptr;       // count, gen
     int32_t* fb_done = nullptr;    // k_fb completion counter
-    int32_t* amax = nullptr;         // nj_verify_greedy: argmax per row [Nmax]
+    unsigned long long* amax = nullptr;   // nj_verify_greedy: per-row argmax keys [Nmax]
     int mass_nst = 2;                 // k_mass cp.async ring stages (NJ_MASS_NST: 2..4; 2 = 3 CTAs / SM)
     int mass_occ = 1;                 // resident k_mass CTAs per SM at mass_nst
     int32_t* scratch_i = nullptr;  // [MB]
@@ -1332,6 +1332,7 @@ nj_status nj_verify_greedy(nj_ctx* c, void* stream, const uint16_t* hidden, cons
     // all N rows through the LM-head GEMM in blocks of the staged logits buffer
     // (one W stream per block), fp32 logits -> row argmax
     const int cap = std::min(c->Nmax, kStagedMaxN);
+    NJ_CUDA(c, cudaMemsetAsync(c->amax, 0, (size_t)pl.N * sizeof(unsigned long long), st));
     for (int r0 = 0; r0 < pl.N; r0 += cap) {
         const int R = std::min(cap, pl.N - r0);
         GemmBigParams gp{};
@@ -1343,7 +1344,8 @@ nj_status nj_verify_greedy(nj_ctx* c, void* stream, const uint16_t* hidden, cons
         if ((s = launch_lmhead<true, true, false>(c, st, hidden + (size_t)r0 * c->cfg.d, R, gp, false, &grid)) != NJ_OK)
             return s;
         if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
-        k_argmax_rows<<<R, 256, 0, st>>>(c->logits_st, c->V_local, c->V_local, c->amax + r0);
+        const int nsplit = std::max(1, std::min((c->V_local + 2047) / 2048, (c->num_sms * 4 + R - 1) / R));
+        k_argmax_rows<<<dim3(nsplit, R), 256, 0, st>>>(c->logits_st, c->V_local, c->V_local, c->amax + r0);
         NJ_LAUNCHED(c, "k_argmax_rows", st);
     }
     const ReqMeta meta = make_meta(pl);

@@ -448,30 +448,50 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
 constexpr size_t mass_smem(int nst, int B) { return (size_t)nst * 2 * kChunk * sizeof(float) + (size_t)B * 8; }
 
 // nj_verify_greedy: argmax over the vocabulary of
-// each fp32 logits row (ties -> lowest id).  Block per row.
+// each fp32 logits row (ties -> lowest id).  Grid (nsplit, rows): a CTA scans
+// one contiguous segment of a row with 8 loads in flight per thread and folds
+// its (max, id) into the row's 64-bit key by atomicMax: key = order-preserving
+// float bits << 32 | (0xffffffff - id), so the largest key is the largest
+// logit with the lowest id.  keys must be zero on entry.
+__device__ __forceinline__ unsigned long long argmax_key(float v, int x) {
+    const uint32_t u = __float_as_uint(v);
+    const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((unsigned long long)o << 32) | (unsigned long long)(0xffffffffu - (uint32_t)x);
+}
 __global__ void __launch_bounds__(256) k_argmax_rows(const float* __restrict__ logits, int64_t ld, int V,
-                                                      int32_t* __restrict__ out) {
-    const float* row = logits + (int64_t)blockIdx.x * ld;
-    float m = -INFINITY;
-    int mi = 0x7fffffff;
-    for (int x = threadIdx.x; x < V; x += blockDim.x) {
-        const float v = __ldcs(&row[x]);
-        if (v > m) { m = v; mi = x; }   // ascending x per thread: first maximum kept
+                                                      unsigned long long* __restrict__ keys) {
+    const float* row = logits + (int64_t)blockIdx.y * ld;
+    const int seg = (V + gridDim.x - 1) / gridDim.x;
+    const int x0 = blockIdx.x * seg, x1 = min(V, x0 + seg);
+    unsigned long long best = 0ull;
+    constexpr int U = 8;
+    for (int base = x0 + (int)threadIdx.x; base < x1; base += U * 256) {
+        float v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int x = base + k * 256;
+            v[k] = x < x1 ? __ldcs(&row[x]) : -INFINITY;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int x = base + k * 256;
+            if (x < x1) {
+                const unsigned long long key = argmax_key(v[k], x);
+                best = key > best ? key : best;
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, mi, o);
-        if (m2 > m || (m2 == m && i2 < mi)) { m = m2; mi = i2; }
+        const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, best, o);
+        best = k2 > best ? k2 : best;
     }
-    __shared__ float sm[8];
-    __shared__ int si[8];
-    if (lane_id() == 0) { sm[warp_id()] = m; si[warp_id()] = mi; }
+    __shared__ unsigned long long sk[8];
+    if (lane_id() == 0) sk[warp_id()] = best;
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x / 32); ++w)
-            if (sm[w] > m || (sm[w] == m && si[w] < mi)) { m = sm[w]; mi = si[w]; }
-        out[blockIdx.x] = mi == 0x7fffffff ? 0 : mi;
+        for (int w = 1; w < (int)(blockDim.x / 32); ++w) best = sk[w] > best ? sk[w] : best;
+        if (best) atomicMax(&keys[blockIdx.y], best);
     }
 }
 
@@ -479,16 +499,20 @@ __global__ void __launch_bounds__(256) k_argmax_rows(const float* __restrict__ l
 // u q(x) < p(x) accepts x_i iff x_i == a_i; the residual max(0, p - q) of the
 // first rejected row n is one-hot at a_n, and the bonus row gives a_gamma, so
 // next_token = a_n in every case.  Thread per request.
+__device__ __forceinline__ int argmax_of_key(unsigned long long k) {
+    return (int)(0xffffffffu - (uint32_t)(k & 0xffffffffull));
+}
 __global__ void k_greedy_decide(const ReqMeta m, const int32_t* __restrict__ draft_tokens,
-                                const int32_t* __restrict__ amax, int32_t* accept_len, int32_t* next_token) {
+                                const unsigned long long* __restrict__ keys, int32_t* accept_len,
+                                int32_t* next_token) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= m.B) return;
     const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
     int n = gam;
     for (int i = 0; i < gam; ++i)
-        if (draft_tokens[g0 + i] != amax[ro + i]) { n = i; break; }
+        if (draft_tokens[g0 + i] != argmax_of_key(keys[ro + i])) { n = i; break; }
     accept_len[b] = n;
-    next_token[b] = amax[ro + n];
+    next_token[b] = argmax_of_key(keys[ro + n]);
 }
 
 // K-D2: block per request.  Locate chunk -> sub-tile -> token.
