@@ -137,9 +137,20 @@ def bench_reference(args, ws, rank):
     import oracle
     from synth.inputs import make_batch, make_weight
 
-    B, gamma, _ = CONFIGS[args.config]
-    W = make_weight(V_Q, D_Q, args.seed)
-    b = make_batch(B, gamma, V=V_Q, d=D_Q, seed=args.seed, W=W)
+    metric, unit = METRIC, UNIT
+    Vr, dr = V_Q, D_Q
+    if args.config == "propose":                       # draft proposal row
+        B, gamma, Vr, dr = 64, 0, 151936, 896
+        metric, unit = "proposed tokens/s (draft LM head + softmax + inverse-CDF draw)", "proposed tokens/s"
+    elif args.config.startswith("greedy"):             # greedy verification row
+        B, gamma = (8, 3) if args.config == "greedy_c2" else (256, 5)
+        metric = "verified positions/s (greedy target)"
+    elif args.config == "c4":                          # the trace's largest batch shape
+        B, gamma = 256, "mixed:5"
+    else:
+        B, gamma, _ = CONFIGS[args.config]
+    W = make_weight(Vr, dr, args.seed + (9 if args.config == "propose" else 0))
+    b = make_batch(B, gamma, V=Vr, d=dr, seed=args.seed, W=W)
     n = b.to_numpy()
     g = n["gamma"]
     ro = np.concatenate([[0], np.cumsum(g + 1)])
@@ -148,9 +159,14 @@ def bench_reference(args, ws, rank):
     def one(i):
         k = i % B
         sl = slice(ro[k], ro[k + 1])
-        oracle.verify(n["hidden_bits"][sl], n["W_bits"], n["draft_tokens"][do[k]:do[k + 1]],
-                      n["draft_probs"][do[k]:do[k + 1]] if g[k] else n["draft_probs"][:1], g[k:k + 1],
-                      n["uniforms"][sl])
+        if args.config == "propose":
+            oracle.propose(n["hidden_bits"][sl], n["W_bits"], n["uniforms"][sl])
+        elif args.config.startswith("greedy"):
+            oracle.verify_greedy(n["hidden_bits"][sl], n["W_bits"], n["draft_tokens"][do[k]:do[k + 1]], g[k:k + 1])
+        else:
+            oracle.verify(n["hidden_bits"][sl], n["W_bits"], n["draft_tokens"][do[k]:do[k + 1]],
+                          n["draft_probs"][do[k]:do[k + 1]] if g[k] else n["draft_probs"][:1], g[k:k + 1],
+                          n["uniforms"][sl])
         return int(g[k]) + 1
 
     for i in range(args.warmup):
@@ -159,14 +175,14 @@ def bench_reference(args, ws, rank):
     pos = sum(one(i) for i in range(args.steps))
     dt = time.perf_counter() - t0
     val = pos / dt
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+    line = {"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"qwen7b_{args.config}", "B": B, "gamma": gamma, "d": D_Q, "V": V_Q,
+            "config": {"workload": f"qwen7b_{args.config}", "B": B, "gamma": gamma, "d": dr, "V": Vr,
                        "step": "one request of the batch (bounded sample)"},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": unit, "cores": oracle.max_threads(), "kind": "oracle",
                              "sample": f"{args.steps} single-request steps of the {args.config} batch"},
-            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
 
@@ -961,7 +977,7 @@ def main():
     if args.sweep:
         bench_sweep(args, ws, rank, local)
         return
-    if args.config == "c4":
+    if args.config == "c4" and args.impl != "reference":
         bench_c4(args, ws, rank, local)
         return
     if args.config == "c5" and args.impl != "reference":
