@@ -59,8 +59,11 @@ def _load():
         lib.oracle_logits.argtypes = [P, P, I64, P, I64, I64, P, ctypes.c_int]
         lib.oracle_logits.restype = ctypes.c_int
         lib.oracle_verify.argtypes = [P, P, I64, I64, P, P, I64, P, P, I32, P, P,
-                                      P, P, P, P, P, P, P, P, P, D, ctypes.c_int]
+                                      P, P, P, P, P, P, P, P, P, P, D, ctypes.c_int]
         lib.oracle_verify.restype = ctypes.c_int
+        lib.oracle_verify_logits.argtypes = [P, I64, P, P, I64, P, P, I32, P, P,
+                                             P, P, P, P, P, P, P, P, P, P, D, ctypes.c_int]
+        lib.oracle_verify_logits.restype = ctypes.c_int
         lib.oracle_sample_from_logits.argtypes = [P, I64, I64, P, P, I64, P, I32, P, P,
                                                   P, P, P, D, ctypes.c_int]
         lib.oracle_sample_from_logits.restype = ctypes.c_int
@@ -104,19 +107,65 @@ def logits(hidden_bits, W_bits, rows=None, nthreads: int = 0) -> np.ndarray:
     return out
 
 
+def weight_f64(W_bits) -> np.ndarray:
+    """bf16 bits -> fp64 (exact), for reuse across logits_blas calls."""
+    Wb = _c(bf16_bits(W_bits), np.uint16)
+    return (Wb.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def logits_blas(hidden_bits, W_bits, rows=None, v_chunk: int = 16384, W64=None) -> np.ndarray:
+    """Step 1 with a library matmul (numpy/BLAS fp64) instead of the C loops:
+    the same definition l[r, x] = sum_k W[x,k] h[r,k] of the identical bf16
+    values, summed in the library's order (pinned against oracle.logits to
+    1e-12 relative, tests/test_oracle_pins.py).  Used only where the C loops
+    would take minutes (full-size batches of >= 1000 rows)."""
+    H = _c(bf16_bits(hidden_bits), np.uint16)
+    if rows is not None:
+        H = H[np.asarray(rows, np.int64)]
+    h = (H.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    if W64 is not None:
+        return h @ W64.T
+    Wb = _c(bf16_bits(W_bits), np.uint16)
+    V = Wb.shape[0]
+    out = np.empty((h.shape[0], V), np.float64)
+    for v0 in range(0, V, v_chunk):
+        w = (Wb[v0:v0 + v_chunk].astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        np.matmul(h, w.T, out=out[:, v0:v0 + w.shape[0]])
+    return out
+
+
 def verify(hidden_bits, W_bits, draft_tokens, draft_probs, gamma, uniforms,
-           tie_eps: float = TIE_EPS, nthreads: int = 0) -> dict:
+           tie_eps: float = TIE_EPS, nthreads: int = 0, gemm: str = "c") -> dict:
     """Full fp64 verification of a packed ragged batch (layout of include/nj.h).
 
-    ``uniforms`` may be fp32 (converted exactly) or fp64 (brute force).
-    Returns dict with accept_len, next_token and the fp64 debug arrays."""
+    ``uniforms`` may be fp32 (converted exactly) or fp64 (brute force, tie
+    branches).  ``gemm``: "c" (the plain loops of nj_oracle.c) or "blas"
+    (logits_blas).  Returns dict with accept_len, next_token and the fp64
+    debug arrays (see verify_from_logits)."""
     H = _c(bf16_bits(hidden_bits), np.uint16)
     Wb = _c(bf16_bits(W_bits), np.uint16)
     V, d = Wb.shape
     g = _c(gamma, np.int32)
-    B = g.shape[0]
-    N, G = int(g.sum()) + B, int(g.sum())
+    N = int(g.sum()) + g.shape[0]
     assert H.shape == (N, d), (H.shape, N, d)
+    L = logits_blas(H, Wb) if gemm == "blas" else logits(H, Wb, nthreads=nthreads)
+    return verify_from_logits(L, draft_tokens, draft_probs, gamma, uniforms, tie_eps=tie_eps, nthreads=nthreads)
+
+
+def verify_from_logits(L, draft_tokens, draft_probs, gamma, uniforms, tie_eps: float = TIE_EPS,
+                       nthreads: int = 0) -> dict:
+    """Steps 2-6 of the verification given the fp64 logits L [N, V] of the
+    packed rows (step 1).  Returns accept_len, next_token and the fp64 debug
+    arrays: lse [N], p_draft / ratio [G] (a_i = p_i(x_i)/q_i(x_i)), mass [B]
+    (W_b), F_lo / F_hi [B] (the drawn token's normalised CDF interval), flags,
+    accept_margin / draw_margin [B], p_tie [B] (probability over the
+    uniforms that the request is flagged a tie, R12) and tie."""
+    L = _c(L, np.float64)
+    N, V = L.shape
+    g = _c(gamma, np.int32)
+    B = g.shape[0]
+    G = int(g.sum())
+    assert N == G + B, (N, G, B)
     x = _c(draft_tokens, np.int32).reshape(-1)
     assert x.shape[0] == G
     q = np.asarray(draft_probs, dtype=np.float32)
@@ -132,16 +181,17 @@ def verify(hidden_bits, W_bits, draft_tokens, draft_probs, gamma, uniforms,
         "lse": np.empty(N), "p_draft": np.empty(max(G, 1)), "ratio": np.empty(max(G, 1)),
         "mass": np.empty(B), "F_lo": np.empty(B), "F_hi": np.empty(B),
         "flags": np.empty(B, np.int32), "accept_margin": np.empty(B), "draw_margin": np.empty(B),
+        "p_tie": np.empty(B),
     }
     xs = x if G else np.zeros(1, np.int32)
-    rc = _load().oracle_verify(
-        _ptr(H), _ptr(Wb), V, d, _ptr(xs), _ptr(q), ldq, _ptr(g), _ptr(u), B,
+    rc = _load().oracle_verify_logits(
+        _ptr(L), V, _ptr(xs), _ptr(q), ldq, _ptr(g), _ptr(u), B,
         _ptr(out["accept_len"]), _ptr(out["next_token"]), _ptr(out["lse"]),
         _ptr(out["p_draft"]), _ptr(out["ratio"]), _ptr(out["mass"]), _ptr(out["F_lo"]),
         _ptr(out["F_hi"]), _ptr(out["flags"]), _ptr(out["accept_margin"]),
-        _ptr(out["draw_margin"]), tie_eps, nthreads)
+        _ptr(out["draw_margin"]), _ptr(out["p_tie"]), tie_eps, nthreads)
     if rc:
-        raise MemoryError("oracle_verify failed")
+        raise MemoryError("oracle_verify_logits failed")
     out["p_draft"] = out["p_draft"][:G]
     out["ratio"] = out["ratio"][:G]
     out["tie"] = (out["flags"] & (F_ACCEPT_TIE | F_DRAW_TIE)) != 0

@@ -134,9 +134,10 @@ static void verify_one(const double* l, int64_t V, const double* lse,
                        double* p_draft, double* ratio,
                        double* mass_out, double* flo_out, double* fhi_out,
                        int32_t* flags_out, double* am_out, double* dm_out,
-                       double* w /* scratch [V] */) {
+                       double* ptie_out, double* w /* scratch [V] */) {
     int32_t flags = 0;
     double amargin = INFINITY;
+    double ptie = 0.0;   /* R12: probability over the uniforms of a tie flag */
     /* (3) acceptance: accept iff u_i * q_i(x_i) < p_i(x_i) (strict, R2);
      *     n = first failing i, else gamma.                               */
     int n = gamma;
@@ -150,6 +151,8 @@ static void verify_one(const double* l, int64_t V, const double* lse,
         double mg = fabs(a - u[i]);
         if (mg < amargin) amargin = mg;
         if (mg <= tie_eps) flags |= OF_ACCEPT_TIE;
+        /* P(|u_i - a_i| <= tie_eps) for u_i ~ U[0,1): |[a - eps, a + eps] n [0, 1)| */
+        ptie += fmax(0.0, fmin(a + tie_eps, 1.0) - fmax(a - tie_eps, 0.0));
         if (!(u[i] * qx < p)) { n = i; break; }
     }
     /* later drafts are never tested; their p/ratio are still reported */
@@ -196,6 +199,11 @@ static void verify_one(const double* l, int64_t V, const double* lse,
     double Flo = Cprev / W, Fhi = C / W;
     double dmargin = fmin(fabs(Fhi - u[gamma]), fabs(u[gamma] - Flo));
     if (dmargin <= tie_eps) flags |= OF_DRAW_TIE;
+    /* P(draw tie) for u_gamma ~ U[0,1): token x owns [F(x-1), F(x)) of width
+     * w(x)/W, and u is flagged iff it lies within tie_eps of either end of the
+     * interval it falls in, so the flagged measure is sum_x min(w(x)/W, 2 eps). */
+    for (int64_t v = 0; v < V; ++v)
+        if (w[v] > 0.0) ptie += fmin(w[v] / W, 2.0 * tie_eps);
     *n_out = n;
     *t_out = (int32_t)t;
     if (mass_out) *mass_out = W;
@@ -204,34 +212,33 @@ static void verify_one(const double* l, int64_t V, const double* lse,
     if (flags_out) *flags_out = flags;
     if (am_out) *am_out = amargin;
     if (dm_out) *dm_out = dmargin;
+    if (ptie_out) *ptie_out = ptie;
 }
 
-/* Full verification of a packed ragged batch (layout as include/nj.h, but
- * this file does not include it).  u is fp64 here (the fp32 uniforms
- * converted exactly by the caller; the brute-force checker passes cell
- * midpoints that are not fp32 values).  Debug pointers may be NULL.
- * Requests are processed independently (OpenMP over requests after an
- * OpenMP GEMM over all rows). */
-int oracle_verify(const uint16_t* H, const uint16_t* W, int64_t V, int64_t d,
-                  const int32_t* draft_tokens, const float* q, int64_t ldq,
-                  const int32_t* gamma, const double* u, int32_t B,
-                  int32_t* accept_len, int32_t* next_token,
-                  double* dbg_lse, double* dbg_p_draft, double* dbg_ratio,
-                  double* dbg_mass, double* dbg_flo, double* dbg_fhi,
-                  int32_t* dbg_flags, double* dbg_amargin, double* dbg_dmargin,
-                  double tie_eps, int nthreads) {
-    int64_t N = 0, G = 0;
-    for (int32_t b = 0; b < B; ++b) { N += gamma[b] + 1; G += gamma[b]; }
-    double* L = (double*)malloc(sizeof(double) * (size_t)(N * V));
+/* Steps (2)-(6) of a packed ragged batch (layout as include/nj.h, but this
+ * file does not include it) given the fp64 logits L[N][V] of its rows (step 1,
+ * oracle_logits).  u is fp64 here (the fp32 uniforms converted exactly by the
+ * caller; the brute-force checker and the tie-branch checks of the tests pass
+ * values that are not fp32).  Debug pointers may be NULL.  Requests are
+ * processed independently (OpenMP over requests). */
+int oracle_verify_logits(const double* L, int64_t V,
+                         const int32_t* draft_tokens, const float* q, int64_t ldq,
+                         const int32_t* gamma, const double* u, int32_t B,
+                         int32_t* accept_len, int32_t* next_token,
+                         double* dbg_lse, double* dbg_p_draft, double* dbg_ratio,
+                         double* dbg_mass, double* dbg_flo, double* dbg_fhi,
+                         int32_t* dbg_flags, double* dbg_amargin, double* dbg_dmargin,
+                         double* dbg_ptie, double tie_eps, int nthreads) {
+    int64_t N = 0;
+    for (int32_t b = 0; b < B; ++b) N += gamma[b] + 1;
     double* lse = (double*)malloc(sizeof(double) * (size_t)N);
-    if (!L || !lse) { free(L); free(lse); return 1; }
-    if (oracle_logits(H, NULL, N, W, V, d, L, nthreads)) { free(L); free(lse); return 1; }
+    int64_t* row_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(B + 1));
+    int64_t* drf_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(B + 1));
+    if (!lse || !row_off || !drf_off) { free(lse); free(row_off); free(drf_off); return 1; }
     set_threads(nthreads);
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t r = 0; r < N; ++r) lse[r] = row_lse(L + r * V, V);
     if (dbg_lse) memcpy(dbg_lse, lse, sizeof(double) * (size_t)N);
-    int64_t* row_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(B + 1));
-    int64_t* drf_off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(B + 1));
     row_off[0] = 0; drf_off[0] = 0;
     for (int32_t b = 0; b < B; ++b) {
         row_off[b + 1] = row_off[b] + gamma[b] + 1;
@@ -258,12 +265,34 @@ int oracle_verify(const uint16_t* H, const uint16_t* W, int64_t V, int64_t d,
                            dbg_fhi ? dbg_fhi + b : NULL,
                            dbg_flags ? dbg_flags + b : NULL,
                            dbg_amargin ? dbg_amargin + b : NULL,
-                           dbg_dmargin ? dbg_dmargin + b : NULL, w);
+                           dbg_dmargin ? dbg_dmargin + b : NULL,
+                           dbg_ptie ? dbg_ptie + b : NULL, w);
             }
             free(w);
         }
     }
-    free(row_off); free(drf_off); free(L); free(lse);
+    free(row_off); free(drf_off); free(lse);
+    return err;
+}
+
+/* Full verification: step (1) by oracle_logits, then oracle_verify_logits. */
+int oracle_verify(const uint16_t* H, const uint16_t* W, int64_t V, int64_t d,
+                  const int32_t* draft_tokens, const float* q, int64_t ldq,
+                  const int32_t* gamma, const double* u, int32_t B,
+                  int32_t* accept_len, int32_t* next_token,
+                  double* dbg_lse, double* dbg_p_draft, double* dbg_ratio,
+                  double* dbg_mass, double* dbg_flo, double* dbg_fhi,
+                  int32_t* dbg_flags, double* dbg_amargin, double* dbg_dmargin,
+                  double* dbg_ptie, double tie_eps, int nthreads) {
+    int64_t N = 0;
+    for (int32_t b = 0; b < B; ++b) N += gamma[b] + 1;
+    double* L = (double*)malloc(sizeof(double) * (size_t)(N * V));
+    if (!L) return 1;
+    if (oracle_logits(H, NULL, N, W, V, d, L, nthreads)) { free(L); return 1; }
+    int err = oracle_verify_logits(L, V, draft_tokens, q, ldq, gamma, u, B, accept_len, next_token,
+                                   dbg_lse, dbg_p_draft, dbg_ratio, dbg_mass, dbg_flo, dbg_fhi,
+                                   dbg_flags, dbg_amargin, dbg_dmargin, dbg_ptie, tie_eps, nthreads);
+    free(L);
     return err;
 }
 
@@ -307,12 +336,12 @@ int oracle_sample_from_logits(const float* logits, int64_t ld_l, int64_t V,
                     memcpy(l2, l, sizeof(double) * (size_t)V);
                     memcpy(l2 + V, l, sizeof(double) * (size_t)V);
                     verify_one(l2, V, lse2, 1, &x0, q + (int64_t)b * ldq, ldq, uu, tie_eps,
-                               &n, &t, NULL, NULL, &W, &Flo, &Fhi, &fl, &am, &dm, w);
+                               &n, &t, NULL, NULL, &W, &Flo, &Fhi, &fl, &am, &dm, NULL, w);
                     free(l2);
                 } else {
                     double uu[1] = {u[b]};
                     verify_one(l, V, &lse, 0, NULL, q, ldq, uu, tie_eps,
-                               &n, &t, NULL, NULL, &W, &Flo, &Fhi, &fl, &am, &dm, w);
+                               &n, &t, NULL, NULL, &W, &Flo, &Fhi, &fl, &am, &dm, NULL, w);
                 }
                 next_token[b] = t;
                 if (mass) mass[b] = W;

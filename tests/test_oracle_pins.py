@@ -315,3 +315,110 @@ def test_greedy_is_zero_temperature_limit():
     x = np.concatenate([L[ro[b]:ro[b] + g[b]].argmax(axis=1) for b in range(len(g))]).astype(np.int32)
     r2 = oracle.verify_greedy(n["hidden_bits"], n["W_bits"], x, g)
     assert (r2["accept_len"] == g).all()
+
+
+# ------------------------------------------------------------------ tie classifier (R12)
+def _one_row_case(V=64, d=16, seed=21):
+    b = make_batch(1, 0, V=V, d=d, seed=seed)
+    n = _np(b)
+    P, _ = _exact_p(n)
+    return n, P[0]
+
+
+def test_tie_classifier_draw_band():
+    """Draw tie iff |u - F(t)| or |u - F(t-1)| <= 1e-6, F = cumsum(p) / sum(p)
+    computed here with np.cumsum of the scipy softmax: u = F(k) -/+ 5e-7 is a
+    tie (tokens k / k+1), u = F(k) -/+ 2e-6 is not; F_lo / F_hi / draw_margin
+    are the interval ends and the distance to the nearer one."""
+    n, p = _one_row_case()
+    F = np.cumsum(p) / p.sum()
+    widths = np.diff(np.concatenate([[0.0], F]))
+    ks = [k for k in range(len(p) - 1) if widths[k] > 1e-5 and widths[k + 1] > 1e-5][:6]
+    assert len(ks) >= 3
+    for k in ks:
+        for delta, tie in [(-2e-6, False), (-5e-7, True), (5e-7, True), (2e-6, False)]:
+            u = np.array([F[k] + delta])
+            r = oracle.verify(n["hidden_bits"], n["W_bits"], np.zeros(0, np.int32), np.zeros((0, 64), np.float32),
+                              np.array([0], np.int32), u)
+            t = k if delta < 0 else k + 1
+            assert r["next_token"][0] == t
+            assert bool(r["flags"][0] & oracle.F_DRAW_TIE) == tie, (k, delta)
+            assert bool(r["tie"][0]) == tie
+            assert abs(r["F_lo"][0] - (F[t - 1] if t else 0.0)) < 1e-12 and abs(r["F_hi"][0] - F[t]) < 1e-12
+            assert abs(r["draw_margin"][0] - abs(delta)) < 1e-12
+
+
+def test_tie_classifier_accept_band():
+    """Acceptance tie iff |a_i - u_i| <= 1e-6 for a TESTED draft, a_i =
+    p_i(x_i) / q_i(x_i) from the scipy softmax: u = a -/+ 5e-7 ties, -/+ 2e-6
+    does not; accept iff u < a; a draft after the first rejection is never
+    tested and cannot tie."""
+    for seed in range(8, 200):   # first seed whose draft 0 has a0 < 1 (a rejectable draft)
+        b = make_batch(1, 2, V=64, d=16, seed=seed)
+        n = _np(b)
+        P, _ = _exact_p(n)
+        x = n["draft_tokens"]
+        q = n["draft_probs"].astype(np.float64)
+        a = [P[i, x[i]] / q[i, x[i]] for i in range(2)]
+        a0 = a[0]
+        if 4e-6 < a0 < 0.6:
+            break
+    assert 4e-6 < a0 < 0.6, a
+    for delta, tie in [(-2e-6, False), (-5e-7, True), (5e-7, True), (2e-6, False)]:
+        u = np.array([a0 + delta, 0.0, 0.5])
+        r = _verify({**n, "uniforms": u})
+        assert bool(r["flags"][0] & oracle.F_ACCEPT_TIE) == tie, delta
+        assert (r["accept_len"][0] >= 1) == (delta < 0)
+        assert abs(r["ratio"][0] - a0) < 1e-12 * max(1.0, a0)
+        margin = min(abs(delta), a[1]) if delta < 0 else abs(delta)   # test 1 (u_1 = 0) only after an accept
+        assert abs(r["accept_margin"][0] - margin) < 1e-12
+    # draft 1 is not tested when draft 0 is rejected: a tie at u_1 = a_1 is ignored
+    u = np.array([min(a0 + 0.3, 0.999), a[1] + 1e-7, 0.5])
+    r = _verify({**n, "uniforms": u})
+    assert r["accept_len"][0] == 0 and not r["flags"][0] & oracle.F_ACCEPT_TIE
+
+
+def test_p_tie_closed_form_uniform_p():
+    """p uniform over V tokens (h = 0: every logit 0): the flagged measure of
+    the final uniform is V * min(1/V, 2 eps) exactly."""
+    V, d = 8, 16
+    H = np.zeros((1, d), np.uint16)
+    W = make_batch(1, 0, V=V, d=d, seed=1).to_numpy()["W_bits"]
+    for eps, expect in [(1e-6, 8 * 2e-6), (1e-3, 8 * 2e-3), (0.1, 1.0)]:
+        r = oracle.verify(H, W, np.zeros(0, np.int32), np.zeros((0, V), np.float32), np.array([0], np.int32),
+                          np.array([0.3]), tie_eps=eps)
+        assert abs(r["p_tie"][0] - expect) < 1e-12
+
+
+@pytest.mark.parametrize("gamma", [0, 1])
+def test_p_tie_monte_carlo(gamma):
+    """p_tie (the probability over the uniforms that a request is flagged) is
+    checked against the observed tie frequency of 20000 independent uniform
+    draws of the same request (band widened to 1e-3 so ties are common);
+    |freq - mean p_tie| <= 4 sigma."""
+    V, d, R = 48, 16, 20000
+    b = make_batch(1, gamma, V=V, d=d, seed=17)
+    n = _np(b)
+    H = np.tile(n["hidden_bits"], (R, 1))
+    rng = np.random.default_rng(5)
+    u = rng.random(R * (gamma + 1))
+    x = np.tile(n["draft_tokens"], R)
+    q = np.tile(n["draft_probs"], (R, 1)) if gamma else n["draft_probs"]
+    r = oracle.verify(H, n["W_bits"], x, q, np.full(R, gamma, np.int32), u, tie_eps=1e-3)
+    freq = r["tie"].mean()
+    mean = r["p_tie"].mean()
+    sd = np.sqrt(mean * (1 - mean) / R)
+    assert 0.02 < mean < 0.5
+    assert abs(freq - mean) <= 4 * sd + 1e-3 * gamma, (freq, mean, sd)
+
+
+def test_logits_blas_matches_c_loops():
+    """oracle.logits_blas (library fp64 matmul, used for full-size batches) is
+    the same step-1 definition as the C loops: equal to 1e-12 relative."""
+    b = make_batch(5, 1, V=3000, d=256, seed=2)
+    n = _np(b)
+    a = oracle.logits(n["hidden_bits"], n["W_bits"])
+    c = oracle.logits_blas(n["hidden_bits"], n["W_bits"], v_chunk=777)
+    assert np.max(np.abs(a - c)) <= 1e-12 * np.max(np.abs(a))
+    d = oracle.logits_blas(n["hidden_bits"], n["W_bits"], W64=oracle.weight_f64(n["W_bits"]))
+    assert np.max(np.abs(a - d)) <= 1e-12 * np.max(np.abs(a))
