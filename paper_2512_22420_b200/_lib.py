@@ -27,12 +27,12 @@ NJ_FLAG_FALLBACK, NJ_FLAG_ZERO_MASS, NJ_FLAG_CLAMP = 1, 2, 4
 # every symbol include/nj.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "nj_create", "nj_destroy", "nj_last_error", "nj_verify", "nj_verify_host", "nj_set_option", "nj_plan",
-    "nj_kernel_time", "nj_stream_test",
-    "nj_lmhead_logits", "nj_lmhead_logits_ks", "nj_sample_from_logits", "nj_bandit_create", "nj_bandit_destroy", "nj_select_gamma",
+    "nj_kernel_time",
+    "nj_lmhead_logits", "nj_sample_from_logits", "nj_bandit_create", "nj_bandit_destroy", "nj_select_gamma",
     "nj_observe", "nj_exploitation_score", "nj_prefill_cost_ms", "nj_bandit_state", "nj_bandit_arm",
     "nj_bandit_last_gamma", "nj_bandit_snapshot_json",
     "nj_shard_range", "nj_nccl_get_unique_id", "nj_nccl_comm_init", "nj_nccl_comm_destroy", "nj_group_create",
-    "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify", "nj_mma_probe",
+    "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify",
     "nj_propose", "nj_verify_greedy",
 ]
 NJ_NCCL_ID_BYTES = 128
@@ -42,6 +42,14 @@ class NJError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"libnj status {status}: {msg}")
         self.status = status
+
+
+class NJArgError(NJError, ValueError):
+    """Argument rejected by the binding's checks before any pointer crosses the
+    C ABI (the same status codes the library uses: NJ_EINVAL / NJ_ESHAPE)."""
+
+    def __init__(self, status, msg):
+        super().__init__(status, msg)
 
 
 class nj_config(ctypes.Structure):
@@ -77,9 +85,7 @@ def load():
         "nj_set_option": ([P, I32, I64], I32),
         "nj_plan": ([P, P, I32, P, P], I32),
         "nj_kernel_time": ([P, P, P, I32], I32),
-        "nj_stream_test": ([P, P, P, I32, I32, I32, P, I32], I32),
-        "nj_lmhead_logits": ([P, P, P, P, P, I32, P, I64], I32),
-        "nj_lmhead_logits_ks": ([P, P, P, P, P, I32, P, I64, I32], I32),
+        "nj_lmhead_logits": ([P, P, P, P, P, I32, P, I64, I32], I32),
         "nj_sample_from_logits": ([P, P, P, I64, P, P, I64, P, I32, P, P], I32),
         "nj_propose": ([P, P, P, P, P, I32, P, P, I64], I32),
         "nj_verify_greedy": ([P, P, P, P, P, P, I32, P, P], I32),
@@ -102,7 +108,6 @@ def load():
         "nj_group_member": ([P, I32], P),
         "nj_group_last_error": ([P], ctypes.c_char_p),
         "nj_group_verify": ([P, P, P, P, P, P, I64, P, P, I32, P, P, P], I32),
-        "nj_mma_probe": ([P, P, I32, I32, I32, P], I32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -119,6 +124,56 @@ def _ptr(t):
     if isinstance(t, np.ndarray):
         return t.ctypes.data
     return t.data_ptr()
+
+
+def _dev(t, name: str, dtype: str, rowmajor: bool = False, host: bool = False, min_rows: int = 0,
+         min_numel: int = 0, ncols: int | None = None, min_cols: int | None = None):
+    """Argument check before a raw pointer crosses the C ABI: a torch tensor on
+    the right kind of device with the dtype the ABI expects, and a layout the
+    kernels can index (contiguous; or, with rowmajor, 2-D with unit column
+    stride and any row pitch).  Raises NJArgError (an NJError and a ValueError)
+    instead of letting the library misread memory."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise NJArgError(NJ_EINVAL, f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if t.dtype != getattr(torch, dtype):
+        raise NJArgError(NJ_EINVAL, f"{name}: dtype {t.dtype}, expected torch.{dtype}")
+    if host and t.is_cuda:
+        raise NJArgError(NJ_EINVAL, f"{name}: expected a host (CPU) tensor")
+    if not host and not t.is_cuda:
+        raise NJArgError(NJ_EINVAL, f"{name}: expected a CUDA tensor")
+    if rowmajor:
+        if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1) or t.stride(0) < t.shape[1]:
+            raise NJArgError(NJ_ESHAPE, f"{name}: expected a 2-D row-major tensor (unit column stride), "
+                             f"shape {tuple(t.shape)} strides {t.stride()}")
+    elif not t.is_contiguous():
+        raise NJArgError(NJ_ESHAPE, f"{name}: expected a contiguous tensor, strides {t.stride()}")
+    if min_rows and (t.dim() < 1 or t.shape[0] < min_rows):
+        raise NJArgError(NJ_ESHAPE, f"{name}: needs >= {min_rows} rows, shape {tuple(t.shape)}")
+    if min_numel and t.numel() < min_numel:
+        raise NJArgError(NJ_ESHAPE, f"{name}: needs >= {min_numel} elements, has {t.numel()}")
+    if ncols is not None and (t.dim() != 2 or t.shape[1] != ncols):
+        raise NJArgError(NJ_ESHAPE, f"{name}: expected {ncols} columns, shape {tuple(t.shape)}")
+    if min_cols is not None and (t.dim() != 2 or t.shape[1] < min_cols):
+        raise NJArgError(NJ_ESHAPE, f"{name}: expected >= {min_cols} columns, shape {tuple(t.shape)}")
+    return t
+
+
+def _check_batch(cfg, hidden, W, draft_tokens, draft_probs, g, uniforms, accept_len, next_token, host=False,
+                 ldq=None):
+    """Shape / dtype / layout checks of one nj_verify-style call (include/nj.h)."""
+    B, G = int(g.shape[0]), int(g.sum())
+    N = G + B
+    _dev(hidden, "hidden", "bfloat16", host=host, min_rows=N, ncols=cfg.d)
+    if W is not None:
+        _dev(W, "W_lm", "bfloat16", ncols=cfg.d, min_rows=cfg.v_end - cfg.v_begin)
+    _dev(uniforms, "uniforms", "float32", host=host, min_numel=N)
+    _dev(accept_len, "accept_len", "int32", host=host, min_numel=B)
+    _dev(next_token, "next_token", "int32", host=host, min_numel=B)
+    if G > 0:
+        _dev(draft_tokens, "draft_tokens", "int32", host=host, min_numel=G)
+        _dev(draft_probs, "draft_probs", "float32", rowmajor=ldq is None, host=host, min_rows=G,
+             min_cols=cfg.V if ldq is None else None)
 
 
 def _stream(stream):
@@ -175,8 +230,14 @@ class Verifier:
                debug: dict | None = None, stream=None):
         """nj_verify on device tensors; outputs written into accept_len / next_token."""
         g = np.ascontiguousarray(gamma, np.int32)
+        _check_batch(self.cfg, hidden, W, draft_tokens, draft_probs, g, uniforms, accept_len, next_token)
         dbg = None
         if debug is not None:
+            B, N, G = int(g.shape[0]), int(g.sum()) + int(g.shape[0]), int(g.sum())
+            for k, dt, n in (("lse", "float32", N), ("p_draft", "float32", G), ("mass", "float64", B),
+                             ("flags", "int32", B)):
+                if debug.get(k) is not None:
+                    _dev(debug[k], "debug." + k, dt, min_numel=n)
             dbg = nj_debug(_ptr(debug.get("lse")), _ptr(debug.get("p_draft")), _ptr(debug.get("mass")),
                            _ptr(debug.get("flags")))
         self._check(self._lib.nj_verify(
@@ -187,22 +248,31 @@ class Verifier:
     def verify_host(self, hidden_h, W, tok_h, q_h, gamma, u_h, acc_h, next_h, ldq=None, stream=None):
         """nj_verify_host: host (pinned) inputs/outputs, resident W; synchronous."""
         g = np.ascontiguousarray(gamma, np.int32)
+        _check_batch(self.cfg, hidden_h, W, tok_h, q_h, g, u_h, acc_h, next_h, host=True, ldq=ldq)
         ldq = int(q_h.stride(0)) if ldq is None else ldq
         self._check(self._lib.nj_verify_host(
             self._h, _stream(stream), _ptr(hidden_h), _ptr(W), _ptr(tok_h), _ptr(q_h), ldq, _ptr(g),
             _ptr(u_h), g.shape[0], _ptr(acc_h), _ptr(next_h)))
 
-    def lmhead_logits(self, hidden, W, rows, out, stream=None):
+    def lmhead_logits(self, hidden, W, rows, out, ks: int = 0, stream=None):
+        """nj_lmhead_logits: fp32 logits of hidden[rows] through the production GEMM."""
+        _dev(hidden, "hidden", "bfloat16")
+        _dev(W, "W", "bfloat16")
+        _dev(rows, "rows", "int32")
+        _dev(out, "out", "float32", rowmajor=True)
         self._check(self._lib.nj_lmhead_logits(self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(rows),
-                                               int(rows.shape[0]), _ptr(out), int(out.stride(0))))
-
-    def lmhead_logits_ks(self, hidden, W, rows, out64, ks: int, stream=None):
-        self._check(self._lib.nj_lmhead_logits_ks(self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(rows),
-                                                  int(rows.shape[0]), _ptr(out64), int(out64.stride(0)), int(ks)))
+                                               int(rows.shape[0]), _ptr(out), int(out.stride(0)), int(ks)))
 
     def verify_greedy(self, hidden, W, draft_tokens, gamma, accept_len, next_token, stream=None):
         """nj_verify_greedy: verification against the argmax target (include/nj.h)."""
         g = np.ascontiguousarray(np.asarray(gamma, dtype=np.int32))
+        B, G = int(g.shape[0]), int(g.sum())
+        _dev(hidden, "hidden", "bfloat16", min_rows=G + B, ncols=self.cfg.d)
+        _dev(W, "W_lm", "bfloat16", ncols=self.cfg.d)
+        _dev(accept_len, "accept_len", "int32", min_numel=B)
+        _dev(next_token, "next_token", "int32", min_numel=B)
+        if G:
+            _dev(draft_tokens, "draft_tokens", "int32", min_numel=G)
         self._check(self._lib.nj_verify_greedy(
             self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(draft_tokens), g.ctypes.data, g.shape[0],
             _ptr(accept_len), _ptr(next_token)))
@@ -210,11 +280,25 @@ class Verifier:
     def propose(self, hidden, W, u, tokens, q_out, stream=None):
         """nj_propose: draft LM head + softmax + inverse-CDF draw (include/nj.h):
         tokens[b] ~ q_out[b] = softmax(W @ hidden[b]) with uniform u[b]."""
+        B = int(hidden.shape[0])
+        _dev(hidden, "hidden", "bfloat16", ncols=self.cfg.d)
+        _dev(W, "W_lm", "bfloat16", ncols=self.cfg.d)
+        _dev(u, "u", "float32", min_numel=B)
+        _dev(tokens, "tokens", "int32", min_numel=B)
+        _dev(q_out, "q_out", "float32", rowmajor=True, min_rows=B, min_cols=self.cfg.V)
         self._check(self._lib.nj_propose(
             self._h, _stream(stream), _ptr(hidden), _ptr(W), _ptr(u), int(hidden.shape[0]), _ptr(tokens),
             _ptr(q_out), int(q_out.stride(0))))
 
     def sample_from_logits(self, logits, residual, q, u, next_token, mass=None, stream=None):
+        B = int(logits.shape[0])
+        _dev(logits, "logits", "float32", rowmajor=True, min_cols=self.cfg.V)
+        _dev(residual, "residual", "int32", min_numel=B)
+        _dev(q, "q", "float32", rowmajor=True, min_rows=B, min_cols=self.cfg.V)
+        _dev(u, "u", "float32", min_numel=B)
+        _dev(next_token, "next_token", "int32", min_numel=B)
+        if mass is not None:
+            _dev(mass, "mass", "float64", min_numel=B)
         self._check(self._lib.nj_sample_from_logits(
             self._h, _stream(stream), _ptr(logits), int(logits.stride(0)), _ptr(residual), _ptr(q),
             int(q.stride(0)), _ptr(u), int(logits.shape[0]), _ptr(next_token), _ptr(mass)))
@@ -296,6 +380,10 @@ class ShardGroup:
     def verify(self, hidden, W_shards, draft_tokens, draft_probs, gamma, uniforms, accept_len, next_token,
                debug: dict | None = None, stream=None):
         g = np.ascontiguousarray(gamma, np.int32)
+        _check_batch(self.cfg, hidden, None, draft_tokens, draft_probs, g, uniforms, accept_len, next_token)
+        for r, w in enumerate(W_shards):
+            vb, ve = self.ranges[r]
+            _dev(w, f"W_shards[{r}]", "bfloat16", ncols=self.cfg.d, min_rows=ve - vb)
         ptrs = (ctypes.c_void_p * self.n)(*[_ptr(w) for w in W_shards])
         dbg = None
         if debug is not None:

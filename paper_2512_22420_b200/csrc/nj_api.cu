@@ -21,10 +21,7 @@
 #include "nj.h"
 #include "nj_gemm.cuh"
 #include "nj_sampler.cuh"
-#include "nj_probe_ks.cuh"
-#include "nj_stream_test.cuh"
 #include "nj_shard.cuh"
-#include "nj_mma_probe.cuh"
 
 #include <dlfcn.h>
 
@@ -69,15 +66,7 @@ constexpr int kStagedMaxN = kBigMaxRowG;   // staged path: rows of one GEMM pass
 inline int round16(int x) { return (x + 15) & ~15; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// device smem carve-up mirrors (must match nj_gemm.cuh / nj_fused.cuh)
-size_t gemm_rows_tail(int R, bool stats, bool capture, int S) {
-    size_t t = 4 * 256 * sizeof(float2);
-    if (stats) t += (size_t)R * sizeof(float2);
-    if (capture) t += (size_t)R * sizeof(int32_t);
-    t = align_up(t, 8);
-    t += (size_t)(2 * S + 4) * 8 + 8;
-    return t;
-}
+// device smem carve-up mirror (must match nj_fused.cuh)
 size_t fused_tail(int NPAD, int S) {
     const int kMaxT = 16;
     size_t t = 0;
@@ -93,22 +82,47 @@ size_t fused_tail(int NPAD, int S) {
     return t;
 }
 
-struct Dev {
-    void* p = nullptr;
-    size_t bytes = 0;
+// Tuning / probe knobs (DESIGN.md §8 "knobs"): read from the environment ONCE
+// at nj_create (never per launch); -1 = unset (the measured defaults apply).
+struct Knobs {
+    int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
+    int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
+    int w_evict_first = -1, mass_probe = 0;
 };
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+Knobs read_knobs() {
+    Knobs k;
+    k.fgroups = env_int("NJ_FGROUPS", -1);
+    k.kpd = env_int("NJ_KPD", -1);
+    k.sacc = env_int("NJ_SACC", -1);
+    k.kgroup = env_int("NJ_KGROUP", -1);
+    k.phase_ts = env_int("NJ_PHASE_TS", 0) == 1;
+    k.big_gk = env_int("NJ_BIG_GK", -1);
+    k.big_nbuf = env_int("NJ_BIG_NBUF", -1);
+    k.big_dbg = env_int("NJ_BIG_DBG", 0);
+    k.spin = env_int("NJ_SPIN", 0);
+    k.stats = env_int("NJ_STATS", 1);
+    k.sleep_ns = env_int("NJ_SLEEP", 0);
+    k.big_s = env_int("NJ_BIG_S", -1);
+    k.w_evict_first = env_int("NJ_W_EVICT_FIRST", -1);
+    k.mass_probe = env_int("NJ_MASS_PROBE", 0);
+    return k;
+}
 
 }  // namespace
 
 struct nj_ctx {
     nj_config cfg{};
+    Knobs kn;
     int V_local = 0;
     int num_sms = 0;
     int grid = 0;       // persistent grid (CTAs)
     int pld = 0;        // row stride of the per-CTA softmax partials (>= every GEMM grid)
     int gemm_ks = 4;    // k_gemm_big: k-blocks per accumulator restart
     int gemm_ks_ka = 8; // two-pass K-A (acceptance statistics only, certified): restart period
-    int gemm_acc = 0;   // 1: use the per-k-block-restart k_gemm_acc instead (A/B, NJ_GEMM=acc)
     int gemm_cg = 0;    // k_gemm_big CTA group: 0 auto, 1 single CTA, 2 CTA pair (NJ_CG)
     int gemm_pf = 0;    // k_gemm_big: W k-blocks prefetched into L2 ahead of the ring (NJ_PF)
     int gemm_maxt = 256;  // k_gemm_big: max token chunk (NJ_BIG_MAXT)
@@ -328,21 +342,21 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
         // as many one-partial groups as the spare TMEM holds: the MMAs run that
         // many stages ahead of the epilogue's per-tile work
         fp.ngroups = std::max(2, std::min(8, spare / NPAD));
-        if (const char* e = getenv("NJ_FGROUPS")) fp.ngroups = std::max(2, std::min(fp.ngroups, atoi(e)));
+        if (c->kn.fgroups > 0) fp.ngroups = std::max(2, std::min(fp.ngroups, c->kn.fgroups));
         fp.nbuf = fp.ngroups;
     } else {
         fp.ngroups = 0;
         fp.nbuf = std::max(1, std::min(8, spare / NPAD));
         fp.kpd = 4;
     }
-    if (const char* e = getenv("NJ_KPD")) fp.kpd = std::max(1, atoi(e));   // tuning knobs
-    if (const char* e = getenv("NJ_SACC")) fp.sacc = atoi(e);
+    if (c->kn.kpd > 0) fp.kpd = c->kn.kpd;   // tuning knobs
+    if (c->kn.sacc >= 0) fp.sacc = c->kn.sacc;
     if (!fp.sacc && fp.ngroups > 0) {   // one partial per k-block: GK partial slots per group
         GK = std::max(1, std::min(4, spare / (2 * NPAD)));
         fp.ngroups = 2;
         fp.nbuf = 2 * GK;
     }
-    if (const char* e = getenv("NJ_KGROUP")) GK = std::max(1, atoi(e));
+    if (c->kn.kgroup > 0) GK = c->kn.kgroup;
     const size_t stage2 = (size_t)GK * (kTileBytesA + NPAD * 128);
     const int S = (int)std::min<size_t>(8, (kSmemLimit - fused_tail(NPAD, 8) - 1024) / stage2);
     fp.nstages = S;
@@ -351,8 +365,8 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     // every 2 -> 4e-6; every 3-4 k-blocks (<= 16 MMAs) -> the k_gemm_big margin
     const int kspan = (fp.ngroups > 0 && fp.sacc) ? GK : fp.kpd;
     fp.eps_acc = kspan == 1 ? c->eps_acc_fused : kspan == 2 ? 2.0f * c->eps_acc_fused : c->eps_acc;
-    if (const char* e = getenv("NJ_PHASE_TS")) {
-        if (*e == '1' && !c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
+    if (c->kn.phase_ts) {
+        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
         fp.phase_ts = c->phase_ts;
     }
     const size_t smem = (size_t)S * stage2 + fused_tail(NPAD, S);
@@ -389,60 +403,8 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     return NJ_OK;
 }
 
-// k_gemm_rows launcher (rows contiguous in `h`, R rows)
-template <bool WRITE, bool STATS, bool CAPTURE>
-nj_status launch_gemm_rows(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, GemmRowsParams gp) {
-    if (R <= 0) return NJ_OK;
-    const int box = std::min(256, round16(R));
-    CUtensorMap tmH;
-    if (!encode_2d(&tmH, h, R, c->cfg.d, box)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
-    gp.R = R;
-    gp.box_rows = box;
-    gp.nchunks = (R + box - 1) / box;
-    gp.V_local = c->V_local;
-    gp.U = c->U;
-    gp.num_kb = (c->cfg.d + kBK - 1) / kBK;
-    gp.v_begin = c->cfg.v_begin;
-    gp.part_ld = c->grid;
-    const size_t stage = kTileBytesA + (size_t)box * 128;
-    int S = (int)std::min<size_t>(8, (kSmemLimit - gemm_rows_tail(R, STATS, CAPTURE, 8) - 1024) / stage);
-    if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_rows: not enough shared memory (R=%d)", R);
-    gp.nstages = S;
-    const size_t smem = (size_t)S * stage + gemm_rows_tail(R, STATS, CAPTURE, S);
-    k_gemm_rows<WRITE, STATS, CAPTURE><<<c->grid, kThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
-    NJ_LAUNCHED(c, "k_gemm_rows", st);
-    return NJ_OK;
-}
-
-// k_gemm_acc launcher (two-pass path): accurate LM-head GEMM over R contiguous rows
-template <bool WRITE, bool STATS, bool CAPTURE>
-nj_status launch_gemm_acc(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, GemmAccParams gp) {
-    if (R <= 0) return NJ_OK;
-    CUtensorMap tmH;
-    if (!encode_2d(&tmH, h, R, c->cfg.d, kAccT)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
-    gp.R = R;
-    gp.nchunks = (R + kAccT - 1) / kAccT;
-    gp.V_local = c->V_local;
-    gp.U = c->U;
-    gp.num_kb = (c->cfg.d + kBK - 1) / kBK;
-    gp.v_begin = c->cfg.v_begin;
-    gp.part_ld = c->pld;
-    const size_t stage = (size_t)kAccGK * (kTileBytesA + kAccT * 128);
-    size_t tail = 2 * 4 * kAccNC * sizeof(float2) + (STATS ? (size_t)R * 8 : 0) + (CAPTURE ? (size_t)R * 4 : 0);
-    tail = align_up(tail, 8) + (2 * 8 + 4) * 8 + 8;
-    const int S = (int)std::min<size_t>(4, (kSmemLimit - tail - 1024) / stage);
-    if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_acc: not enough shared memory (R=%d)", R);
-    gp.nstages = S;
-    const size_t smem = (size_t)S * stage + tail;
-    k_gemm_acc<WRITE, STATS, CAPTURE><<<c->grid, kAccThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, gp);
-    NJ_LAUNCHED(c, "k_gemm_acc", st);
-    return NJ_OK;
-}
-
-
-// LM-head GEMM of the staged / two-pass paths over R contiguous rows of h.
-// k_gemm_big (default) or, with NJ_GEMM=acc, the per-k-block-restart
-// k_gemm_acc (A/B only).  rr: deal (tile, chunk) items round-robin over
+// LM-head GEMM of the staged / two-pass paths over R contiguous rows of h
+// (k_gemm_big).  rr: deal (tile, chunk) items round-robin over
 // grid_rr = min(SMs, tiles) CTAs; otherwise the tile-balanced vocab split
 // over c->grid (CG = 1).  CTA pairs (CG = 2) always deal (tile pair, chunk)
 // items round-robin.  grid_force > 0: use that grid (several launches that
@@ -451,17 +413,6 @@ template <bool WRITE, bool STATS, bool CAPTURE>
 nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, const GemmBigParams& in, bool rr,
                         int* grid_used, int grid_force = 0) {
     if (R <= 0) return NJ_OK;
-    if (c->gemm_acc) {
-        if (rr) return set_err(c, NJ_EUNSUPPORTED, "NJ_GEMM=acc: no round-robin mode");
-        if (in.use_row_g && R > kAccMaxRowG) return set_err(c, NJ_EUNSUPPORTED, "NJ_GEMM=acc: staged rows <= %d", kAccMaxRowG);
-        GemmAccParams gp{};
-        gp.logits = in.logits; gp.ld_out = in.ld_out; gp.part_m = in.part_m; gp.part_s = in.part_s;
-        gp.tok = in.tok; gp.dl = in.dl; gp.w_evict_first = in.w_evict_first; gp.use_row_g = in.use_row_g;
-        for (int i = 0; i < kAccMaxRowG && i < kBigMaxRowG; ++i) gp.row_g[i] = in.row_g[i];
-        nj_status s = launch_gemm_acc<WRITE, STATS, CAPTURE>(c, st, h, R, gp);
-        if (grid_used) *grid_used = c->grid;
-        return s;
-    }
     GemmBigParams gp = in;
     gp.R = R;
     const int CG = c->gemm_cg == 2 ? 2 : 1;
@@ -499,26 +450,22 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     // ~600 cycles per stage, so a stage must carry more MMA work than
     // that -- 4 / 3 / 2 k-blocks for chunks of <= 64 / <= 128 / more columns (~96 KB stages)
     gp.gk = gp.chunk <= 64 ? 4 : gp.chunk <= 128 ? 3 : 2;
-    if (const char* e = getenv("NJ_BIG_GK")) gp.gk = std::max(1, atoi(e));
+    if (c->kn.big_gk > 0) gp.gk = c->kn.big_gk;
     gp.ks = in.ks > 0 ? in.ks : c->gemm_ks;   // accumulator groups are counted per k-block, not per stage
     // as many accumulator buffers as TMEM holds: small chunks let the MMAs run
     // further ahead of the epilogue's per-item output
     gp.bstride = std::max(32, (gp.chunk + 31) & ~31);
     gp.nbuf = std::max(2, std::min(kBigMaxBuf, 512 / gp.bstride));
     if (gp.teams == 2) gp.nbuf &= ~1;   // an even split between the teams
-    if (const char* e = getenv("NJ_BIG_NBUF")) gp.nbuf = std::max(2, std::min(gp.nbuf, atoi(e)));
+    if (c->kn.big_nbuf > 0) gp.nbuf = std::max(2, std::min(gp.nbuf, c->kn.big_nbuf));
     gp.pf = c->gemm_pf;
-    gp.dbg = 0;
-    if (const char* e = getenv("NJ_BIG_DBG")) gp.dbg = atoi(e);
-    gp.spin = 0;
-    if (const char* e = getenv("NJ_SPIN")) gp.spin = atoi(e);
-    gp.stats_mode = 1;
-    if (const char* e = getenv("NJ_STATS")) gp.stats_mode = atoi(e);
-    gp.sleep_ns = 0;
-    if (const char* e = getenv("NJ_SLEEP")) gp.sleep_ns = atoi(e);
+    gp.dbg = c->kn.big_dbg;
+    gp.spin = c->kn.spin;
+    gp.stats_mode = c->kn.stats;
+    gp.sleep_ns = c->kn.sleep_ns;
     gp.ts = nullptr;
-    if (const char* e = getenv("NJ_PHASE_TS")) {
-        if (*e == '1' && !c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
+    if (c->kn.phase_ts) {
+        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
         gp.ts = c->phase_ts;
     }
     CUtensorMap tmH;
@@ -529,7 +476,7 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
                   (CAPTURE ? (size_t)R * 4 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 2 * kBigMaxBuf) * 8 + 8;
     int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
-    if (const char* e = getenv("NJ_BIG_S")) S = (gp.dbg & 4) ? std::min(64, atoi(e)) : std::min(S, std::max(2, atoi(e)));
+    if (c->kn.big_s > 0) S = (gp.dbg & 4) ? std::min(64, c->kn.big_s) : std::min(S, std::max(2, c->kn.big_s));
     if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_gemm_big: not enough shared memory (R=%d)", R);
     gp.nstages = S;
     const size_t smem = ((gp.dbg & 4) ? 0 : (size_t)S * stage) + tail + ((gp.dbg & 4) ? (size_t)S * 16 : 0);
@@ -565,7 +512,7 @@ nj_status launch_mass(nj_ctx* c, cudaStream_t st, const MassParams& mp, int B, b
     }
     const int total = B * c->nchunks;
     const int grid = std::max(1, std::min(total, c->num_sms * c->mass_occ));
-    if (const char* e = getenv("NJ_MASS_PROBE")) const_cast<MassParams&>(mp).probe = atoi(e);
+    const_cast<MassParams&>(mp).probe = c->kn.mass_probe;
     const size_t sm = mass_smem(c->mass_nst, B);
     if (c->mass_nst == 2) k_mass<2><<<grid, kSampThreads, sm, st>>>(mp, B);
     else if (c->mass_nst == 4) k_mass<4><<<grid, kSampThreads, sm, st>>>(mp, B);
@@ -751,7 +698,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
             NJ_CUDA(c, cudaMemsetAsync(c->dl, 0xFF, (size_t)pl.G * sizeof(double), st));   // NaN: not owned
             k_gather_drafts<<<pl.G, 128, 0, st>>>(a.hidden, c->cfg.d, a.meta, c->hd);
             NJ_LAUNCHED(c, "k_gather_drafts", st);
-            const bool rrA = pl.G > kBigMaxT && !c->gemm_acc;
+            const bool rrA = pl.G > kBigMaxT;
             for (int r0 = 0; r0 < pl.G; r0 += kMaxStatRows) {
                 const int R = std::min(kMaxStatRows, pl.G - r0);
                 GemmBigParams gp{};
@@ -788,7 +735,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
             GemmBigParams gp{};
             gp.logits = c->logits_s; gp.ld_out = c->V_local;
             gp.part_m = c->part2_m; gp.part_s = c->part2_s;
-            const bool rrC = pl.B > kBigMaxT && !c->gemm_acc;
+            const bool rrC = pl.B > kBigMaxT;
             if ((s = launch_lmhead<true, true, false>(c, st, c->hs, pl.B, gp, rrC, &a.gridC)) != NJ_OK) return s;
         }
         MassParams& mp = a.mp;
@@ -855,7 +802,9 @@ nj_status shard_call(nj_ctx* c, ShardCall& a, const uint16_t* hidden, const uint
     if ((s = ensure_w_maps(c, W)) != NJ_OK) return s;
     a.meta = make_meta(a.pl);
     a.hidden = hidden; a.W = W; a.tok = tok; a.q = q; a.ldq = ldq; a.u = u; a.acc = acc; a.nxt = nxt; a.dbg = dbg;
-    a.certify = c->certify || c->force_fb;
+    // the sharded driver always runs its fallback phases: they also carry the
+    // zero-residual-mass draws (R6), which no single rank can redo alone
+    a.certify = 1;
     return NJ_OK;
 }
 
@@ -929,6 +878,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
 
     nj_ctx* c = new nj_ctx();
     c->cfg = *cfg;
+    c->kn = read_knobs();
     c->nranks = nranks;
     c->rank = rank;
     c->ncomm = cfg->nccl_comm;
@@ -952,7 +902,6 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     c->Gmax = std::max(1, MB * GM);
     nj_status s = NJ_OK;
     c->pld = std::max(c->grid, c->num_sms);
-    if (const char* e = getenv("NJ_GEMM")) c->gemm_acc = strcmp(e, "acc") == 0;
     if (const char* e = getenv("NJ_KS")) c->gemm_ks = std::max(1, atoi(e));
     if (const char* e = getenv("NJ_KS_KA")) c->gemm_ks_ka = std::max(1, atoi(e));
     if (const char* e = getenv("NJ_CG")) c->gemm_cg = atoi(e);
@@ -995,12 +944,6 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_fused_verify<16>);
     e = e ? e : set_smem_attr(k_fused_verify<32>);
     e = e ? e : set_smem_attr(k_fused_verify<48>);
-    e = e ? e : set_smem_attr(k_gemm_rows<true, false, false>);
-    e = e ? e : set_smem_attr(k_gemm_rows<false, true, true>);
-    e = e ? e : set_smem_attr(k_gemm_rows<true, true, false>);
-    e = e ? e : set_smem_attr(k_gemm_acc<false, true, true>);
-    e = e ? e : set_smem_attr(k_gemm_acc<true, true, false>);
-    e = e ? e : set_smem_attr(k_gemm_acc<true, true, true>);
     e = e ? e : set_smem_attr(k_gemm_big<false, true, true, 1>);
     e = e ? e : set_smem_attr(k_gemm_big<true, true, false, 1>);
     e = e ? e : set_smem_attr(k_gemm_big<true, true, true, 1>);
@@ -1080,7 +1023,7 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
     int n = 0;
     if (c->sharded()) {
         // gather+K-A+pack1, accept, K-C, mass, pack2, locate, finish (+ 6 fallback kernels)
-        n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 6 + (c->certify ? 6 : 0);
+        n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 6 + 6;
         if (path_out) *path_out = pl.path;
         if (launches_out) *launches_out = n;
         return NJ_OK;
@@ -1088,7 +1031,7 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
     if (pl.path == NJ_PATH_FUSED) n = 1;
     else if (pl.path == NJ_PATH_STAGED) n = 5;   // GEMM, row lse, accept, mass, locate
     else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 4;   // gather+KA, row lse, KB, KC, KD1, KD2
-    if (c->certify) n += 1;   // k_fb
+    n += 1;   // k_fb (every call; exits at once on an empty queue)
     if (path_out) *path_out = pl.path;
     if (launches_out) *launches_out = n;
     return NJ_OK;
@@ -1150,7 +1093,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         gp.tok = draft_tokens; gp.dl = c->dl;
         gp.use_row_g = 1;
         gp.w_evict_first = pl.N <= kBigMaxT ? 1 : 0;   // two chunks re-read W tiles from L2
-        if (const char* e = getenv("NJ_W_EVICT_FIRST")) gp.w_evict_first = atoi(e);
+        if (c->kn.w_evict_first >= 0) gp.w_evict_first = c->kn.w_evict_first;
         for (int b = 0; b < pl.B; ++b)
             for (int r = pl.row_off[b]; r < pl.row_off[b + 1]; ++r)
                 gp.row_g[r] = r + 1 < pl.row_off[b + 1] ? r - b : -1;
@@ -1192,7 +1135,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
         // K-A: stats GEMM over the draft rows (gathered contiguous), draft-logit capture;
         // all K-A launches share one partial layout (round-robin mode when G > 256)
-        const bool rrA = pl.G > kBigMaxT && !c->gemm_acc;
+        const bool rrA = pl.G > kBigMaxT;
         int gridA = c->grid;
         if (pl.G > 0) {
             k_gather_drafts<<<pl.G, 128, 0, st>>>(hidden, c->cfg.d, meta, c->hd);
@@ -1236,7 +1179,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             GemmBigParams gp{};
             gp.logits = c->logits_s; gp.ld_out = c->V_local;
             gp.part_m = c->part2_m; gp.part_s = c->part2_s;
-            const bool rrC = pl.B > kBigMaxT && !c->gemm_acc;
+            const bool rrC = pl.B > kBigMaxT;
             if ((s = launch_lmhead<true, true, false>(c, st, c->hs, pl.B, gp, rrC, &gridC)) != NJ_OK) return s;
         }
         // K-D: residual / bonus masses and the inverse-CDF draw
@@ -1254,7 +1197,10 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
         NJ_LAUNCHED(c, "k_locate", st);
     }
-    if (certify) {
+    // the fp64 fallback runs on every call (an empty queue exits at once): with
+    // certification it recomputes flagged decisions, and it always takes the
+    // zero-residual-mass draws (R6), which must come from p_n
+    {
         FbParams f = fb_params(c, hidden, W_lm, draft_tokens, draft_probs, ldq, uniforms, accept_len, next_token, dbg);
         if ((s = launch_fallback(c, st, f, meta)) != NJ_OK) return s;
     }
@@ -1372,7 +1318,7 @@ nj_status nj_propose(nj_ctx* c, void* stream, const uint16_t* hidden, const uint
         GemmBigParams gp{};
         gp.logits = q_out; gp.ld_out = ldq;
         gp.part_m = c->part2_m; gp.part_s = c->part2_s;
-        const bool rr = B > kBigMaxT && !c->gemm_acc;
+        const bool rr = B > kBigMaxT;
         std::pair<cudaEvent_t, cudaEvent_t> ev;
         if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
         if ((s = launch_lmhead<true, true, false>(c, st, hidden, B, gp, rr, &grid)) != NJ_OK) return s;
@@ -1398,72 +1344,28 @@ nj_status nj_propose(nj_ctx* c, void* stream, const uint16_t* hidden, const uint
 }
 
 nj_status nj_lmhead_logits(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
-                           const int32_t* rows, int32_t n_rows, float* logits, int64_t ld_out) {
+                           const int32_t* rows, int32_t n_rows, float* logits, int64_t ld_out, int32_t ks) {
     if (!c) return NJ_EINVAL;
     if (!hidden || !W_lm || !rows || !logits) return set_err(c, NJ_EINVAL, "NULL device pointer");
-    if (n_rows < 1 || n_rows > c->Gmax) return set_err(c, NJ_ESHAPE, "n_rows=%d outside [1, %d]", n_rows, c->Gmax);
+    if (n_rows < 1 || n_rows > std::min(c->Gmax, kMaxStatRows))
+        return set_err(c, NJ_ESHAPE, "n_rows=%d outside [1, %d]", n_rows, std::min(c->Gmax, kMaxStatRows));
     if (ld_out < c->V_local) return set_err(c, NJ_ESHAPE, "ld_out=%lld < V_local", (long long)ld_out);
+    if (ks < 0) return set_err(c, NJ_EINVAL, "ks=%d", ks);
     nj_status s;
     if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     k_gather_rows<<<n_rows, 128, 0, st>>>(hidden, c->cfg.d, rows, c->hd);
     NJ_LAUNCHED(c, "k_gather_rows", st);
-    GemmRowsParams gp{};
+    // the production LM-head GEMM (k_gemm_big, as the staged / two-pass paths and
+    // nj_propose launch it) writing fp32 logits; statistics go to scratch partials
+    GemmBigParams gp{};
     gp.logits = logits;
     gp.ld_out = ld_out;
-    return launch_gemm_rows<true, false, false>(c, st, c->hd, n_rows, gp);
-}
-
-nj_status nj_lmhead_logits_ks(nj_ctx* c, void* stream, const uint16_t* hidden, const uint16_t* W_lm,
-                              const int32_t* rows, int32_t n_rows, double* logits, int64_t ld_out, int32_t ks) {
-    if (!c) return NJ_EINVAL;
-    if (!hidden || !W_lm || !rows || !logits) return set_err(c, NJ_EINVAL, "NULL device pointer");
-    if (n_rows < 1 || n_rows > 32 || n_rows > c->Gmax) return set_err(c, NJ_ESHAPE, "n_rows=%d outside [1, 32]", n_rows);
-    if (ks < 1) return set_err(c, NJ_EINVAL, "ks=%d", ks);
-    nj_status s;
-    if ((s = ensure_w_maps(c, W_lm)) != NJ_OK) return s;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    k_gather_rows<<<n_rows, 128, 0, st>>>(hidden, c->cfg.d, rows, c->hd);
-    NJ_LAUNCHED(c, "k_gather_rows", st);
-    CUtensorMap tmH;
-    if (!encode_2d(&tmH, c->hd, n_rows, c->cfg.d, 32)) return set_err(c, NJ_ECUDA, "tensor map (H)");
-    ProbeKsParams pp{};
-    pp.R = n_rows; pp.V_local = c->V_local; pp.U = c->U; pp.num_kb = (c->cfg.d + kBK - 1) / kBK;
-    pp.nstages = 8; pp.ks = ks; pp.logits = logits; pp.ld_out = ld_out;
-    const size_t smem = (size_t)8 * (kTileBytesA + 32 * 128) + (2 * 8 + 2 * kProbeBufs) * 8 + 16;
-    static bool attr = false;
-    if (!attr) { NJ_CUDA(c, set_smem_attr(k_probe_ks)); attr = true; }
-    k_probe_ks<<<c->grid, kThreads, smem, st>>>(c->tmW128, c->tmW16, tmH, pp);
-    NJ_LAUNCHED(c, "k_probe_ks", st);
-    return NJ_OK;
-}
-
-nj_status nj_stream_test(nj_ctx* c, void* stream, const uint16_t* W, int32_t mode, int32_t group, int32_t nstages,
-                         const uint16_t* H, int32_t hrows) {
-    if (!c || !W) return NJ_EINVAL;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    StreamTestParams sp{};
-    sp.V_local = c->V_local; sp.U = c->U; sp.num_kb = (c->cfg.d + kBK - 1) / kBK; sp.nstages = nstages;
-    sp.mode = mode; sp.group = group; sp.ntiles_total = c->V_local / kTileV;
-    CUtensorMap m128, m16;
-    if (mode == 2) {
-        if (!encode_2d(&m128, W, (int64_t)sp.ntiles_total * sp.num_kb * kTileV, kBK, 128)) return set_err(c, NJ_ECUDA, "map");
-        m16 = m128;
-    } else {
-        if (!encode_2d(&m128, W, c->V_local, c->cfg.d, 128) || !encode_2d(&m16, W, c->V_local, c->cfg.d, 16))
-            return set_err(c, NJ_ECUDA, "map");
-    }
-    sp.hrows = H ? hrows : 0;
-    CUtensorMap mh = m128;
-    if (H && !encode_2d(&mh, H, hrows, c->cfg.d, hrows)) return set_err(c, NJ_ECUDA, "map H");
-    const size_t smem = (size_t)nstages * group * (kTileBytesA + sp.hrows * 128) + 2 * nstages * 8 + 16;
-    if (smem > (size_t)kSmemLimit) return set_err(c, NJ_ESHAPE, "smem %zu", smem);
-    NJ_CUDA(c, set_smem_attr(k_stream_test));
+    gp.part_m = c->part_m;
+    gp.part_s = c->part_s;
+    gp.ks = ks;
     int grid = c->grid;
-    if (const char* e = getenv("NJ_GRID")) grid = std::max(1, std::min(c->grid, atoi(e)));
-    k_stream_test<<<grid, 128, smem, st>>>(m128, m16, mh, sp);
-    NJ_LAUNCHED(c, "k_stream_test", st);
-    return NJ_OK;
+    return launch_lmhead<true, true, false>(c, st, c->hd, n_rows, gp, n_rows > kBigMaxT, &grid);
 }
 
 nj_status nj_sample_from_logits(nj_ctx* c, void* stream, const float* logits, int64_t ld_l, const int32_t* residual,
@@ -1493,7 +1395,7 @@ nj_status nj_sample_from_logits(nj_ctx* c, void* stream, const float* logits, in
     if (nj_status s2 = launch_mass(c, st, mp, B, false)) return s2;
     k_locate<<<B, kSampThreads, 0, st>>>(mp, meta);
     NJ_LAUNCHED(c, "k_locate", st);
-    if (c->certify) {
+    {   // certified draws (certify on) and zero-mass draws (R6, always)
         FbParams f{};
         f.V_local = c->V_local;
         f.fb_count = c->fb_count(); f.fb_list = c->fb_list(); f.req_flags = c->req_flags();
@@ -1650,15 +1552,5 @@ const char* nj_group_last_error(const nj_group* g) {
     return "";
 }
 
-
-nj_status nj_mma_probe(nj_ctx* c, void* stream, int32_t n, int32_t iters, int32_t mode, int64_t* cycles_out) {
-    if (!c || !cycles_out || n < 16 || n > 256 || n % 16 || iters < 1) return NJ_EINVAL;
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const size_t smem = kTileBytesA + 256 * 128 + 64;
-    NJ_CUDA(c, cudaFuncSetAttribute(k_mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_mma_probe<<<c->num_sms, 128, smem, st>>>(n, iters, mode, reinterpret_cast<long long*>(cycles_out));
-    NJ_LAUNCHED(c, "k_mma_probe", st);
-    return NJ_OK;
-}
 
 }  // extern "C"

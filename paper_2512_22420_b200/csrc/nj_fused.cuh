@@ -666,12 +666,12 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
             if (W > 0.0) {
                 if (T >= W) own = (cta == lp) ? 2 : 0;   // rounding overshoot (R5): clamp
                 else if (Ec <= T && T < Ic) own = 1;
-            } else if (cta == 0) {   // zero residual mass (R6): the fp64 fallback draws from p_n
-                p.accept_len[b] = r.n;
+            } else if (cta == 0) {   // zero residual mass (R6): the fp64 fallback (always
+                p.accept_len[b] = r.n;   // launched) draws from p_n, certified or not
                 p.next_token[b] = 0;
                 if (p.dbg_mass) p.dbg_mass[b] = 0.0;
                 if (p.dbg_flags) p.dbg_flags[b] = 2;
-                if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 2);
+                push_fallback(p.fb_count, p.fb_list, p.req_flags, b, 2);
             }
             owner[b] = own;
             tprime[b] = tp;

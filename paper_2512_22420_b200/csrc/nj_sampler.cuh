@@ -260,9 +260,12 @@ struct MassParams {
     int32_t probe;         // k_mass timing probes (NJ_MASS_PROBE; 0 in normal runs): 1 no copies, 2 no scans, 4 no totals
 };
 
+// Queue a draw for the fp64 fallback: certificate hits (certify on) and, always,
+// zero residual mass (R6: the draw must come from p_n, which the fallback does;
+// the fallback kernel is launched on every call).
 __device__ __forceinline__ void flag_draw(const MassParams& p, int b, int32_t bits) {
     if (p.xflags) atomicOr(&p.xflags[b], bits | 0x100);
-    else if (p.certify) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, bits);
+    else if (p.certify || (bits & 2)) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, bits);
 }
 
 __device__ __forceinline__ double sample_lse(const MassParams& p, int b) {
@@ -283,12 +286,25 @@ __device__ __forceinline__ double sample_lse(const MassParams& p, int b) {
 __device__ __forceinline__ const float* logits_row(const MassParams& p, int b) {
     return p.logits + (int64_t)(p.s_row ? p.s_row[b] : b) * p.ld;
 }
+// p(x) = exp(l(x) - lse) as exp(l - c) * corr with c = fp32(lse) and corr =
+// exp(c - lse) formed once per request in fp64: the fp32 rounding of lse (up to
+// ~1e-6 relative for |lse| ~ 15-25) would otherwise scale every p of the row
+// against q in the residual max(0, p - q) (the fused kernel's sample_weight
+// does the same).  __fmul_rn / __fsub_rn keep k_mass and k_locate bit-identical
+// (no contraction into an FMA in one of them only).
+__device__ __forceinline__ float p_weight(float l, float c, float corr) { return __fmul_rn(__expf(l - c), corr); }
+__device__ __forceinline__ float resid_weight(float pe, float qv) { return fmaxf(__fsub_rn(pe, qv), 0.f); }
+__device__ __forceinline__ float lse_corr(double lse) {
+    const float c = (float)lse;
+    return (float)exp((double)c - lse);
+}
+
 __device__ __forceinline__ float chunk_weight(const MassParams& p, const float* lrow, int c, int s, float lsef,
-                                              bool resid, const float* qrow) {
+                                              float corr, bool resid, const float* qrow) {
     const int x = c * kChunk + s * kSampThreads + (int)threadIdx.x;
     if (x >= p.V_local) return 0.f;
-    const float pe = p.w_inplace ? __ldcg(&lrow[x]) : __expf(__ldcg(&lrow[x]) - lsef);
-    return resid ? fmaxf(pe - __ldg(&qrow[x]), 0.f) : pe;
+    const float pe = p.w_inplace ? __ldcg(&lrow[x]) : p_weight(__ldcg(&lrow[x]), lsef, corr);
+    return resid ? resid_weight(pe, __ldg(&qrow[x])) : pe;
 }
 
 
@@ -363,9 +379,12 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
     // dependent global load (each would cost a DRAM latency per item)
     int* t_qrow = reinterpret_cast<int*>(ring + (size_t)NST * 2 * kChunk);   // -1: bonus row (no q)
     float* t_lsef = reinterpret_cast<float*>(t_qrow + B);
+    float* t_corr = t_lsef + B;
     for (int b = threadIdx.x; b < B; b += kSampThreads) {
         t_qrow[b] = p.s_resid[b] ? p.s_qrow[b] : -1;
-        t_lsef[b] = (float)__ldcg(&p.s_lse[b]);
+        const double l = __ldcg(&p.s_lse[b]);
+        t_lsef[b] = (float)l;
+        t_corr[b] = lse_corr(l);
     }
     __syncthreads();
     const int total = B * p.nchunks;
@@ -391,7 +410,7 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
         const int b = it / p.nchunks, c = it - b * p.nchunks;
         const int slot = j % NST;
         const bool resid = t_qrow[b] >= 0;
-        const float lsef = t_lsef[b];
+        const float lsef = t_lsef[b], corr = t_corr[b];
         const float* sl = ring + (size_t)slot * 2 * kChunk;
         const float* sq = sl + kChunk;
         const int x0 = c * kChunk + (int)threadIdx.x;
@@ -400,16 +419,16 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
 #pragma unroll
             for (int s = 0; s < kSubTiles; ++s) {
                 const int o = s * kSampThreads + (int)threadIdx.x;
-                const float e = __expf(sl[o] - lsef);
-                v[s] = resid ? fmaxf(e - sq[o], 0.f) : e;
+                const float e = p_weight(sl[o], lsef, corr);
+                v[s] = resid ? resid_weight(e, sq[o]) : e;
             }
         } else {
 #pragma unroll
             for (int s = 0; s < kSubTiles; ++s) {
                 const int o = s * kSampThreads + (int)threadIdx.x;
                 const bool in = x0 + s * kSampThreads < p.V_local;
-                const float l = in ? sl[o] : -INFINITY;
-                v[s] = resid ? fmaxf(__expf(l - lsef) - (in ? sq[o] : 0.f), 0.f) : __expf(l - lsef);
+                const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
+                v[s] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
             }
         }
         if (p.w_inplace && !resid) {   // nj_propose: q = the draw's weights, over the logits
@@ -445,7 +464,7 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
     }
     cp_async_wait_all();
 }
-constexpr size_t mass_smem(int nst, int B) { return (size_t)nst * 2 * kChunk * sizeof(float) + (size_t)B * 8; }
+constexpr size_t mass_smem(int nst, int B) { return (size_t)nst * 2 * kChunk * sizeof(float) + (size_t)B * 12; }
 
 // nj_verify_greedy: argmax over the vocabulary of
 // each fp32 logits row (ties -> lowest id).  Grid (nsplit, rows): a CTA scans
@@ -519,7 +538,7 @@ __global__ void k_greedy_decide(const ReqMeta m, const int32_t* __restrict__ dra
 __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, const ReqMeta m) {
     const int b = blockIdx.x;
     const double lse = sample_lse(p, b);
-    const float lsef = (float)lse;
+    const float lsef = (float)lse, corr = lse_corr(lse);
     const bool resid = p.s_resid[b] != 0;
     const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
     const float* lrow = logits_row(p, b);
@@ -624,7 +643,7 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     const double tp = sh[0];
     float w[kSubTiles], v[kSubTiles];
 #pragma unroll
-    for (int s = 0; s < kSubTiles; ++s) v[s] = w[s] = chunk_weight(p, lrow, c, s, lsef, resid, qrow);
+    for (int s = 0; s < kSubTiles; ++s) v[s] = w[s] = chunk_weight(p, lrow, c, s, lsef, corr, resid, qrow);
     warp_totals16(v, wt);   // k_mass's totals, bit for bit
     __syncthreads();
     __shared__ double spre[kSubTiles + 1];

@@ -4,6 +4,7 @@ import json, sys, time
 import numpy as np, torch
 sys.path.insert(0, ".")
 from paper_2512_22420_b200 import Verifier
+from scripts.probes import _probe
 from synth.inputs import make_batch, make_weight
 dev = torch.device("cuda:0")
 res = {}
@@ -64,14 +65,14 @@ v.lmhead_logits(b.hidden, Wf, rows, L32); torch.cuda.synchronize()
 res["plain"] = stats(L32.double())
 for ks in [1, 2, 4, 8, 16, 56, 224]:
     L = torch.empty(R, V, dtype=torch.float64, device=dev)
-    v.lmhead_logits_ks(b.hidden, Wf, rows, L, ks)
+    _probe.logits_ks(b.hidden[rows.long()], Wf, L, ks)
     torch.cuda.synchronize()
     st = stats(L)
     st["f32_rounded"] = stats(L.float().double())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(5):
-        v.lmhead_logits_ks(b.hidden, Wf, rows, L, ks)
+        _probe.logits_ks(b.hidden[rows.long()], Wf, L, ks)
     e1.record(); torch.cuda.synchronize()
     st["us"] = e0.elapsed_time(e1) / 5 * 1e3
     res[f"ks{ks}"] = st

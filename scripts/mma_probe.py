@@ -1,15 +1,13 @@
 """tcgen05.mma issue rate: cycles per 4-MMA group (M=128, N=n, K=16 each)."""
 import ctypes, sys, torch
 sys.path.insert(0, ".")
-from paper_2512_22420_b200 import Verifier, load
-lib = load()
+from scripts.probes import _probe
 dev = torch.device("cuda:0")
-v = Verifier(64, 1024, max_batch=1, gamma_max=1)
 out = torch.zeros(148, dtype=torch.int64, device=dev)
 for mode in (0, 2, 1):
     for n in (32, 64, 128, 256):
         for _ in range(2):
-            st = lib.nj_mma_probe(v._h, None, n, 4096, mode, out.data_ptr())
+            _probe.mma_probe(n, 4096, mode, out)
         torch.cuda.synchronize()
         c = out.float()
         ideal = 4 * 128 * n / 256

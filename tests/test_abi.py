@@ -33,8 +33,15 @@ def test_every_declared_symbol_is_exported():
     assert len(syms) >= 19
     missing = [s for s in syms if not hasattr(lib, s)]
     assert not missing, missing
-    assert sorted(set(syms) - {"nj_stream_test"}) == sorted(set(_lib.EXPORTS) - {"nj_stream_test"}) or \
-        set(_lib.EXPORTS) <= set(syms)
+    assert sorted(syms) == sorted(_lib.EXPORTS)
+
+
+def test_probes_are_not_in_the_product_library():
+    """Measurement probes live in scripts/probes/libnj_probe.so, not libnj.so."""
+    out = subprocess.run(["nm", "-D", "--defined-only", _build.build()], capture_output=True, text=True).stdout
+    for sym in ("nj_stream_test", "nj_mma_probe", "nj_lmhead_logits_ks", "k_probe_ks", "k_stream_test",
+                "k_mma_probe", "k_gemm_acc", "k_gemm_rows"):
+        assert sym not in out, sym
 
 
 def test_sass_is_sm100a_tcgen05():

@@ -32,6 +32,17 @@ def check(b, acc, nxt, tokens=None):
     ok = ~r["tie"]
     assert ((acc != r["accept_len"]) & ok).sum() == 0, (acc, r["accept_len"])
     assert ((nxt != r["next_token"]) & ok).sum() == 0, (nxt, r["next_token"])
+    # excused requests (a consulted row's top-2 gap <= 1e-4): the GPU outcome must
+    # follow from SOME choice of near-maximal tokens (within 1e-4 of the row max)
+    if (~ok).any():
+        L = oracle.logits(n["hidden_bits"], n["W_bits"])
+        g = n["gamma"]
+        ro = np.concatenate([[0], np.cumsum(g + 1)])
+        near = lambda j, t: L[j, t] >= L[j].max() - 1e-4
+        for bb in np.nonzero(~ok)[0]:
+            a, t, r0, d0 = int(acc[bb]), int(nxt[bb]), ro[bb], ro[bb] - bb
+            assert all(near(r0 + i, x[d0 + i]) for i in range(a)), bb
+            assert near(r0 + a, t) and (a == g[bb] or t != x[d0 + a]), bb
     return r
 
 

@@ -1,20 +1,28 @@
 """GPU parity: libnj (CUDA, sm_100a, through the C ABI) vs the fp64 oracle on
 identical seeded inputs.
 
-Bar (BASELINE.json north_star; R11/R12):
+Bar (BASELINE.json north_star; R11/R12; tests/parity.py):
   * accept_len / next_token bit-exact, except requests whose oracle margin
-    |a_i - u_i| or |F - u| is <= 1e-6 (counted, reported, excused);
+    |a_i - u_i| or |F - u| is <= 1e-6; those are counted (terminal summary),
+    their number is bounded by the oracle's expected count sum p_tie, and the
+    GPU outcome must still be one of the tied decisions' branches;
+    requests the GPU recomputed in fp64 (NJ_FLAG_FALLBACK) are exact even in
+    the band;
   * probabilities: |ln p_gpu - ln p_oracle| <= 2e-3 (bf16 GEMM inputs), and the
     tighter regression bound this build actually meets;
+    W_b (dbg mass) within 2e-5 absolute of the oracle's (the sum over the
+    vocabulary of the <= 4e-6 relative p error of DESIGN.md §6, 5x margin);
   * sampler stage on given fp32 logits: W_b within 1e-5 relative.
 """
 import dataclasses
+import os
 
 import numpy as np
 import pytest
 import torch
 
 import oracle
+import parity
 from oracle import bruteforce
 from paper_2512_22420_b200 import (NJ_FLAG_FALLBACK, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PATH,
                                    NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_STAGED, NJ_PATH_TWOPASS, NJError, Verifier)
@@ -23,6 +31,7 @@ from synth.inputs import dyadic_rows, make_batch, make_sampler_case, make_weight
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
 QV, QD = 152064, 3584
+MASS_TOL = 2e-5
 _W = {}
 
 
@@ -32,9 +41,17 @@ def w_full():
     return _W["W"]
 
 
-def run(b, path=NJ_PATH_AUTO, certify=True, force_fb=False, max_batch=None, gamma_max=5):
+def w_full_f64():
+    """fp64 copy of the Qwen-shape W for the oracle's BLAS step 1 (reused)."""
+    if "W64" not in _W:
+        _W["W64"] = oracle.weight_f64(oracle.bf16_bits(w_full()))
+    return _W["W64"]
+
+
+def run(b, path=NJ_PATH_AUTO, certify=True, force_fb=False, max_batch=None, gamma_max=5, v=None):
     B = b.B
-    v = Verifier(b.hidden.shape[1], b.W.shape[0], max_batch=max_batch or B, gamma_max=gamma_max)
+    if v is None:
+        v = Verifier(b.hidden.shape[1], b.W.shape[0], max_batch=max_batch or B, gamma_max=gamma_max)
     v.set_option(NJ_OPT_PATH, path)
     v.set_option(NJ_OPT_CERTIFY, int(certify))
     v.set_option(NJ_OPT_FORCE_FALLBACK, int(force_fb))
@@ -47,47 +64,104 @@ def run(b, path=NJ_PATH_AUTO, certify=True, force_fb=False, max_batch=None, gamm
     return acc.cpu().numpy(), nxt.cpu().numpy(), {k: t.cpu().numpy() for k, t in dd.items()}, v
 
 
-def check(b, acc, nxt, dd, lnp_tol=2e-3, lse_tol=None):
-    n = b.to_numpy()
-    r = oracle.verify(n["hidden_bits"], n["W_bits"], n["draft_tokens"], n["draft_probs"], n["gamma"], n["uniforms"])
-    ok = ~r["tie"]
-    bad_a = np.nonzero((acc != r["accept_len"]) & ok)[0]
-    bad_t = np.nonzero((nxt != r["next_token"]) & ok)[0]
-    assert bad_a.size == 0, (bad_a, acc[bad_a], r["accept_len"][bad_a])
-    assert bad_t.size == 0, (bad_t, nxt[bad_t], r["next_token"][bad_t])
-    assert ((acc >= 0) & (acc <= n["gamma"])).all()
+def oracle_logits(b, n=None):
+    n = n or b.to_numpy()
+    if b.W.shape == (QV, QD) and b.N >= 64:
+        return oracle.logits_blas(n["hidden_bits"], None, W64=w_full_f64())
+    return oracle.logits(n["hidden_bits"], n["W_bits"])
+
+
+def check(b, acc, nxt, dd, lnp_tol=2e-3, lse_tol=None, name=None, certified=True, L=None, n=None, r=None,
+          mass_tol=MASS_TOL):
+    """Decisions via tests/parity.py; probabilities (p_draft, lse, W_b) against
+    the oracle's fp64 values.  Returns the oracle result."""
+    name = name or os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0]
+    n = n or b.to_numpy()
+    if L is None and r is None:
+        L = oracle_logits(b, n)
+    r = parity.check(name, n, acc, nxt, r=r, gpu_flags=dd.get("flags"), L=L, certified=certified)
     if b.G:
         m = r["p_draft"] > 1e-20
         lnp = np.abs(np.log(np.maximum(dd["p_draft"][:b.G][m], 1e-38)) - np.log(r["p_draft"][m]))
-        assert lnp.max(initial=0) <= lnp_tol
+        assert lnp.max(initial=0) <= lnp_tol, lnp.max(initial=0)
     if lse_tol is not None:
         fin = np.isfinite(dd["lse"])
         assert np.abs(dd["lse"][fin] - r["lse"][fin]).max(initial=0) <= lse_tol
-    return int(r["tie"].sum())
+    # W_b of the distribution drawn from, where the GPU drew from the same one
+    same = (acc == r["accept_len"]) & ~((r["flags"] & oracle.F_ZERO_MASS) != 0)
+    if "mass" in dd and same.any():
+        err = np.abs(dd["mass"][same] - r["mass"][same])
+        assert err.max() <= mass_tol, (err.max(), np.argmax(err))
+    return r
 
 
-# ----------------------------------------------------------------- GEMM probe
-@pytest.mark.parametrize("V,d,R", [(1024, 128, 20), (1000, 64, 37), (QV, QD, 32)])
-def test_lmhead_probe_vs_fp64(V, d, R):
+# ----------------------------------------------------------------- golden C1 (BJ configs[0])
+@pytest.mark.parametrize("path", [NJ_PATH_FUSED, NJ_PATH_STAGED, NJ_PATH_TWOPASS])
+def test_c1_golden_fixed_uniforms(path):
+    """tests/golden/c1_fixed_uniforms.json (written by scripts/make_golden.py from
+    the oracle only): forced uniforms hitting accept_len 0, 1, 2, 3 and random
+    draws, on every path, bit-exact."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c1_fixed_uniforms.json")))
+    b = make_batch(1, 3, V=g["V"], d=g["d"], seed=g["seed"])   # generated on the host, as the fixture was
+    cases = g["cases"]
+    step = 12 if path == NJ_PATH_FUSED else len(cases)        # fused path: N <= 48 rows per call
+    for s0 in range(0, len(cases), step):
+        cs = cases[s0:s0 + step]
+        R = len(cs)
+        # the cases as one batch of R identical requests with their own uniforms
+        bb = dataclasses.replace(b, hidden=b.hidden.repeat(R, 1).to(DEV), W=b.W.to(DEV),
+                                 draft_tokens=b.draft_tokens.repeat(R).to(DEV),
+                                 draft_probs=b.draft_probs.repeat(R, 1).to(DEV), gamma=np.full(R, 3, np.int32),
+                                 uniforms=torch.tensor([x for c in cs for x in c["uniforms"]], dtype=torch.float32,
+                                                       device=DEV))
+        acc, nxt, dd, _ = run(bb, path, max_batch=R)
+        assert [int(x) for x in acc] == [c["accept_len"] for c in cs]
+        assert [int(x) for x in nxt] == [c["next_token"] for c in cs]
+
+
+# ----------------------------------------------------------------- production GEMM, element-wise
+@pytest.mark.parametrize("V,d,R,ks", [(1024, 128, 20, 0), (1000, 64, 37, 0), (QV, QD, 40, 0), (QV, QD, 300, 0),
+                                      (QV, QD, 40, 8)])
+def test_production_gemm_logits_vs_oracle(V, d, R, ks):
+    """nj_lmhead_logits runs k_gemm_big (the kernel the staged / two-pass paths
+    and nj_propose launch) and returns fp32 logits; every element of every row
+    is compared with the oracle's fp64 logits (R = 300: two token chunks), and
+    the full p rows via ln p = l - logsumexp(l): within BJ's 2e-3 and within the
+    measured bound of DESIGN.md §6 (restart every 4 k-blocks: |d ln p| <= 2e-5;
+    every 8: <= 4e-5)."""
     W = w_full() if V == QV else make_weight(V, d, 1, DEV)
-    h = (torch.randn(R, d, device=DEV) * 1.2).to(torch.bfloat16)
+    g = torch.Generator(device=DEV).manual_seed(R + ks)
+    h = (torch.randn(R, d, device=DEV, generator=g) *
+         torch.exp(torch.empty(R, 1, device=DEV).uniform_(np.log(0.6), np.log(1.6), generator=g))).to(torch.bfloat16)
     v = Verifier(d, V, max_batch=R, gamma_max=1)
     out = torch.full((R, V), float("nan"), device=DEV)
-    v.lmhead_logits(h, W, torch.arange(R, dtype=torch.int32, device=DEV), out)
+    v.lmhead_logits(h, W, torch.arange(R, dtype=torch.int32, device=DEV), out, ks=ks)
     torch.cuda.synchronize()
-    ref = h.double() @ W.double().t()
-    assert not torch.isnan(out).any()
-    assert float((out.double() - ref).abs().max()) < 2e-4          # plain tcgen05 fp32 accumulation
+    hb = oracle.bf16_bits(h)
+    ref = (oracle.logits_blas(hb, None, W64=w_full_f64()) if V == QV else oracle.logits(hb, oracle.bf16_bits(W)))
+    got = out.double().cpu().numpy()
+    assert np.isfinite(got).all()
+    dl = np.abs(got - ref)
+    lse_g = np.logaddexp.reduce(got, axis=1)
+    lse_r = np.logaddexp.reduce(ref, axis=1)
+    dlnp = np.abs((got - lse_g[:, None]) - (ref - lse_r[:, None]))
+    bound = 4e-5 if ks == 8 else 2e-5
+    print(f"[gemm] V={V} R={R} ks={ks}: max|dl|={dl.max():.3g} max|d ln p|={dlnp.max():.3g}")
+    assert dlnp.max() <= 2e-3
+    assert dlnp.max() <= bound, dlnp.max()
+    assert dl.max() <= 2 * bound, dl.max()
 
 
 def test_accuracy_probe_restarted_accumulator():
     """ks = 4 (accumulator restarted every k-block, fp64 partial sums) is the
-    fused path's scheme: logit error <= 2e-6 at the Qwen shape."""
+    fused path's scheme: logit error <= 2e-6 at the Qwen shape (probe kernel,
+    scripts/probes)."""
+    from scripts.probes import _probe
     W = w_full()
     b = make_batch(8, 3, V=QV, d=QD, seed=11, device=DEV, W=W)
-    v = Verifier(QD, QV, max_batch=64, gamma_max=5)
     L = torch.empty(b.N, QV, dtype=torch.float64, device=DEV)
-    v.lmhead_logits_ks(b.hidden, W, torch.arange(b.N, dtype=torch.int32, device=DEV), L, 4)
+    _probe.logits_ks(b.hidden, W, L, 4)
     torch.cuda.synchronize()
     ref = b.hidden.double() @ W.double().t()
     assert float((L - ref).abs().max()) < 2e-6
@@ -103,11 +177,10 @@ def test_fused_toy_c1(seed):
 
 def test_fused_c2_full_size():
     W = w_full()
-    ties = 0
     for seed in range(4):
         b = make_batch(8, 3, V=QV, d=QD, seed=100 + seed, device=DEV, W=W)
         acc, nxt, dd, _ = run(b)
-        ties += check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)   # 16-MMA partials, DESIGN.md §6
+        check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)   # 16-MMA partials, DESIGN.md §6
 
 
 @pytest.mark.parametrize("B,g", [(8, "mixed:5"), (1, 0), (48, 0), (16, 2), (12, 3), (6, 5), (24, 1)])
@@ -236,10 +309,16 @@ def test_forced_fp64_fallback_matches_oracle():
         assert (dd["flags"] & NJ_FLAG_FALLBACK).all()
 
 
-def test_sampler_stage_vs_oracle():
-    for B, V in [(6, 5000), (32, QV)]:
-        logits, resid, q, u = make_sampler_case(B, V, 3, DEV)
+@pytest.mark.parametrize("certify", [1, 0])
+def test_sampler_stage_vs_oracle(certify):
+    """K-D alone (k_mass + k_locate) on given fp32 logits vs the stage oracle:
+    W_b within 1e-5 relative, tokens exact outside the 1e-6 band -- with the
+    draw certificate on and OFF (the raw sampler production relies on:
+    every draw of nj_verify is uncertified, R16)."""
+    for B, V, seed in [(6, 5000, 3), (32, QV, 3), (256, QV, 4)]:
+        logits, resid, q, u = make_sampler_case(B, V, seed, DEV)
         v = Verifier(16, V, max_batch=B, gamma_max=1)
+        v.set_option(NJ_OPT_CERTIFY, certify)
         nxt = torch.empty(B, dtype=torch.int32, device=DEV)
         mass = torch.empty(B, dtype=torch.float64, device=DEV)
         v.sample_from_logits(logits, resid, q, u, nxt, mass)
@@ -248,7 +327,13 @@ def test_sampler_stage_vs_oracle():
                                       u.cpu().numpy().astype(np.float64))
         np.testing.assert_allclose(mass.cpu().numpy(), r["mass"], rtol=1e-5)
         ok = ~r["tie"]
-        assert (nxt.cpu().numpy()[ok] == r["next_token"][ok]).all()
+        bad = np.nonzero(nxt.cpu().numpy()[ok] != r["next_token"][ok])[0]
+        assert bad.size == 0, (certify, B, bad)
+        parity.STATS.append({"test": f"sampler_stage certify={certify} B={B} V={V}", "B": B, "N": B,
+                             "ties": int(r["tie"].sum()), "accept_ties": 0, "draw_ties": int(r["tie"].sum()),
+                             "expected_ties": float("nan"), "excused": int(r["tie"].sum()),
+                             "excused_differing": int((nxt.cpu().numpy()[~ok] != r["next_token"][~ok]).sum()),
+                             "fallback": 0, "certified": bool(certify)})
 
 
 def test_verify_host_equals_device():
@@ -278,7 +363,24 @@ def test_uncertified_decisions_full_size(B, g):
     paths by size)."""
     b = make_batch(B, g, V=QV, d=QD, seed=B * 3 + 1, device=DEV, W=w_full())
     acc, nxt, dd, v = run(b, certify=False)
-    check(b, acc, nxt, dd, lnp_tol=2e-5)
+    check(b, acc, nxt, dd, lnp_tol=2e-5, certified=False)
+
+
+# ----------------------------------------------------------------- full size (the bench configurations)
+@pytest.mark.parametrize("B,g,seed", [(256, 5, 901), (256, "mixed:5", 902), (256, 2, 903), (64, 3, 904)])
+def test_full_size_bench_configs(B, g, seed):
+    """Every request of the batches bench.py times (C3-max B=256 gamma=5, the
+    mixed-gamma batch, C5's B=256 gamma=2 unsharded, the staged ridge point
+    B=64 gamma=3) against the oracle, in the launch configuration the bench
+    uses (AUTO path, certificate on), then the same batch with the certificate
+    OFF (the raw kernels' decisions)."""
+    b = make_batch(B, g, V=QV, d=QD, seed=seed, device=DEV, W=w_full())
+    n = b.to_numpy()
+    L = oracle_logits(b, n)
+    acc, nxt, dd, v = run(b)
+    r = check(b, acc, nxt, dd, lnp_tol=4e-5, n=n, L=L, name=f"full_size B={B} g={g} certified")
+    acc, nxt, dd, _ = run(b, certify=False, v=v)
+    check(b, acc, nxt, dd, lnp_tol=4e-5, n=n, L=L, r=r, certified=False, name=f"full_size B={B} g={g} uncertified")
 
 
 def test_verify_host_zero_copy_and_copy_paths_agree():

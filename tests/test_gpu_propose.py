@@ -9,6 +9,7 @@ import pytest
 import torch
 
 import oracle
+import parity
 from paper_2512_22420_b200 import NJError, Verifier
 from synth.inputs import make_batch, make_weight
 
@@ -29,11 +30,16 @@ def run(b, ldq=None):
 
 
 def check(b, tok, q, lnq_tol=2e-5):
+    """Tokens via tests/parity.py (nj_propose is the gamma = 0 draw of q:
+    bit-exact outside the 1e-6 band, excused draws must be a neighbour across
+    the tied CDF boundary, excused count vs sum p_tie); q rows vs fp64."""
+    import os
     n = b.to_numpy()
     r = oracle.propose(n["hidden_bits"], n["W_bits"], n["uniforms"])
-    ok = ~r["tie"]
-    bad = np.nonzero((tok != r["tokens"]) & ok)[0]
-    assert bad.size == 0, (bad, tok[bad], r["tokens"][bad])
+    V = b.W.shape[0]
+    nv = {"hidden_bits": n["hidden_bits"], "W_bits": n["W_bits"], "draft_tokens": np.zeros(0, np.int32),
+          "draft_probs": np.zeros((1, V), np.float32), "gamma": np.zeros(b.B, np.int32), "uniforms": n["uniforms"]}
+    parity.check(os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], nv, np.zeros(b.B, np.int32), tok)
     assert (q[np.arange(b.B), tok] > 0).all()
     m = r["q"] > 1e-30
     err = np.abs(np.log(np.maximum(q[m], 1e-45)) - np.log(r["q"][m]))
