@@ -121,6 +121,21 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks with
+    torch.distributed.run on this node (127.0.0.1, a free port); rank 0 prints
+    the JSON line.  Returns the launcher's exit code."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -205,16 +220,76 @@ def cpu_baseline(b, budget_s: float, max_requests: int | None = None):
         if time.perf_counter() - t0 > budget_s or runs >= 20:
             break
     dt = time.perf_counter() - t0
+    # per-core figure: one thread on the first request only
+    nr1, nd1 = int(g[0] + 1), int(g[0])
+    t1 = time.perf_counter()
+    oracle.verify(n["hidden_bits"][:nr1], n["W_bits"], n["draft_tokens"][:nd1], n["draft_probs"][:max(nd1, 1)],
+                  g[:1], n["uniforms"][:nr1], nthreads=1)
+    dt1 = time.perf_counter() - t1
     return {"value": nr * runs / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
-            "sample": f"{runs} full run(s) of {k} request(s) of the {b.B}-request batch ({nr} positions), {dt:.1f} s"}
+            "cpu_model": cpu_model(), "per_core_value": nr1 / dt1,
+            "sample": f"{runs} full run(s) of {k} request(s) of the {b.B}-request batch ({nr} positions), {dt:.1f} s; "
+                      f"per core: 1 thread, 1 request ({nr1} positions), {dt1:.1f} s"}
+
+
+def sub_batch(b, b0: int, b1: int):
+    """Requests [b0, b1) of a packed batch as their own packed batch (contiguous
+    copies): the row-balanced share of one rank in the strong-scaling mode."""
+    import numpy as np
+
+    from synth.inputs import Batch
+    g = b.gamma
+    ro = np.concatenate([[0], np.cumsum(g + 1)])
+    do = np.concatenate([[0], np.cumsum(g)])
+    G = int(do[b1] - do[b0])
+    q = b.draft_probs[do[b0]:do[b1]].contiguous() if G else b.draft_probs[:1].contiguous()
+    return Batch(b.hidden[ro[b0]:ro[b1]].contiguous(), b.W, b.draft_tokens[do[b0]:do[b1]].contiguous(), q,
+                 np.ascontiguousarray(g[b0:b1]), b.uniforms[ro[b0]:ro[b1]].contiguous())
+
+
+def step_stats(ms):
+    """median / p10 / p90 / mean of per-step device times (ms)."""
+    import numpy as np
+    a = np.asarray(ms, np.float64)
+    if a.size == 0:
+        return None
+    return {"median": float(np.median(a)), "p10": float(np.percentile(a, 10)), "p90": float(np.percentile(a, 90)),
+            "mean": float(a.mean()), "n": int(a.size)}
+
+
+def timed_steps(run_step, steps: int, stream, local: int):
+    """Time `steps` calls of run_step(i) on `stream` with CUDA events: one event
+    before the first and one after every step (so per-step device times come
+    from consecutive events), NVML clocks sampled meanwhile.  Returns
+    (total_ms, per_step_ms, clock summary)."""
+    import torch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    with ClockSampler(local) as clk:
+        ev[0].record(stream)
+        for i in range(steps):
+            run_step(i)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    return ev[0].elapsed_time(ev[-1]), per, clk.summary()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def bench_nj(args, ws, rank, local):
     import numpy as np
     import torch
 
-    from paper_2512_22420_b200 import (NJ_OPT_PATH, NJ_OPT_PROFILE, NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_STAGED,
-                                       NJ_PATH_TWOPASS, Verifier)
+    from paper_2512_22420_b200 import NJ_OPT_PATH, NJ_OPT_PROFILE, NJ_PATH_FUSED, NJ_PATH_STAGED, Verifier
+    from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
     torch.cuda.set_device(local)
@@ -224,45 +299,51 @@ def bench_nj(args, ws, rank, local):
         dist.init_process_group("nccl", device_id=dev)
     B, gamma, path = CONFIGS[args.config]
     path = PATH_NAMES.index(args.path or path)
+    strong = args.scaling == "strong" and ws > 1
     W = make_weight(V_Q, D_Q, args.seed, dev)
-    nb = 4   # rotate independent batches (each rank its own seeds)
-    batches = [make_batch(B, gamma, V=V_Q, d=D_Q, seed=args.seed * 1000 + rank * 16 + i, device=dev, W=W)
-               for i in range(nb)]
-    gmax = max(int(b.gamma.max()) for b in batches)
-    v = Verifier(D_Q, V_Q, max_batch=B, gamma_max=max(gmax, 1), device=local)
+    nb = 4   # rotating independent batches
+    if strong:
+        # one global batch per step, identical on every rank; each rank verifies its
+        # row-balanced contiguous share (no data-path collective)
+        full = [make_batch(B, gamma, V=V_Q, d=D_Q, seed=args.seed * 1000 + i, device=dev, W=W) for i in range(nb)]
+        batches = []
+        for bf in full:
+            b0, b1 = njdist.split_requests(bf.gamma, ws, rank)
+            batches.append(sub_batch(bf, b0, b1))
+        N_global = full[0].N
+        del full
+    else:
+        batches = [make_batch(B, gamma, V=V_Q, d=D_Q, seed=args.seed * 1000 + rank * 16 + i, device=dev, W=W)
+                   for i in range(nb)]
+        N_global = batches[0].N * ws
+    Bl = batches[0].B
+    gmax = max([int(b.gamma.max()) for b in batches if b.B] + [1])
+    v = Verifier(D_Q, V_Q, max_batch=max(Bl, 1), gamma_max=max(gmax, 1), device=local)
     v.set_option(NJ_OPT_PATH, path)
-    p_used, launches = v.plan(batches[0].gamma)
-    acc = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(nb)]
-    nxt = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(nb)]
+    p_used, launches = v.plan(batches[0].gamma) if Bl else (0, 0)
+    acc = [torch.empty(max(Bl, 1), dtype=torch.int32, device=dev) for _ in range(nb)]
+    nxt = [torch.empty(max(Bl, 1), dtype=torch.int32, device=dev) for _ in range(nb)]
     stream = torch.cuda.current_stream()
 
     def step(i):
         b = batches[i % nb]
-        v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc[i % nb], nxt[i % nb])
+        if b.B:
+            v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc[i % nb], nxt[i % nb])
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
+    # eager pass: the dominant kernel bracketed by CUDA events on the launch stream
     v.set_option(NJ_OPT_PROFILE, 1)
     v.kernel_time(reset=True)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for i in range(args.steps):
-            step(i)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    ms = e0.elapsed_time(e1)
+    ms_eager, per_eager, clk = timed_steps(step, args.steps, stream, local)
     kms, kn = v.kernel_time(reset=True)
     v.set_option(NJ_OPT_PROFILE, 0)
-    ms_eager = ms
-    graph_ok = False
-    if not args.no_graph:
+    ms, per, graph_ok = ms_eager, per_eager, False
+    if not args.no_graph and Bl:
         # the same steps replayed from CUDA graphs (one per rotating batch; nj_verify does
         # no host synchronisation, so a call is capturable): no per-launch host overhead
         try:
@@ -285,42 +366,32 @@ def bench_nj(args, ws, rank, local):
             if ws > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with ClockSampler(local) as clk:
-                g0.record(stream)
-                for i in range(args.steps):
-                    graphs[i % nb].replay()
-                g1.record(stream)
-                torch.cuda.synchronize()
-            if ws > 1:
-                dist.barrier()
-            ms = g0.elapsed_time(g1)
+            ms, per, clk = timed_steps(lambda i: graphs[i % nb].replay(), args.steps, stream, local)
             graph_ok = True
         except Exception as e:   # graph capture unavailable: keep the eager timing
             print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
-    # accepted tokens in the timed steps (outputs of the last nb steps are representative: same batches)
-    acc_tok, rejected = 0, 0
+    if ws > 1:
+        dist.barrier()
+    # accepted tokens in the timed steps (the last outputs of each rotating batch)
     per_batch = []
     for j in range(nb):
-        a = acc[j].cpu().numpy()
+        a = acc[j][:Bl].cpu().numpy()
         per_batch.append((int((a + 1).sum()), int((a < batches[j].gamma).sum())))
-    for i in range(args.steps):
-        acc_tok += per_batch[i % nb][0]
-        rejected += per_batch[i % nb][1]
-    N = batches[0].N
-    G = batches[0].G
-    t_max = ms
+    acc_tok = sum(per_batch[i % nb][0] for i in range(args.steps))
+    rejected = sum(per_batch[i % nb][1] for i in range(args.steps))
+    N, G = batches[0].N, batches[0].G
+    t_max = njdist.max_over_ranks(ms, dev)
+    tok_all = acc_tok
     if ws > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
-    positions = N * args.steps * ws
-    value = positions / (t_max / 1e3)
+        t = torch.tensor([float(acc_tok)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        tok_all = float(t.item())
+    value = N_global * args.steps / (t_max / 1e3)
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
     # roofline of the dominant kernel (DESIGN.md §5 / §8): fused path -> HBM bytes;
     # staged -> the one GEMM pass over N rows; two-pass -> K-A over the G draft rows.
-    # A GEMM over R rows is HBM-bound below the ridge (R < peak_flops / (hbm_bw)
-    # ~ 250 rows: algorithmic bytes = W + H) and tensor-bound above (2 R V d flops).
+    # A GEMM over R rows is HBM-bound below the ridge (R < peak_flops / hbm_bw
+    # ~ 248 rows: algorithmic bytes = W + H) and tensor-bound above (2 R V d flops).
     kern_ms = kms / max(kn, 1)
     R_avg = rejected / args.steps
     ridge = tf_burst * 1e12 / (hbm * 1e9)
@@ -345,133 +416,216 @@ def bench_nj(args, ws, rank, local):
                     "frac": achieved / tf_burst, "algorithmic_flops_per_launch": flops, "rows": R}
     roof["peak_source"] = peak_src
     roof["kernel_ms_avg"] = kern_ms
-    roof["kernel_share_of_step"] = kms / ms if ms > 0 else None
+    # share of the step in the SAME (eager, event-bracketed) pass the kernel was timed in
+    roof["kernel_share_of_step"] = kms / ms_eager if ms_eager > 0 else None
     traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     roof["traffic"] = None
     if os.path.exists(traffic_file):
-        tr = json.load(open(traffic_file)).get(args.config, {}).get(roof["kernel"].split()[0])
-        roof["traffic"] = tr
+        roof["traffic"] = json.load(open(traffic_file)).get(args.config, {}).get(roof["kernel"].split()[0])
     # end-to-end through the host API (pinned host buffers, copies inside the timed region)
     e2e = None
-    if rank == 0 or ws > 1:
+    if Bl:
         b = batches[0]
         pin = lambda t: t.cpu().pin_memory()
         hh, th, qh, uh = pin(b.hidden), pin(b.draft_tokens), pin(b.draft_probs), pin(b.uniforms)
-        ah = torch.empty(B, dtype=torch.int32).pin_memory()
-        nh = torch.empty(B, dtype=torch.int32).pin_memory()
+        ah = torch.empty(Bl, dtype=torch.int32).pin_memory()
+        nh = torch.empty(Bl, dtype=torch.int32).pin_memory()
         k_e2e = max(5, min(args.steps, 50))
         for _ in range(3):
             v.verify_host(hh, W, th, qh, b.gamma, uh, ah, nh)
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
         for _ in range(k_e2e):
             v.verify_host(hh, W, th, qh, b.gamma, uh, ah, nh)
         s1.record(stream)
         torch.cuda.synchronize()
-        e_ms = s0.elapsed_time(s1)
+        e_ms = njdist.max_over_ranks(s0.elapsed_time(s1), dev)
         # bytes that cross the host link per step: the copied hidden / tokens / uniforms,
         # plus the draft-probability bytes the kernels read in place (zero copy):
         # q_i(x_i) of every draft and the sample row of every rejected request
         rej0 = per_batch[0][1]
         h2d = (b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.N * 4 + b.G * 4 + rej0 * V_Q * 4)
-        e2e = {"value": N * k_e2e * ws / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(2 * B * 4), "steps": k_e2e, "api": "nj_verify_host",
+        e2e = {"value": N_global * k_e2e / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(2 * Bl * 4), "steps": k_e2e, "api": "nj_verify_host",
                "q_rows": "read in place from pinned host memory (NJ_OPT_Q_ZERO_COPY)"}
     if ws > 1:
         dist.barrier()
     if rank != 0:
         dist.destroy_process_group()
         return
-    cpu = None if args.no_cpu_baseline else cpu_baseline(batches[0].to_cpu() if hasattr(batches[0], "to_cpu")
-                                                          else _cpu_batch(batches[0]), args.cpu_budget)
+    cpu = None if args.no_cpu_baseline else cpu_baseline(_cpu_batch(batches[0]), args.cpu_budget)
+    scaling = "strong" if strong else "weak"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"qwen7b_{args.config}", "B": B, "gamma": gamma, "N_per_step": N,
-                       "d": D_Q, "V": V_Q, "global_batch": B * ws,
+            "config": {"workload": f"qwen7b_{args.config}", "B": B, "gamma": gamma, "N_per_step": N_global,
+                       "N_per_rank_rank0": N, "d": D_Q, "V": V_Q, "global_batch": B * (1 if strong else ws),
                        "path": PATH_NAMES[p_used],
-                       "parallelism": f"request-sharded x{ws} (no data-path collective)",
-                       "l2": "inputs larger than L2: W_lm (1.09 GB) streamed from HBM every step",
+                       "parallelism": (f"request-sharded x{ws}, " + ("one global batch split by rows"
+                                                                     if strong else "own batch per rank")
+                                       + " (no data-path collective)"),
+                       "l2": "inputs larger than L2: W_lm (1.09 GB > 126 MB L2) streamed from HBM every step; "
+                             "4 rotating batches",
                        "launch": "CUDA graph replay per step" if graph_ok else "eager launches",
                        "ms_per_step_eager": ms_eager / args.steps},
-            "accepted_tokens_per_s": acc_tok * ws / (t_max / 1e3),
-            "realised_beta_tokens_per_request": acc_tok / (args.steps * B),
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "step_ms": step_stats(per), "step_ms_eager": step_stats(per_eager),
+            "accepted_tokens_per_s": tok_all / (t_max / 1e3),
+            "realised_tokens_per_request": acc_tok / (args.steps * max(Bl, 1)),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(launches * args.steps)}
     emit(line)
     if ws > 1:
         dist.destroy_process_group()
 
 
+# batch sizes a continuous-batching server captures CUDA graphs for (vLLM's
+# default capture sizes up to 256): the C4 trace pads B_t up to one of them
+GRAPH_BUCKETS = [1, 2, 4] + list(range(8, 257, 8))
+
+
+def load_cprefill(args):
+    """c_prefill(L_max, B) table for the bandit (Eq. 3): the B200 measurement of
+    scripts/measure_cprefill.py when present (profiles/r02_cprefill_b200.csv),
+    else PAPER Table 1 (RTX 4090, tests/golden/table1_cprefill.csv) x
+    --cprefill-scale.  Returns (len_buckets, batch_buckets, cost_ms, source)."""
+    import numpy as np
+    meas = os.path.join(ROOT, "profiles", "r02_cprefill_b200.csv")
+    if os.path.exists(meas) and not args.cprefill_table1:
+        path, scale, src = meas, 1.0, "B200-measured draft KV-reconstruction prefill (profiles/r02_cprefill_b200.csv)"
+    else:
+        path, scale = os.path.join(ROOT, "tests", "golden", "table1_cprefill.csv"), args.cprefill_scale
+        src = f"PAPER Table 1 (RTX 4090) x {scale}"
+    rows = [l.strip().split(",") for l in open(path) if l[0].isdigit()]
+    L = sorted({int(r[0]) for r in rows})
+    Bb = sorted({int(r[1]) for r in rows})
+    C = np.zeros((len(L), len(Bb)))
+    for r in rows:
+        C[L.index(int(r[0])), Bb.index(int(r[1]))] = float(r[2]) * scale
+    return L, Bb, C, src
+
+
 def bench_c4(args, ws, rank, local):
     """BASELINE configs[3]: Nightjar-driven trace.  B_t follows a synthetic QPS
-    ramp 5 -> 300 -> 5 (fig:trace1 shape); gamma_t = nj_select_gamma
-    (Algorithm 1 + Eq. 3, Table 1 c_prefill scaled by --cprefill-scale); every
-    step runs nj_verify on the first B_t requests of a pre-generated pool with
-    gamma_t drafts each, is timed with CUDA events, and feeds the realised
-    goodput sum(n_b + 1) / t_step back through nj_observe."""
+    ramp 5 -> 300 -> 5 over --trace-steps steps (fig:trace1 shape),
+    padded up to the server's CUDA-graph batch buckets; gamma_t =
+    nj_select_gamma(B_t, L_max) (Algorithm 1 + Eq. 3 with the c_prefill table
+    of load_cprefill); every step replays the CUDA graph of nj_verify for
+    (B_t, gamma_t) on the first B_t requests of a pre-generated pool, is timed
+    with CUDA events, and feeds the realised goodput sum(n_b + 1) / t_step back
+    through nj_observe.  Reported: accepted tokens/s over
+    the trace, and gamma histograms per B range split into exploration and
+    exploitation bins (Algorithm 1's bin type), whose exploitation means show
+    gamma* falling as load rises."""
     import numpy as np
     import torch
 
     from paper_2512_22420_b200 import Bandit, Verifier
     from synth.inputs import make_batch, make_weight, qps_ramp
 
+    if ws > 1 and rank != 0:
+        return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     BMAX, GMAX = 256, 5
     W = make_weight(V_Q, D_Q, args.seed, dev)
     pools = {g: make_batch(BMAX, g, V=V_Q, d=D_Q, seed=args.seed * 100 + g, device=dev, W=W) for g in range(GMAX + 1)}
     v = Verifier(D_Q, V_Q, max_batch=BMAX, gamma_max=GMAX, device=local)
-    tab = os.path.join(ROOT, "tests", "golden", "table1_cprefill.csv")
-    rows = [l.strip().split(",") for l in open(tab) if l[0].isdigit()]
-    L = sorted({int(r[0]) for r in rows})
-    Bb = sorted({int(r[1]) for r in rows})
-    C = np.zeros((len(L), len(Bb)))
-    for r in rows:
-        C[L.index(int(r[0])), Bb.index(int(r[1]))] = float(r[2]) * args.cprefill_scale
+    L, Bb, C, csrc = load_cprefill(args)
     bandit = Bandit(GMAX, BMAX, args.seed, L, Bb, C)
     trace = qps_ramp(args.trace_steps, seed=args.seed)
+    if args.c4_buckets == "graph":
+        trace = np.array([min(x for x in GRAPH_BUCKETS if x >= int(B)) for B in trace], np.int32)
     acc = torch.empty(BMAX, dtype=torch.int32, device=dev)
     nxt = torch.empty(BMAX, dtype=torch.int32, device=dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    lag, tok_tot, t_tot, pos_tot = 0, 0, 0.0, 0
-    hist = {}
-    sel_us = []
-    for t, B in enumerate(trace):
-        B = int(B)
-        t0 = time.perf_counter()
-        g = bandit.select(B, lag if bandit.last_gamma == 0 else 0)
-        sel_us.append((time.perf_counter() - t0) * 1e6)
+    acc_h = torch.empty(BMAX, dtype=torch.int32).pin_memory()
+    stream = torch.cuda.current_stream()
+    cap = torch.cuda.Stream()
+    graphs = {}
+
+    def launch(B, g):
         b = pools[g]
         n_rows, n_dr = B * (g + 1), B * g
         gam = np.full(B, g, np.int32)
-        e0.record()
-        v.verify(b.hidden[:n_rows], W, b.draft_tokens[:max(n_dr, 0)], b.draft_probs[:max(n_dr, 1)], gam,
+        v.verify(b.hidden[:n_rows], W, b.draft_tokens[:n_dr], b.draft_probs[:max(n_dr, 1)], gam,
                  b.uniforms[:n_rows], acc, nxt)
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
-        toks = int((acc[:B] + 1).sum().item())
-        bandit.observe(B, g, toks / (ms / 1e3))
-        lag = lag + 1 if g == 0 else 0
-        if t >= args.warmup:
-            tok_tot += toks
-            pos_tot += n_rows
-            t_tot += ms / 1e3
-            key = f"B{(B - 1) // 32 * 32 + 1}-{(B - 1) // 32 * 32 + 32}"
-            hist.setdefault(key, [0] * (GMAX + 1))[g] += 1
+
+    def graph_for(B, g):
+        key = (B, g)
+        if key not in graphs and not args.no_graph:
+            try:
+                cap.wait_stream(stream)
+                with torch.cuda.stream(cap):
+                    launch(B, g)
+                    cap.synchronize()
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr, stream=cap):
+                        launch(B, g)
+                stream.wait_stream(cap)
+                graphs[key] = gr
+            except Exception as e:   # pragma: no cover
+                print(f"[bench] c4 graph capture failed: {e}", file=sys.stderr)
+                graphs[key] = None
+        return graphs.get(key)
+
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    lag, tok_tot, t_tot, pos_tot = 0, 0, 0.0, 0
+    hist = {"explore": {}, "exploit": {}}
+    sel_us, step_ms = [], []
+    with ClockSampler(local) as clk:
+        for t, B in enumerate(trace):
+            B = int(B)
+            t0 = time.perf_counter()
+            g = bandit.select(B, lag if bandit.last_gamma == 0 else 0)
+            sel_us.append((time.perf_counter() - t0) * 1e6)
+            kind = "explore" if bandit.state(B)[4] == 1 else "exploit"
+            gr = graph_for(B, g)
+            e0.record(stream)
+            if gr is not None:
+                gr.replay()
+            else:
+                launch(B, g)
+            e1.record(stream)
+            acc_h[:B].copy_(acc[:B], non_blocking=True)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            toks = int((acc_h[:B] + 1).sum())
+            bandit.observe(B, g, toks / (ms / 1e3))
+            lag = lag + 1 if g == 0 else 0
+            if t >= args.warmup:
+                tok_tot += toks
+                pos_tot += B * (g + 1)
+                t_tot += ms / 1e3
+                step_ms.append(ms)
+                key = f"B{(B - 1) // 32 * 32 + 1}-{(B - 1) // 32 * 32 + 32}"
+                hist[kind].setdefault(key, [0] * (GMAX + 1))[g] += 1
+    keys = sorted(set(hist["explore"]) | set(hist["exploit"]), key=lambda k: int(k[1:].split("-")[0]))
+    mean_exploit = {k: (float(np.dot(hist["exploit"][k], np.arange(GMAX + 1)) / sum(hist["exploit"][k]))
+                        if k in hist["exploit"] and sum(hist["exploit"][k]) else None) for k in keys}
+    # the bandit's learned greedy choice per graph bucket at the end of the trace (no switch cost)
+    greedy = {}
+    for Bq in GRAPH_BUCKETS:
+        sc = [bandit.score(Bq, 1, gg) for gg in range(GMAX + 1)]
+        if not all(np.isnan(sc)):
+            greedy[str(Bq)] = int(np.nanargmin(sc))
+    nsteps = len(step_ms)
     line = {"metric": "accepted tokens/s (bandit-driven trace)", "value": tok_tot / t_tot, "unit": "tokens/s",
-            "n_gpus": 1, "steps": len(trace) - args.warmup, "warmup": args.warmup,
-            "ms_per_step": t_tot / (len(trace) - args.warmup) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "n_gpus": 1, "steps": nsteps, "warmup": args.warmup,
+            "ms_per_step": t_tot / nsteps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "qwen7b_c4_nightjar_trace", "qps": "5->300->5 linear ramp",
-                       "batch_max": BMAX, "gamma_max": GMAX, "cprefill_scale": args.cprefill_scale},
+                       "trace_steps": int(len(trace)), "batch_buckets": args.c4_buckets,
+                       "batch_max": BMAX, "gamma_max": GMAX, "cprefill": csrc,
+                       "launch": "CUDA graph replay per (B, gamma)" if not args.no_graph else "eager launches"},
             "verified_positions_per_s": pos_tot / t_tot,
-            "gamma_histogram_per_B": hist,
+            "step_ms": step_stats(step_ms),
+            "gamma_histogram_per_B": {"exploit": hist["exploit"], "explore": hist["explore"]},
+            "mean_gamma_exploit_per_B": mean_exploit,
+            "greedy_gamma_at_end_per_B": greedy,
             "select_gamma_us_median": statistics.median(sel_us),
+            "graphs_captured": len(graphs), "clocks": clk.summary(),
             "bandit_snapshot_batches": len(bandit.snapshot()["batches"])}
     emit(line)
 
@@ -500,7 +654,13 @@ def bench_c5(args, ws, rank, local):
     vb, ve = shard_range(V_Q, ws, rank)
     Wf = make_weight(V_Q, D_Q, args.seed, dev)
     b = make_batch(B, g, V=V_Q, d=D_Q, seed=args.seed, device=dev, W=Wf)
-    W = Wf[vb:ve].contiguous()
+    # rotating copies of the rank's W shard so consecutive steps never find it in
+    # L2 (126 MB): at G = 8 a shard is 136 MB, so one copy would be largely
+    # L2-resident from the previous step
+    L2_BYTES = 126 * 2 ** 20
+    nW = 1 if (ve - vb) * D_Q * 2 > 2 * L2_BYTES else 3
+    Ws = [Wf[vb:ve].contiguous() for _ in range(nW)]
+    W = Ws[0]
     del Wf
     torch.cuda.empty_cache()
     v = Verifier(D_Q, V_Q, max_batch=B, gamma_max=g, device=local, v_begin=vb, v_end=ve, nccl_comm=comm.handle)
@@ -509,55 +669,44 @@ def bench_c5(args, ws, rank, local):
     nxt = torch.empty(B, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step():
-        v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+    def step(i=0):
+        v.verify(b.hidden, Ws[i % nW], b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
 
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize()
     v.set_option(NJ_OPT_PROFILE, 1)
     v.kernel_time(reset=True)
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms_eager, per_eager, clk = timed_steps(step, args.steps, stream, local)
+    ms, per = ms_eager, per_eager
     kms, kn = v.kernel_time(reset=True)
     v.set_option(NJ_OPT_PROFILE, 0)
-    ms_eager = ms
     graph_ok = False
     if not args.no_graph:
-        # one step (kernels + NCCL collectives on the stream) replayed from a CUDA graph
+        # one step (kernels + NCCL collectives on the stream) per W copy, replayed from CUDA graphs
         try:
             cap = torch.cuda.Stream()
             cap.wait_stream(stream)
+            graphs = []
             with torch.cuda.stream(cap):
                 step()
                 cap.synchronize()
-                graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(graph, stream=cap):
-                    step()
+                for j in range(nW):
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graph, stream=cap):
+                        step(j)
+                    graphs.append(graph)
             stream.wait_stream(cap)
-            for _ in range(args.warmup):
-                graph.replay()
+            for i in range(args.warmup):
+                graphs[i % nW].replay()
             torch.cuda.synchronize()
             if ws > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with ClockSampler(local) as clk:
-                g0.record(stream)
-                for _ in range(args.steps):
-                    graph.replay()
-                g1.record(stream)
-                torch.cuda.synchronize()
-            ms = g0.elapsed_time(g1)
+            ms, per, clk = timed_steps(lambda i: graphs[i % nW].replay(), args.steps, stream, local)
             graph_ok = True
         except Exception as e:
             print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
@@ -569,7 +718,8 @@ def bench_c5(args, ws, rank, local):
     roof = {"kernel": "k_gemm_big<stats> (K-A, draft rows, this rank's shard)", "bound": "tensor",
             "achieved": flops / (kern_ms / 1e3) / 1e12, "peak": tf_burst, "unit": "TFLOP/s",
             "frac": flops / (kern_ms / 1e3) / 1e12 / tf_burst, "algorithmic_flops_per_launch": flops,
-            "peak_source": peak_src, "kernel_ms_avg": kern_ms, "kernel_share_of_step": kms / ms, "traffic": None}
+            "peak_source": peak_src, "kernel_ms_avg": kern_ms, "kernel_share_of_step": kms / ms_eager,
+            "traffic": None}
     # end to end through nj_verify_host (pinned host inputs, copies inside the timed region)
     pin = lambda t: t.cpu().pin_memory()
     hh, th, qh, uh = pin(b.hidden), pin(b.draft_tokens), pin(b.draft_probs), pin(b.uniforms)
@@ -608,10 +758,12 @@ def bench_c5(args, ws, rank, local):
                        "V": V_Q, "V_per_rank_max": max(shard_range(V_Q, ws, r)[1] - shard_range(V_Q, ws, r)[0]
                                                       for r in range(ws)),
                        "parallelism": f"vocab-sharded x{ws} (NCCL allgather x2 + allreduce-MAX per step)",
-                       "l2": "inputs larger than L2 at G <= 4; W shard streamed every step",
+                       "l2": (f"W shard {(ve - vb) * D_Q * 2 / 2 ** 20:.0f} MiB x {nW} rotating copies "
+                              "(> L2 between reuses); streamed from HBM every step"),
                        "launch": "CUDA graph replay per step" if graph_ok else "eager launches",
                        "ms_per_step_eager": ms_eager / args.steps},
             "accepted_tokens_per_s": toks * args.steps / (t_max / 1e3),
+            "step_ms": step_stats(per), "step_ms_eager": step_stats(per_eager),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": int(launches * args.steps)}
     emit(line)
@@ -968,12 +1120,22 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="C3 grid: one JSON line per (B, gamma) point")
     ap.add_argument("--sweep-B", default="1,2,4,8,16,32,48,64,96,128,192,256")
     ap.add_argument("--sweep-gamma", default="0,1,2,3,4,5,mixed:5")
-    ap.add_argument("--trace-steps", type=int, default=1200)
+    ap.add_argument("--trace-steps", type=int, default=4000)
+    ap.add_argument("--c4-buckets", default="graph", choices=["graph", "none"],
+                    help="C4: pad B_t up to the CUDA-graph batch buckets (graph) or not (none)")
+    ap.add_argument("--cprefill-table1", action="store_true",
+                    help="C4: use PAPER Table 1 x --cprefill-scale even if a B200 measurement exists")
     ap.add_argument("--cprefill-scale", type=float, default=0.01)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = every rank its own batch; strong = one global batch split by rows")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     _claim_stdout()
     ws, rank, local = dist_setup()
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.sweep:
         bench_sweep(args, ws, rank, local)
         return
@@ -996,4 +1158,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -38,7 +38,9 @@ static double bf16_to_f64(uint16_t b) {
 
 static void set_threads(int nthreads) {
 #ifdef _OPENMP
-    if (nthreads > 0) omp_set_num_threads(nthreads);
+    static int dflt = 0;   /* the process default, restored when nthreads <= 0 */
+    if (!dflt) dflt = omp_get_max_threads();
+    omp_set_num_threads(nthreads > 0 ? nthreads : dflt);
 #else
     (void)nthreads;
 #endif
@@ -46,6 +48,7 @@ static void set_threads(int nthreads) {
 
 int oracle_max_threads(void) {
 #ifdef _OPENMP
+    set_threads(0);
     return omp_get_max_threads();
 #else
     return 1;
