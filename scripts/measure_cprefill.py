@@ -8,7 +8,8 @@ vocabulary 151936; random bf16 weights, no checkpoint exists here).
 
 This is a MEASUREMENT feeding the host bandit's lookup table (nj_bandit_create
 cost_ms), not part of the verification hot path: it uses plain torch ops
-(cuBLAS GEMMs, SDPA attention) under a CUDA graph, median of 20 replays.
+(cuBLAS GEMMs, SDPA attention with GQA reading the KV cache in place) under a
+CUDA graph, median of 20 replays.
 
     python scripts/measure_cprefill.py [--ctx 1024] [--out profiles/r02_cprefill_b200.csv]
 
@@ -43,8 +44,10 @@ def rms(x, w):
     return (x.float() * torch.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-6)).to(x.dtype) * w
 
 
-def prefill(x, kcache, vcache, layers, lm, mask):
-    """x [B, L, D] new tokens; kcache/vcache per layer [B, HKV, ctx, HD]; returns
+def prefill(x, kcache, vcache, layers, lm, mask, ctx):
+    """x [B, L, D] new tokens; kcache/vcache per layer [B, HKV, ctx + L, HD] (the
+    first ctx positions already filled); the new keys / values are written in
+    place and attention reads the cache directly (GQA, no KV copies); returns
     the last position's logits (the draft then proposes from it)."""
     B, L, _ = x.shape
     for li, p in enumerate(layers):
@@ -52,11 +55,10 @@ def prefill(x, kcache, vcache, layers, lm, mask):
         qkv = h @ p["wqkv"]
         q, k, v = qkv.split([HQ * HD, HKV * HD, HKV * HD], dim=-1)
         q = q.view(B, L, HQ, HD).transpose(1, 2)
-        k = torch.cat([kcache[li], k.view(B, L, HKV, HD).transpose(1, 2)], dim=2)
-        v = torch.cat([vcache[li], v.view(B, L, HKV, HD).transpose(1, 2)], dim=2)
-        k = k.repeat_interleave(HQ // HKV, dim=1)
-        v = v.repeat_interleave(HQ // HKV, dim=1)
-        a = torch.nn.functional.scaled_dot_product_attention(q, k, v, attn_mask=mask)
+        kcache[li][:, :, ctx:] = k.view(B, L, HKV, HD).transpose(1, 2)
+        vcache[li][:, :, ctx:] = v.view(B, L, HKV, HD).transpose(1, 2)
+        a = torch.nn.functional.scaled_dot_product_attention(q, kcache[li], vcache[li], attn_mask=mask,
+                                                             enable_gqa=True)
         x = x + a.transpose(1, 2).reshape(B, L, HQ * HD) @ p["wo"]
         h = rms(x, p["n2"])
         gu = h @ p["wgu"]
@@ -67,18 +69,19 @@ def prefill(x, kcache, vcache, layers, lm, mask):
 
 def measure(L, B, ctx, layers, lm, dev, reps=20):
     x = (torch.randn(B, L, D, device=dev) * 0.5).to(torch.bfloat16)
-    kc = [(torch.randn(B, HKV, ctx, HD, device=dev) * 0.5).to(torch.bfloat16) for _ in range(LAYERS)]
-    vc = [(torch.randn(B, HKV, ctx, HD, device=dev) * 0.5).to(torch.bfloat16) for _ in range(LAYERS)]
-    # causal over the new tokens, full over the cached context (bottom-right aligned)
-    mask = torch.ones(L, ctx + L, dtype=torch.bool, device=dev).tril(diagonal=ctx)
+    kc = [(torch.randn(B, HKV, ctx + L, HD, device=dev) * 0.5).to(torch.bfloat16) for _ in range(LAYERS)]
+    vc = [(torch.randn(B, HKV, ctx + L, HD, device=dev) * 0.5).to(torch.bfloat16) for _ in range(LAYERS)]
+    # causal over the new tokens, full over the cached context (bottom-right aligned);
+    # one new token attends to everything (no mask)
+    mask = None if L == 1 else torch.ones(L, ctx + L, dtype=torch.bool, device=dev).tril(diagonal=ctx)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
         for _ in range(2):
-            prefill(x, kc, vc, layers, lm, mask)
+            prefill(x, kc, vc, layers, lm, mask, ctx)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            prefill(x, kc, vc, layers, lm, mask)
+            prefill(x, kc, vc, layers, lm, mask, ctx)
     torch.cuda.current_stream().wait_stream(s)
     for _ in range(3):
         g.replay()
