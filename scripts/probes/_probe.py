@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 CSRC = os.path.join(ROOT, "paper_2512_22420_b200", "csrc")
 LIB = os.path.join(HERE, "libnj_probe.so")
-SRC = ["nj_probe.cu", "nj_probe_ks.cuh", "nj_stream_test.cuh", "nj_mma_probe.cuh"]
+SRC = ["nj_probe.cu", "nj_probe_ks.cuh", "nj_stream_test.cuh", "nj_mma_probe.cuh", "nj_tmem_bw.cuh"]
 _lib = None
 
 
@@ -36,7 +36,8 @@ def load():
         lib.njp_logits_ks.argtypes = [P, P, I32, I32, P, I32, P, I64, I32]
         lib.njp_stream_test.argtypes = [P, P, I32, I32, I32, I32, I32, P, I32, I32]
         lib.njp_mma_probe.argtypes = [P, I32, I32, I32, P]
-        for f in (lib.njp_logits_ks, lib.njp_stream_test, lib.njp_mma_probe):
+        lib.njp_tmem_bw.argtypes = [P, I32, I32, I32, I32, I32, P]
+        for f in (lib.njp_logits_ks, lib.njp_stream_test, lib.njp_mma_probe, lib.njp_tmem_bw):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -68,3 +69,8 @@ def stream_test(W, mode: int, group: int, nstages: int, H=None, hrows: int = 0, 
 
 def mma_probe(n: int, iters: int, mode: int, out):
     _ok(load().njp_mma_probe(_st(), n, iters, mode, out.data_ptr()), "njp_mma_probe")
+
+
+def tmem_bw(nwarps: int, x: int, inflight: int, cols: int, rounds: int, out):
+    """TMEM read probe: out [2 * SMs] int64 (cycles, checksum) per CTA."""
+    _ok(load().njp_tmem_bw(_st(), nwarps, x, inflight, cols, rounds, out.data_ptr()), "njp_tmem_bw")

@@ -18,6 +18,7 @@
 #include "nj_mma_probe.cuh"
 #include "nj_probe_ks.cuh"
 #include "nj_stream_test.cuh"
+#include "nj_tmem_bw.cuh"
 
 using namespace nj;
 
@@ -113,6 +114,28 @@ int njp_mma_probe(void* stream, int32_t n, int32_t iters, int32_t mode, int64_t*
         return 3;
     k_mma_probe<<<num_sms(), 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
         n, iters, mode, reinterpret_cast<long long*>(cycles_out));
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
+// TMEM read bandwidth: one CTA per SM, nwarps (4..16) warps each reading its
+// slice of `cols` (<= 512) columns of its lane quadrant `rounds` times with
+// 32x32b.x{16,32} loads, `inflight` (1, 2, 4) per tcgen05.wait::ld.
+// out[2 * SMs] = (cycles, checksum) per CTA.
+int njp_tmem_bw(void* stream, int32_t nwarps, int32_t x, int32_t inflight, int32_t cols, int32_t rounds,
+                int64_t* out) {
+    if (!out || nwarps < 4 || nwarps > 16 || nwarps % 4 || cols < 16 || cols > 512) return 1;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    long long* o = reinterpret_cast<long long*>(out);
+    const dim3 g(num_sms()), b(32 * nwarps);
+#define L(X, N) k_tmem_bw<X, N><<<g, b, 0, st>>>(rounds, cols, o)
+    if (x == 16 && inflight == 1) L(16, 1);
+    else if (x == 16 && inflight == 2) L(16, 2);
+    else if (x == 16 && inflight == 4) L(16, 4);
+    else if (x == 32 && inflight == 1) L(32, 1);
+    else if (x == 32 && inflight == 2) L(32, 2);
+    else if (x == 32 && inflight == 4) L(32, 4);
+    else return 1;
+#undef L
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
