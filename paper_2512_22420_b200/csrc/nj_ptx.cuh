@@ -60,22 +60,28 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void watchdog(long long t0) {
     if (clock64() - t0 > NJ_WATCHDOG_CYCLES) __trap();
 }
+__device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    return done != 0;
+}
+// The poll loop is a bare try_wait (a hardware-suspending wait) + branch: the
+// watchdog's clock is read once per 1024 polls, not per poll, so waiting warps
+// spend almost no issue slots (they share sub-partitions with the pipeline's
+// single-thread issuers).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
-    uint32_t done = 0;
-    long long t0 = 0;
-    int spins = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.b32 %0, 1, 0, p;\n\t}"
-            : "=r"(done) : "r"(a), "r"(parity) : "memory");
-        if (!done) {
-            if (spins == 0) t0 = clock64();
-            if ((++spins & 1023) == 0) watchdog(t0);
-        }
-    } while (!done);
+    if (mbar_try_wait(a, parity)) return;
+    const long long t0 = clock64();
+    while (true) {
+        for (int i = 0; i < 1024; ++i)
+            if (mbar_try_wait(a, parity)) return;
+        watchdog(t0);
+    }
 }
 
 // Wait with a nanosleep backoff between polls: for warps that wait long and
@@ -136,7 +142,9 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 }
 // fp32 store with an L2 eviction-priority policy
 __device__ __forceinline__ void st_evict_last(float* ptr, float v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol) : "memory");
+    // no "memory" clobber: nothing in the issuing kernel reads these stores back,
+    // and a clobber would force every cached value to be reloaded per store
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol));
 }
 // 2-D tiled load: box at (c0 = inner / K element, c1 = row) -> smem, completes
 // bytes on `bar`.
@@ -415,6 +423,115 @@ __device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n\ttcgen05.wait::ld.sync.aligned;"
                  : "=r"(r) : "r"(taddr) : "memory");
     return __uint_as_float(r);
+}
+
+__device__ __forceinline__ bool mbar_test_wait(uint32_t a, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(a), "r"(parity) : "memory");
+    return done != 0;
+}
+// Warp-uniform polling wait (test_wait never suspends the warp).
+__device__ __forceinline__ void mbar_wait_w_spin(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (__all_sync(0xffffffffu, mbar_test_wait(a, parity))) return;
+    const long long t0 = clock64();
+    while (true) {
+        for (int i = 0; i < 1024; ++i)
+            if (__all_sync(0xffffffffu, mbar_test_wait(a, parity))) return;
+        watchdog(t0);
+    }
+}
+// Warp-uniform wait: every lane polls, the loop exits on a warp vote, so the
+// control flow after it stays provably uniform (the issue loops below keep
+// their state in uniform registers).
+__device__ __forceinline__ void mbar_wait_w(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    if (__all_sync(0xffffffffu, mbar_try_wait(a, parity))) return;
+    const long long t0 = clock64();
+    while (true) {
+        for (int i = 0; i < 1024; ++i)
+            if (__all_sync(0xffffffffu, mbar_try_wait(a, parity))) return;
+        watchdog(t0);
+    }
+}
+
+// ---------------------------------------- warp-converged single-issue forms
+// Called by ALL 32 lanes of a warp in convergent control flow; one elected lane
+// performs the operation.  Convergent issue lets ptxas keep descriptors, tile
+// coordinates and barrier addresses in uniform registers (UIADD3 / UMOV) and
+// emit bare UTCHMMA / UTMALDG, instead of the per-instruction ELECT + 7x
+// R2UR.BROADCAST + BRA.U.ANY waterfall a lane-0-only loop gets.
+__device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_bf16_cg2_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+        ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc2_w(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}"
+        ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_w(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1,
+                                              uint64_t policy) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;\n\t}"
+        ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1),
+          "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cg2_w(void* smem_dst, const void* tmap, uint32_t mbar_cluster, int32_t c0,
+                                                  int32_t c1, uint64_t policy) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;\n\t}"
+        ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1),
+          "r"(mbar_cluster), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_2d_w(const void* tmap, int32_t c0, int32_t c1) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n\t}"
+        ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1) : "memory");
 }
 
 // ------------------------------------------------------------------ grid sync
