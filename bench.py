@@ -320,6 +320,8 @@ def bench_nj(args, ws, rank, local):
     gmax = max([int(b.gamma.max()) for b in batches if b.B] + [1])
     v = Verifier(D_Q, V_Q, max_batch=max(Bl, 1), gamma_max=max(gmax, 1), device=local)
     v.set_option(NJ_OPT_PATH, path)
+    if args.temperature != 1.0:
+        v.set_temperature(args.temperature)   # target softmax(l / T)
     p_used, launches = v.plan(batches[0].gamma) if Bl else (0, 0)
     acc = [torch.empty(max(Bl, 1), dtype=torch.int32, device=dev) for _ in range(nb)]
     nxt = [torch.empty(max(Bl, 1), dtype=torch.int32, device=dev) for _ in range(nb)]
@@ -461,7 +463,8 @@ def bench_nj(args, ws, rank, local):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"qwen7b_{args.config}", "B": B, "gamma": gamma, "N_per_step": N_global,
+            "config": {"workload": f"qwen7b_{args.config}" + (f"_T{args.temperature:g}" if args.temperature != 1.0 else ""),
+                       "temperature": args.temperature, "B": B, "gamma": gamma, "N_per_step": N_global,
                        "N_per_rank_rank0": N, "d": D_Q, "V": V_Q, "global_batch": B * (1 if strong else ws),
                        "path": PATH_NAMES[p_used],
                        "parallelism": (f"request-sharded x{ws}, " + ("one global batch split by rows"
@@ -1133,6 +1136,7 @@ def main():
     ap.add_argument("--cprefill-table1", action="store_true",
                     help="C4: use PAPER Table 1 x --cprefill-scale even if a B200 measurement exists")
     ap.add_argument("--cprefill-scale", type=float, default=0.01)
+    ap.add_argument("--temperature", type=float, default=1.0, help="target temperature (nj_set_temperature)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = every rank its own batch; strong = one global batch split by rows")
     args = ap.parse_args()

@@ -185,6 +185,19 @@ typedef enum {
 
 nj_status nj_set_option(nj_ctx* ctx, nj_option opt, int64_t value);
 
+/* Target temperature (verification variants; the paper
+ * is silent on sampling settings, R1 reads it as T = 1): every
+ * subsequent nj_verify of ctx uses p_j = softmax(l_j / T) as the target
+ * distribution in place of softmax(l_j) -- acceptance u_i·q_i(x_i) < p_i(x_i),
+ * residual max(0, p_n − q_n), bonus p_gamma -- and nj_propose draws from
+ * softmax(l / T).  The kernels scale the accumulated fp32 logits by fp32(1/T)
+ * before the softmax statistics (the fp64 fallback by 1/T in fp64); the
+ * acceptance certificate widens by max(1, 1/T).  draft_probs are the draft's
+ * own (already tempered) q.  temperature in (0, 1e6]; default 1.  T -> 0 is
+ * nj_verify_greedy.  NJ_EINVAL otherwise.  Not applied by nj_lmhead_logits
+ * (raw logits) or nj_sample_from_logits (given logits). */
+nj_status nj_set_temperature(nj_ctx* ctx, double temperature);
+
 /* Device time of the dominant kernel (fused verify kernel, or the stats GEMM
  * of the two-pass path) accumulated since the last reset, measured with CUDA
  * events recorded on the launch stream (NJ_OPT_PROFILE must be on).

@@ -135,7 +135,7 @@ def logits_blas(hidden_bits, W_bits, rows=None, v_chunk: int = 16384, W64=None) 
 
 
 def verify(hidden_bits, W_bits, draft_tokens, draft_probs, gamma, uniforms,
-           tie_eps: float = TIE_EPS, nthreads: int = 0, gemm: str = "c") -> dict:
+           tie_eps: float = TIE_EPS, nthreads: int = 0, gemm: str = "c", temperature: float = 1.0) -> dict:
     """Full fp64 verification of a packed ragged batch (layout of include/nj.h).
 
     ``uniforms`` may be fp32 (converted exactly) or fp64 (brute force, tie
@@ -149,6 +149,9 @@ def verify(hidden_bits, W_bits, draft_tokens, draft_probs, gamma, uniforms,
     N = int(g.sum()) + g.shape[0]
     assert H.shape == (N, d), (H.shape, N, d)
     L = logits_blas(H, Wb) if gemm == "blas" else logits(H, Wb, nthreads=nthreads)
+    if temperature != 1.0:
+        # target at temperature T (R17): p = softmax(l / T)
+        L = L / float(temperature)
     return verify_from_logits(L, draft_tokens, draft_probs, gamma, uniforms, tie_eps=tie_eps, nthreads=nthreads)
 
 
@@ -229,17 +232,18 @@ def verify_greedy(hidden_bits, W_bits, draft_tokens, gamma, tie_gap: float = 1e-
     return {"accept_len": acc, "next_token": nxt, "argmax": a, "gap": gap, "tie": tie}
 
 
-def propose(hidden_bits, W_bits, uniforms, tie_eps: float = TIE_EPS, nthreads: int = 0) -> dict:
+def propose(hidden_bits, W_bits, uniforms, tie_eps: float = TIE_EPS, nthreads: int = 0,
+            temperature: float = 1.0) -> dict:
     """Draft-side proposal step (the
     draft proposes x ~ q): q_b = softmax(l_b) of the draft LM head and x_b the
     inverse-CDF draw of q_b with uniform u_b.  Written as the definition's two
     pinned pieces: the fp64 logits (step 1) and verification with gamma = 0,
     which draws from p_0 = softmax(l_0) (test_gamma0_is_inverse_cdf_of_p).
     Returns tokens, q (fp64 [B, V]), lse and the draw's tie mask."""
-    L = logits(hidden_bits, W_bits, nthreads=nthreads)
+    L = logits(hidden_bits, W_bits, nthreads=nthreads) / float(temperature)
     B, V = L.shape
-    r = verify(hidden_bits, W_bits, np.zeros(0, np.int32), np.zeros((0, V), np.float32),
-               np.zeros(B, np.int32), uniforms, tie_eps=tie_eps, nthreads=nthreads)
+    r = verify_from_logits(L, np.zeros(0, np.int32), np.zeros((0, V), np.float32), np.zeros(B, np.int32),
+                           uniforms, tie_eps=tie_eps, nthreads=nthreads)
     q = np.exp(L - r["lse"][:, None])
     return {"tokens": r["next_token"], "q": q, "lse": r["lse"], "tie": r["tie"]}
 

@@ -26,7 +26,8 @@ NJ_FLAG_FALLBACK, NJ_FLAG_ZERO_MASS, NJ_FLAG_CLAMP = 1, 2, 4
 
 # every symbol include/nj.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "nj_create", "nj_destroy", "nj_last_error", "nj_verify", "nj_verify_host", "nj_set_option", "nj_plan",
+    "nj_create", "nj_destroy", "nj_last_error", "nj_verify", "nj_verify_host", "nj_set_option", "nj_set_temperature",
+    "nj_plan",
     "nj_kernel_time",
     "nj_lmhead_logits", "nj_sample_from_logits", "nj_bandit_create", "nj_bandit_destroy", "nj_select_gamma",
     "nj_observe", "nj_exploitation_score", "nj_prefill_cost_ms", "nj_bandit_state", "nj_bandit_arm",
@@ -83,6 +84,7 @@ def load():
         "nj_verify": ([P, P, P, P, P, P, I64, P, P, I32, P, P, P], I32),
         "nj_verify_host": ([P, P, P, P, P, P, I64, P, P, I32, P, P], I32),
         "nj_set_option": ([P, I32, I64], I32),
+        "nj_set_temperature": ([P, D], I32),
         "nj_plan": ([P, P, I32, P, P], I32),
         "nj_kernel_time": ([P, P, P, I32], I32),
         "nj_lmhead_logits": ([P, P, P, P, P, I32, P, I64, I32], I32),
@@ -213,6 +215,10 @@ class Verifier:
 
     def set_option(self, opt: int, value: int):
         self._check(self._lib.nj_set_option(self._h, opt, int(value)))
+
+    def set_temperature(self, temperature: float):
+        """nj_set_temperature: target distribution softmax(l / T) for later calls."""
+        self._check(self._lib.nj_set_temperature(self._h, float(temperature)))
 
     def plan(self, gamma):
         g = np.ascontiguousarray(gamma, np.int32)
@@ -372,6 +378,12 @@ class ShardGroup:
             st = self._lib.nj_set_option(m, opt, int(value))
             if st != NJ_OK:
                 raise NJError(st, "nj_set_option")
+
+    def set_temperature(self, temperature: float):
+        for r in range(self.n):
+            st = self._lib.nj_set_temperature(self._lib.nj_group_member(self._h, r), float(temperature))
+            if st != NJ_OK:
+                raise NJError(st, "nj_set_temperature")
 
     def shards(self, W):
         """Views of a full [V, d] weight as the members' shards."""

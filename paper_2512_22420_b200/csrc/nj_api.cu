@@ -135,6 +135,8 @@ struct nj_ctx {
     int path_opt = NJ_PATH_AUTO;
     int certify = 1;
     int force_fb = 0;
+    double temperature = 1.0;   // target temperature T (nj_set_temperature); logits l / T
+    double inv_t = 1.0;
     int profile = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // recorded, not yet harvested
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free;
@@ -364,7 +366,8 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     // accuracy of the partials: restart every k-block -> 2e-6;
     // every 2 -> 4e-6; every 3-4 k-blocks (<= 16 MMAs) -> the k_gemm_big margin
     const int kspan = (fp.ngroups > 0 && fp.sacc) ? GK : fp.kpd;
-    fp.eps_acc = kspan == 1 ? c->eps_acc_fused : kspan == 2 ? 2.0f * c->eps_acc_fused : c->eps_acc;
+    fp.eps_acc = (kspan == 1 ? c->eps_acc_fused : kspan == 2 ? 2.0f * c->eps_acc_fused : c->eps_acc) *
+                 (float)std::max(1.0, c->inv_t);
     if (c->kn.phase_ts) {
         if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
         fp.phase_ts = c->phase_ts;
@@ -415,6 +418,7 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     if (R <= 0) return NJ_OK;
     GemmBigParams gp = in;
     gp.R = R;
+    if (gp.inv_t == 0.f) gp.inv_t = (float)c->inv_t;   // 0: the context's temperature
     const int CG = c->gemm_cg == 2 ? 2 : 1;
     // two epilogue teams (alternate items) need chunks of <= 128 columns: 2 teams x
     // 2 buffers x 128 TMEM columns
@@ -524,6 +528,7 @@ nj_status launch_mass(nj_ctx* c, cudaStream_t st, const MassParams& mp, int B, b
 FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const int32_t* tok, const float* q,
                    int64_t ldq, const float* u, int32_t* acc, int32_t* nxt, const nj_debug* dbg) {
     FbParams f{};
+    f.inv_t = c->inv_t;
     f.hidden = hidden;
     f.W = W;
     f.d = c->cfg.d;
@@ -726,7 +731,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         ap.accept_len = a.acc; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
         ap.fb_count = c->fb_count(); ap.fb_list = c->fb_list(); ap.req_flags = c->req_flags();
         ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
-        ap.certify = a.certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc;
+        ap.certify = a.certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc * (float)std::max(1.0, c->inv_t);
         ap.xr1 = c->xr1; ap.nranks = c->nranks; ap.xld = pl.G;
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, a.meta);
         NJ_LAUNCHED(c, "k_accept", st);
@@ -992,6 +997,15 @@ nj_status nj_set_option(nj_ctx* c, nj_option opt, int64_t v) {
     return set_err(c, NJ_EINVAL, "unknown option %d", (int)opt);
 }
 
+nj_status nj_set_temperature(nj_ctx* c, double temperature) {
+    if (!c) return NJ_EINVAL;
+    if (!(temperature > 0.0) || !(temperature <= 1e6))
+        return set_err(c, NJ_EINVAL, "temperature %g outside (0, 1e6] (T -> 0 is nj_verify_greedy)", temperature);
+    c->temperature = temperature;
+    c->inv_t = 1.0 / temperature;
+    return NJ_OK;
+}
+
 nj_status nj_debug_phase_times(nj_ctx* c, unsigned long long* host_out, int32_t n) {
     if (!c || !c->phase_ts) return NJ_EINVAL;
     NJ_CUDA(c, cudaMemcpy(host_out, c->phase_ts, sizeof(unsigned long long) * std::min(n, 16 * 1024), cudaMemcpyDeviceToHost));
@@ -1076,7 +1090,8 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         fp.dbg_lse = dbg ? dbg->lse : nullptr; fp.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
         fp.dbg_mass = dbg ? dbg->mass : nullptr; fp.dbg_flags = dbg ? dbg->flags : nullptr;
         fp.certify = certify; fp.force_fallback = c->force_fb;
-        fp.eps_acc = c->eps_acc_fused; fp.eps_draw = c->eps_draw_fused;
+        fp.eps_acc = c->eps_acc_fused * (float)std::max(1.0, c->inv_t); fp.eps_draw = c->eps_draw_fused;
+        fp.inv_t = c->inv_t;
         for (int b = 0; b <= pl.B; ++b) fp.row_off[b] = pl.row_off[b];
         if (pl.npad == 16) s = launch_fused<16>(c, st, pl, tmH, fp);
         else if (pl.npad == 32) s = launch_fused<32>(c, st, pl, tmH, fp);
@@ -1109,7 +1124,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         ap.accept_len = accept_len; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
         ap.fb_count = c->fb_count(); ap.fb_list = c->fb_list(); ap.req_flags = c->req_flags();
         ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
-        ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc;
+        ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc * (float)std::max(1.0, c->inv_t);
         ap.staged = 1; ap.s_row = c->s_row;
         k_lse_rows<<<(pl.N + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.N, c->row_lse);
         NJ_LAUNCHED(c, "k_lse_rows", st);
@@ -1164,7 +1179,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         ap.accept_len = accept_len; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
         ap.fb_count = c->fb_count(); ap.fb_list = c->fb_list(); ap.req_flags = c->req_flags();
         ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
-        ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc_ka;
+        ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc_ka * (float)std::max(1.0, c->inv_t);
         ap.lse_sample_from_c = 1;
         if (pl.G > 0) {
             k_lse_rows<<<(pl.G + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.G, c->row_lse);
@@ -1364,6 +1379,7 @@ nj_status nj_lmhead_logits(nj_ctx* c, void* stream, const uint16_t* hidden, cons
     gp.part_m = c->part_m;
     gp.part_s = c->part_s;
     gp.ks = ks;
+    gp.inv_t = 1.f;   // raw logits (no temperature)
     int grid = c->grid;
     return launch_lmhead<true, true, false>(c, st, c->hd, n_rows, gp, n_rows > kBigMaxT, &grid);
 }

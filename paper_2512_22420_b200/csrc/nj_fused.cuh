@@ -405,6 +405,10 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
             }
             const bool valid = vr < min(kTileV, rows - t * kTileV);
             const int xl = r0 + t * kTileV + vr;
+            if (p.inv_t != 1.0) {   // temperature: the target distribution is softmax(l / T)
+#pragma unroll
+                for (int j = 0; j < NC; ++j) acc[j] *= p.inv_t;
+            }
             float f[NC];
 #pragma unroll
             for (int j = 0; j < NC; ++j) f[j] = (float)acc[j];

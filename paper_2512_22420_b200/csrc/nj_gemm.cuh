@@ -85,6 +85,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // W is streamed from HBM exactly once; nothing of size V*N is written.
 // ---------------------------------------------------------------------------
 struct FusedParams {
+    double inv_t;                // 1 / temperature: target logits l / T (include/nj.h nj_set_temperature)
     int32_t B, N, G;
     int32_t V_local, v_begin, U, num_kb, nstages;
     int32_t nbuf, scratch_col;   // scratch accumulators: nbuf x NPAD columns at scratch_col

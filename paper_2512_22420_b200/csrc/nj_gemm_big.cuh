@@ -47,6 +47,7 @@ constexpr int kBigMaxRowG = 512;
 constexpr int kBigMaxBuf = 8;                          // accumulator buffers (512 TMEM columns / chunk)                       // staged path: rows mapped to draft indices
 
 struct GemmBigParams {
+    float inv_t;                         // 1 / temperature applied to the logits (0 or 1: none)
     int32_t R, nchunks, chunk;           // rows, chunks, rows per chunk (multiple of 16, <= 256)
     int32_t V_local, U, num_kb, nstages, v_begin;
     int32_t gk;                          // k-blocks per TMA ring stage (1, 2 or 4)
@@ -406,6 +407,10 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                     if (CG == 2) mbar_arrive_cluster(aempty_cl[buf]);
                     else mbar_arrive(&aempty[buf]);
                 }
+            }
+            if (p.inv_t != 0.f && p.inv_t != 1.f) {   // temperature: logits l / T
+#pragma unroll
+                for (int j = 0; j < kBigNC; ++j) acc[j] *= p.inv_t;
             }
             if (p.dbg & 8) continue;   // probe: no per-item output work
             const bool tsi = p.ts && cta == 0 && warp == 0 && lane == 0 && it < 500;

@@ -718,6 +718,7 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
 // empty queue costs one tiny launch each.
 // ---------------------------------------------------------------------------
 struct FbParams {
+    double inv_t;          // 1 / temperature (fp64 logits l / T); 0 taken as 1
     const uint16_t* hidden;
     const uint16_t* W;
     int32_t d, V_local, v_begin;
@@ -771,6 +772,7 @@ __device__ __forceinline__ void fb_logits_body(const FbParams& p, const ReqMeta&
                     for (int e = 0; e < 8; ++e) acc = fma((double)bf16f(w16[e]), (double)bf16f(h16[e]), acc);
                 }
                 acc = warp_sum_d(acc);
+                if (p.inv_t != 0.0 && p.inv_t != 1.0) acc *= p.inv_t;
                 if (lane == 0) p.fb_logits[(int64_t)j * p.V_local + x] = acc;
             }
         }

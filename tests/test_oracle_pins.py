@@ -422,3 +422,37 @@ def test_logits_blas_matches_c_loops():
     assert np.max(np.abs(a - c)) <= 1e-12 * np.max(np.abs(a))
     d = oracle.logits_blas(n["hidden_bits"], n["W_bits"], W64=oracle.weight_f64(n["W_bits"]))
     assert np.max(np.abs(a - d)) <= 1e-12 * np.max(np.abs(a))
+
+
+# ------------------------------------------------------------------ temperature
+@pytest.mark.parametrize("T", [0.25, 2.0, 4.0])
+def test_temperature_power_of_two_equals_scaled_weights(T):
+    """Target at temperature T = 2^k is the T = 1 verification of W * 2^-k
+    (exact in bf16 and in the fp64 logits): identical decisions and lse, so
+    the temperature path is pinned to the (pinned) T = 1 path by an
+    independent route."""
+    import torch
+    b = make_batch(20, "mixed:5", V=500, d=32, seed=31)
+    n = _np(b)
+    Ws = (b.W.float() / T).to(torch.bfloat16)
+    assert torch.equal(Ws.float(), b.W.float() / T)
+    r_t = oracle.verify(n["hidden_bits"], n["W_bits"], n["draft_tokens"], n["draft_probs"], n["gamma"],
+                        n["uniforms"], temperature=T)
+    r_s = oracle.verify(n["hidden_bits"], oracle.bf16_bits(Ws), n["draft_tokens"], n["draft_probs"], n["gamma"],
+                        n["uniforms"])
+    assert (r_t["accept_len"] == r_s["accept_len"]).all() and (r_t["next_token"] == r_s["next_token"]).all()
+    assert np.array_equal(r_t["lse"], r_s["lse"])
+
+
+def test_high_temperature_draws_uniformly():
+    """T -> infinity: p -> uniform over V, so a gamma = 0 draw is token
+    floor(u * V) (the uniform inverse CDF) away from the interval ends."""
+    V = 50
+    b = make_batch(200, 0, V=V, d=16, seed=4)
+    n = _np(b)
+    r = oracle.verify(n["hidden_bits"], n["W_bits"], np.zeros(0, np.int32), np.zeros((0, V), np.float32),
+                      n["gamma"], n["uniforms"], temperature=1e9)
+    u = n["uniforms"].astype(np.float64)
+    far = np.abs(u * V - np.rint(u * V)) > 1e-4
+    assert far.sum() > 150
+    assert (r["next_token"][far] == np.floor(u[far] * V)).all()
