@@ -10,12 +10,16 @@ against the unsharded definition (oracle.verify):
   X1  per draft row:  (lse_r = log sum_{x in shard} e^{l(x)},  l(x_i) if owned)
       lse = log sum_r e^{lse_r}  (exact identity: the softmax normaliser is a
       sum over the partition of the vocabulary);
-  X2  per request:    (lse used, W_r = sum_{x in shard} w(x)) with w the residual
-      max(0, p_n - q_n) (global lse) or the bonus p_gamma with the rank-local
-      lse (so A_r = W_r e^{lse_r - M} are proportional to the shard masses);
+  X2  per request:    (lse used, W_r = sum_{x in shard} w(x), lse_r(n)) with w the
+      residual max(0, p_n - q_n) (global lse) or the bonus p_gamma with the
+      rank-local lse (so A_r = W_r e^{lse_r - M} are proportional to the shard
+      masses); lse_r(n) is the shard's log-sum-exp of row n;
+  R6  if sum_r W_r == 0 (zero residual mass everywhere) every rank switches to
+      p_n, whose shard masses are A_r = e^{lse_r(n) - M} (exact identity);
   X3  the inverse CDF over ascending ids = the rank whose exclusive prefix
       interval of A holds T = u * sum A, then the local inverse CDF at
-      (T - P_r) / e^{lse_r - M}; max-reduce of the token (-1 elsewhere).
+      (T - P_r) / e^{lse_r - M}; the tokens (-1 elsewhere) are gathered and
+      every rank takes the maximum.
 
 `gather(obj) -> list over ranks` and `allmax(np.ndarray) -> np.ndarray` are
 injected (a plain loop in one process, or torch.distributed).
@@ -75,38 +79,47 @@ def rank_step(rank, nranks, hidden_bits, W_bits, draft_tokens, draft_probs, gamm
             lse_used[b] = lse_d[g0 + n]
         g0 += gam[b]
     # ---- X2: local masses
-    wloc = []
-    x2 = np.zeros((B, 2))
+    wloc, ploc = [], []
+    x2 = np.zeros((B, 3))
     g0 = 0
     for b in range(B):
         row = L[ro[b] + n_out[b]]
+        lr = lse_of(row)
         if resid[b]:
             w = np.maximum(np.exp(row - lse_used[b]) - q_all[g0 + n_out[b], vb:ve], 0.0)
-            x2[b] = (lse_used[b], w.sum())
+            x2[b] = (lse_used[b], w.sum(), lr)
         else:
-            lr = lse_of(row)
             w = np.exp(row - lr)
-            x2[b] = (lr, w.sum())
+            x2[b] = (lr, w.sum(), lr)
         wloc.append(w)
+        ploc.append(np.exp(row - lr))
         g0 += gam[b]
     all2 = gather(x2)
-    # ---- X3: owner rank locates, max-reduce
+    # ---- X3: owner rank locates; tokens gathered, max over ranks taken locally
     tok = np.full(B, -1, np.int32)
     for b in range(B):
         lr = np.array([a[b, 0] for a in all2])
         Wr = np.array([a[b, 1] for a in all2])
+        ln = np.array([a[b, 2] for a in all2])
         pos = Wr > 0
-        M = lr[pos].max()
-        A = np.where(pos, Wr * np.exp(lr - M), 0.0)
+        if pos.any():
+            M = lr[pos].max()
+            A = np.where(pos, Wr * np.exp(lr - M), 0.0)
+            ev, wl = np.exp(lr - M), wloc[b]
+        else:                                   # R6 across shards: draw from p_n
+            M = ln.max()
+            A = np.exp(ln - M)
+            ev, wl = A, ploc[b]
         T = u[ro[b] + gam[b]] * A.sum()
         P = np.concatenate([[0.0], np.cumsum(A)])
         own = [r for r in range(nranks) if A[r] > 0 and P[r] <= T < P[r + 1]]
-        o = own[0] if own else int(np.nonzero(pos)[0][-1])
+        o = own[0] if own else int(np.nonzero(A > 0)[0][-1])
         if o != rank:
             continue
-        c = np.cumsum(wloc[b])
-        t = int(np.searchsorted(c, (T - P[o]) / np.exp(lr[o] - M), side="right")) if own else len(c)
+        c = np.cumsum(wl)
+        t = int(np.searchsorted(c, (T - P[o]) / ev[o], side="right")) if own else len(c)
         if t >= len(c):
-            t = int(np.nonzero(wloc[b] > 0)[0][-1])
+            t = int(np.nonzero(wl > 0)[0][-1])
         tok[b] = vb + t
-    return n_out, allmax(tok)
+    toks = gather(tok)
+    return n_out, np.max(np.stack(toks), axis=0).astype(np.int32)

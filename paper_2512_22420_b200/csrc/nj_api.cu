@@ -177,9 +177,9 @@ struct nj_ctx {
     void* ncomm = nullptr;
     bool in_group = false;
     bool sharded() const { return ncomm != nullptr || in_group; }
-    double *xs1 = nullptr, *xr1 = nullptr, *xs2 = nullptr, *xr2 = nullptr;
-    double *s4 = nullptr, *r4 = nullptr, *s5 = nullptr, *r5 = nullptr, *fblse = nullptr;
-    int32_t *x3 = nullptr, *x6 = nullptr, *fbn = nullptr;
+    double *xs1 = nullptr, *xr1 = nullptr, *xs2 = nullptr, *xr2 = nullptr, *xs3 = nullptr, *xr3 = nullptr;
+    double* fblse = nullptr;
+    int32_t *x6 = nullptr, *fbn = nullptr;
     // host-API staging (lazy)
     uint16_t* st_hidden = nullptr;
     int32_t* st_tok = nullptr;
@@ -630,21 +630,34 @@ void shard_range(int V, int n, int r, int& vb, int& ve) {
     ve = (int)std::min<int64_t>(V, (T * (r + 1) / n) * kTileV);
 }
 
+// Exchange buffers of the sharded step (nj_shard.cuh): per rank
+//   X2: [MB x 3 doubles (lse used, W_r, lse_r(n))] ++ [MB x slots x 2 doubles fallback stats]
+//   X3: [MB int32 tokens | MB int32 flags] ++ [MB x 2 doubles fallback masses]  (3 MB doubles)
+//   X4: [MB int32 tokens | MB int32 flags] (in-place MAX)
+int64_t x2_stride(const nj_ctx* c) {
+    const int64_t MB = c->cfg.max_batch, slots = c->cfg.gamma_max + 1;
+    return 3 * MB + 2 * MB * slots;
+}
+int64_t x3_stride(const nj_ctx* c) { return 3 * (int64_t)c->cfg.max_batch; }
+
 nj_status alloc_shard_ws(nj_ctx* c) {
-    const int MB = c->cfg.max_batch, slots = c->cfg.gamma_max + 1, n = c->nranks;
+    const int MB = c->cfg.max_batch, n = c->nranks;
     nj_status s;
     if ((s = alloc(c, &c->xs1, (size_t)c->Gmax * 2)) != NJ_OK) return s;
     if ((s = alloc(c, &c->xr1, (size_t)n * c->Gmax * 2)) != NJ_OK) return s;
-    if ((s = alloc(c, &c->xs2, (size_t)MB * 2)) != NJ_OK) return s;
-    if ((s = alloc(c, &c->xr2, (size_t)n * MB * 2)) != NJ_OK) return s;
-    if ((s = alloc(c, &c->x3, (size_t)2 * MB)) != NJ_OK) return s;
-    if ((s = alloc(c, &c->s4, (size_t)MB * slots * 2)) != NJ_OK) return s;
-    if ((s = alloc(c, &c->r4, (size_t)n * MB * slots * 2)) != NJ_OK) return s;
-    if ((s = alloc(c, &c->s5, (size_t)MB * 2)) != NJ_OK) return s;
-    if ((s = alloc(c, &c->r5, (size_t)n * MB * 2)) != NJ_OK) return s;
+    if ((s = alloc(c, &c->xs2, (size_t)x2_stride(c))) != NJ_OK) return s;
+    if ((s = alloc(c, &c->xr2, (size_t)n * x2_stride(c))) != NJ_OK) return s;
+    if ((s = alloc(c, &c->xs3, (size_t)x3_stride(c))) != NJ_OK) return s;
+    if ((s = alloc(c, &c->xr3, (size_t)n * x3_stride(c))) != NJ_OK) return s;
     if ((s = alloc(c, &c->x6, (size_t)2 * MB)) != NJ_OK) return s;
     if ((s = alloc(c, &c->fbn, (size_t)MB)) != NJ_OK) return s;
     if ((s = alloc(c, &c->fblse, (size_t)MB)) != NJ_OK) return s;
+    // the exchanges have fixed sizes (max_batch-based); entries a step does not
+    // fill (unused fallback slots) are exchanged too, so start them defined
+    if (cudaMemset(c->xs2, 0, sizeof(double) * (size_t)x2_stride(c)) != cudaSuccess ||
+        cudaMemset(c->xs3, 0, sizeof(double) * (size_t)x3_stride(c)) != cudaSuccess ||
+        cudaMemset(c->x6, 0, sizeof(int32_t) * 2 * (size_t)MB) != cudaSuccess)
+        return set_err(c, NJ_ECUDA, "cudaMemset failed (exchange buffers)");
     return NJ_OK;
 }
 
@@ -672,18 +685,16 @@ struct XSpec {
     int max_i32;   // 1: in-place allreduce-MAX over bytes/4 int32
 };
 
-int shard_nphases(const ShardCall& a) { return a.certify ? 8 : 4; }
+int shard_nphases(const ShardCall&) { return 5; }
 
-// exchange after phase ph (false: none)
+// exchange after phase ph (false: none): X1-X3 allgather, X4 allreduce-MAX
 bool shard_xchg(nj_ctx* c, const ShardCall& a, int ph, XSpec& x) {
-    const size_t MB = (size_t)c->cfg.max_batch, slots = (size_t)c->cfg.gamma_max + 1;
+    const size_t MB = (size_t)c->cfg.max_batch;
     switch (ph) {
         case 0: if (a.pl.G == 0) return false; x = {c->xs1, c->xr1, (size_t)a.pl.G * 16, 0}; return true;
-        case 1: x = {c->xs2, c->xr2, (size_t)a.pl.B * 16, 0}; return true;
-        case 2: x = {c->x3, c->x3, (size_t)a.pl.B * 8, 1}; return true;
-        case 4: x = {c->s4, c->r4, MB * slots * 16, 0}; return true;
-        case 5: x = {c->s5, c->r5, MB * 16, 0}; return true;
-        case 6: x = {c->x6, c->x6, MB * 8, 1}; return true;
+        case 1: x = {c->xs2, c->xr2, (size_t)x2_stride(c) * 8, 0}; return true;
+        case 2: x = {c->xs3, c->xr3, (size_t)x3_stride(c) * 8, 0}; return true;
+        case 3: x = {c->x6, c->x6, MB * 8, 1}; return true;
         default: return false;
     }
 }
@@ -691,9 +702,10 @@ bool shard_xchg(nj_ctx* c, const ShardCall& a, int ph, XSpec& x) {
 nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
     nj_status s = NJ_OK;
     const Plan& pl = a.pl;
-    const int MB = c->cfg.max_batch;
+    const int MB = c->cfg.max_batch, slots = c->cfg.gamma_max + 1;
     const nj_debug* dbg = a.dbg;
     FbParams f = fb_params(c, a.hidden, a.W, a.tok, a.q, a.ldq, a.u, a.acc, a.nxt, dbg);
+    int32_t* x3i = reinterpret_cast<int32_t*>(c->xs3);   // [MB tokens | MB flags] of this rank
     switch (ph) {
     case 0: {   // K-A on the shard, X1 pack
         NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)MB) * sizeof(int32_t), st));
@@ -723,7 +735,8 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         }
         return NJ_OK;
     }
-    case 1: {   // K-B (merged lse, identical on every rank), K-C on the shard, local masses, X2 pack
+    case 1: {   // K-B (merged lse, identical on every rank) + canonical fallback queue, K-C on the
+                // shard, local masses, X2 pack, and the queued requests' fp64 logits / local stats
         AcceptParams ap{};
         ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = a.gridA; ap.pld = c->pld; ap.dl = c->dl;
         ap.draft_tokens = a.tok; ap.q = a.q; ap.ldq = a.ldq; ap.u = a.u;
@@ -731,10 +744,13 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         ap.accept_len = a.acc; ap.s_resid = c->s_resid; ap.s_qrow = c->s_qrow; ap.s_lse = c->s_lse;
         ap.fb_count = c->fb_count(); ap.fb_list = c->fb_list(); ap.req_flags = c->req_flags();
         ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
-        ap.certify = a.certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc * (float)std::max(1.0, c->inv_t);
+        ap.certify = a.certify; ap.force_fallback = c->force_fb;
+        ap.eps_acc = c->eps_acc * (float)std::max(1.0, c->inv_t);
         ap.xr1 = c->xr1; ap.nranks = c->nranks; ap.xld = pl.G;
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, a.meta);
         NJ_LAUNCHED(c, "k_accept", st);
+        k_qcanon<<<1, 32, 0, st>>>(c->req_flags(), pl.B, c->fb_count(), c->fb_list(), c->force_fb);
+        NJ_LAUNCHED(c, "k_qcanon", st);
         a.gridC = c->grid;
         {
             GemmBigParams gp{};
@@ -749,44 +765,40 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         mp.nchunks = c->nchunks; mp.s_resid = c->s_resid; mp.s_qrow = c->s_qrow; mp.s_lse = c->s_lse;
         mp.part2_m = c->part2_m; mp.part2_s = c->part2_s; mp.grid2 = a.gridC; mp.pld2 = c->pld;
         mp.q = a.q; mp.ldq = a.ldq; mp.u = a.u; mp.stage_mode = 0; mp.cmass = c->cmass;
-        mp.accept_len = a.acc; mp.next_token = c->x3;
+        mp.accept_len = a.acc; mp.next_token = x3i;
         mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
         mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = nullptr;
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = a.certify; mp.eps_draw = c->eps_draw;
-        mp.xr2 = c->xr2; mp.nranks = c->nranks; mp.rank = c->rank; mp.xflags = c->x3 + pl.B;
+        mp.xr2 = c->xr2; mp.xstride = x2_stride(c); mp.nranks = c->nranks; mp.rank = c->rank;
+        mp.xflags = x3i + MB;
         if ((s = launch_mass(c, st, mp, pl.B, true)) != NJ_OK) return s;
         k_xpack2<<<(pl.B + 7) / 8, 256, 0, st>>>(mp, pl.B, c->xs2);
         NJ_LAUNCHED(c, "k_xpack2", st);
-        NJ_CUDA(c, cudaMemsetAsync(c->x3, 0, 2 * (size_t)pl.B * sizeof(int32_t), st));
-        return NJ_OK;
-    }
-    case 2:     // owner rank of each draw locates its token (others write -1)
-        k_locate<<<pl.B, kSampThreads, 0, st>>>(a.mp, a.meta);
-        NJ_LAUNCHED(c, "k_locate", st);
-        return NJ_OK;
-    case 3:
-        k_xfinish<<<1, 256, 0, st>>>(c->x3, pl.B, a.nxt, c->req_flags(), c->fb_count(), c->fb_list(),
-                                     dbg ? dbg->flags : nullptr, a.certify);
-        NJ_LAUNCHED(c, "k_xfinish", st);
-        return NJ_OK;
-    case 4:     // certified fallback (fp64): local logits + per-row local lse / owned draft logit
+        NJ_CUDA(c, cudaMemsetAsync(x3i + MB, 0, (size_t)MB * sizeof(int32_t), st));   // X3 flags
         k_fb_logits<<<c->num_sms * 2, 256, 0, st>>>(f, a.meta);
         NJ_LAUNCHED(c, "k_fb_logits", st);
-        k_fbx_stats<<<std::min(MB, c->num_sms), 256, 0, st>>>(f, a.meta, c->cfg.gamma_max + 1, c->s4);
+        k_fbx_stats<<<std::min(MB, c->num_sms), 256, 0, st>>>(f, a.meta, slots, c->xs2 + 3 * (size_t)MB);
         NJ_LAUNCHED(c, "k_fbx_stats", st);
         return NJ_OK;
-    case 5:
-        k_fbx_accept<<<std::min(MB, c->num_sms), 256, 0, st>>>(f, a.meta, c->r4, c->nranks, c->cfg.gamma_max + 1,
-                                                                MB, c->s5, c->fbn, c->fblse);
+    }
+    case 2:     // owner rank of each draw locates its token (others write -1); fp64 fallback
+                // acceptance + local masses of the queued requests (X2's second part)
+        k_locate<<<pl.B, kSampThreads, 0, st>>>(a.mp, a.meta);
+        NJ_LAUNCHED(c, "k_locate", st);
+        k_fbx_accept<<<std::min(MB, c->num_sms), 256, 0, st>>>(f, a.meta, c->xr2 + 3 * (size_t)MB, x2_stride(c),
+                                                                c->nranks, slots, c->xs3 + MB, c->fbn, c->fblse);
         NJ_LAUNCHED(c, "k_fbx_accept", st);
         return NJ_OK;
-    case 6:
-        k_fbx_locate<<<std::min(MB, c->num_sms), 256, 0, st>>>(f, a.meta, c->r5, c->nranks, c->rank, MB, c->fbn,
-                                                                c->fblse, c->x6);
+    case 3:     // outputs = max over the gathered X3 tokens; the fallback's owner-rank draw
+        k_xfinish2<<<1, 256, 0, st>>>(reinterpret_cast<const int32_t*>(c->xr3), c->nranks, 2 * x3_stride(c), MB,
+                                      pl.B, a.nxt, dbg ? dbg->flags : nullptr);
+        NJ_LAUNCHED(c, "k_xfinish2", st);
+        k_fbx_locate<<<std::min(MB, c->num_sms), 256, 0, st>>>(f, a.meta, c->xr3 + MB, x3_stride(c), c->nranks,
+                                                                c->rank, MB, c->fbn, c->fblse, c->x6);
         NJ_LAUNCHED(c, "k_fbx_locate", st);
         return NJ_OK;
-    case 7:
+    case 4:
         k_fbx_write<<<1, 256, 0, st>>>(f, c->fbn, c->x6, MB);
         NJ_LAUNCHED(c, "k_fbx_write", st);
         return NJ_OK;
@@ -1036,8 +1048,9 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
     if (s != NJ_OK) return s;
     int n = 0;
     if (c->sharded()) {
-        // gather+K-A+pack1, accept, K-C, mass, pack2, locate, finish (+ 6 fallback kernels)
-        n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 6 + 6;
+        // gather + K-A + pack1; accept, qcanon, K-C, sample_lse, mass, pack2, fb_logits, fbx_stats;
+        // locate, fbx_accept; xfinish2, fbx_locate; fbx_write
+        n = (pl.G > 0 ? 1 + ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 8 + 2 + 2 + 1;
         if (path_out) *path_out = pl.path;
         if (launches_out) *launches_out = n;
         return NJ_OK;

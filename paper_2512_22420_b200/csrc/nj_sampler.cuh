@@ -252,6 +252,7 @@ struct MassParams {
     // next_token then points at the X3 buffer (-1 on non-owner ranks) and
     // flags go to xflags[b] (reduced by MAX, queued by k_xfinish)
     const double* xr2;
+    int64_t xstride;       // doubles per rank in xr2 (entries of 3 per request)
     int32_t nranks, rank;
     int32_t* xflags;
     // nj_propose: k_mass writes each bonus row's weights exp(l - lse) over its
@@ -264,7 +265,9 @@ struct MassParams {
 // zero residual mass (R6: the draw must come from p_n, which the fallback does;
 // the fallback kernel is launched on every call).
 __device__ __forceinline__ void flag_draw(const MassParams& p, int b, int32_t bits) {
-    if (p.xflags) atomicOr(&p.xflags[b], bits | 0x100);
+    // sharded mode: informational flags only (exchanged in X3); the draw itself is
+    // final -- the fp64 fallback there takes acceptance near-ties, decided before X2
+    if (p.xflags) atomicOr(&p.xflags[b], bits);
     else if (p.certify || (bits & 2)) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, bits);
 }
 
@@ -535,11 +538,16 @@ __global__ void k_greedy_decide(const ReqMeta m, const int32_t* __restrict__ dra
 }
 
 // K-D2: block per request.  Locate chunk -> sub-tile -> token.
+// Vocab-sharded mode (xr2: X2 entries (lse used, local mass W_r, rank-local lse
+// of the sample row) per rank, `xstride` doubles apart): the rank whose
+// exclusive prefix of the rescaled masses holds u * total locates the token,
+// the others write -1.  If the residual mass is zero on every rank (R6), all
+// ranks see it identically after X2 and draw from p_n instead: the masses are
+// exp(lse_r(n) - M), and the owner recomputes its p_n chunk masses here.
 __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, const ReqMeta m) {
     const int b = blockIdx.x;
     const double lse = sample_lse(p, b);
-    const float lsef = (float)lse, corr = lse_corr(lse);
-    const bool resid = p.s_resid[b] != 0;
+    const bool resid0 = p.s_resid[b] != 0;
     const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
     const float* lrow = logits_row(p, b);
     __shared__ double sh[4];
@@ -547,8 +555,8 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     __shared__ float wt[kSubTiles][8];
     const int gam = p.stage_mode ? 0 : m.row_off[b + 1] - m.row_off[b] - 1;
     const float uf = p.stage_mode ? p.u[b] : p.u[m.row_off[b] + gam];
-    __shared__ int s_own;
-    __shared__ double s_scale;
+    __shared__ int s_own, s_zero;
+    __shared__ double s_scale, s_T, s_lse;
     // the request's chunk masses -> smem with one parallel load (thread 0's
     // fixed-order scans below then run on smem, not on dependent global loads)
     constexpr int kMaxSmemChunks = 64;
@@ -557,55 +565,117 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     if (cm_smem)
         for (int c = threadIdx.x; c < p.nchunks; c += blockDim.x) scm[c] = __ldcg(&p.cmass[(int64_t)b * p.nchunks + c]);
     __syncthreads();
-    const double* cm = cm_smem ? scm : p.cmass + (int64_t)b * p.nchunks;
+    double* cm = cm_smem ? scm : p.cmass + (int64_t)b * p.nchunks;
     if (threadIdx.x == 0) {
-        double P = 0.0, Pc = 0.0;
-        int csel = -1, lastpos = -1;
         double W = 0.0;
         for (int c = 0; c < p.nchunks; ++c) W = W + cm[c];
         double T = (double)uf * W;
-        int own = 1, zero_g = 0, clamp_g = 0;
+        int own = 1, zero_g = 0;
         double scale = 1.0;   // local mass units -> natural (p) units
+        double lse_use = lse;
         if (p.xr2) {
             // global inverse CDF over the ranks' masses in rank order (nj_shard.cuh, X2)
+            const int64_t xs = p.xstride;
+            auto X = [&](int r, int k) { return p.xr2[(int64_t)r * xs + (int64_t)b * 3 + k]; };
             double M = -INFINITY;
             for (int r = 0; r < p.nranks; ++r)
-                if (p.xr2[((int64_t)r * m.B + b) * 2 + 1] > 0.0) M = fmax(M, p.xr2[((int64_t)r * m.B + b) * 2]);
+                if (X(r, 1) > 0.0) M = fmax(M, X(r, 0));
             double Tot = 0.0;
-            for (int r = 0; r < p.nranks; ++r) {
-                const double Wr = p.xr2[((int64_t)r * m.B + b) * 2 + 1];
-                if (Wr > 0.0) Tot += Wr * exp(p.xr2[((int64_t)r * m.B + b) * 2] - M);
-            }
-            const double nrm = resid ? 1.0 : 1.0 / Tot;   // bonus rows: natural mass = A / Tot
-            if (!(Tot > 0.0)) {
+            for (int r = 0; r < p.nranks; ++r)
+                if (X(r, 1) > 0.0) Tot += X(r, 1) * exp(X(r, 0) - M);
+            const bool pn = !(Tot > 0.0);   // zero residual mass on every rank (R6): p_n
+            int col = 0;
+            double nrm = resid0 ? 1.0 : 1.0 / Tot;   // bonus rows: natural mass = A / Tot
+            if (pn) {
                 zero_g = 1;
-                own = 0;
-            } else {
-                const double Tg = (double)uf * Tot;
-                double Pg = 0.0, Po = 0.0, Ao = 0.0;
-                int o = -1, lastr = -1;
-                for (int r = 0; r < p.nranks; ++r) {
-                    const double Wr = p.xr2[((int64_t)r * m.B + b) * 2 + 1];
-                    const double A = Wr > 0.0 ? Wr * exp(p.xr2[((int64_t)r * m.B + b) * 2] - M) : 0.0;
-                    if (A > 0.0) {
-                        lastr = r;
-                        if (o < 0 && Tg < Pg + A) { o = r; Po = Pg; Ao = A; }
-                    }
-                    Pg += A;
+                M = -INFINITY;
+                for (int r = 0; r < p.nranks; ++r) M = fmax(M, X(r, 2));
+                Tot = 0.0;
+                for (int r = 0; r < p.nranks; ++r) Tot += exp(X(r, 2) - M);
+                col = 2;
+                nrm = 1.0 / Tot;
+            }
+            const double Tg = (double)uf * Tot;
+            double Pg = 0.0, Po = 0.0, Ao = 0.0;
+            int o = -1, lastr = -1;
+            for (int r = 0; r < p.nranks; ++r) {
+                const double A = pn ? exp(X(r, 2) - M) : (X(r, 1) > 0.0 ? X(r, 1) * exp(X(r, 0) - M) : 0.0);
+                if (A > 0.0) {
+                    lastr = r;
+                    if (o < 0 && Tg < Pg + A) { o = r; Po = Pg; Ao = A; }
                 }
-                if (o < 0) { o = lastr; clamp_g = 1; }
-                own = (o == p.rank);
-                if (own) {
-                    const double e = exp(p.xr2[((int64_t)p.rank * m.B + b) * 2] - M);
-                    scale = e * nrm;
+                Pg += A;
+            }
+            int clamp_g = 0;
+            if (o < 0) { o = lastr; clamp_g = 1; }
+            own = (o == p.rank);
+            if (own) {
+                const double e = exp(X(p.rank, col) - M);   // this rank's units -> the global ones
+                scale = e * nrm;
+                if (pn) {
+                    lse_use = X(p.rank, 2);   // local weights exp(l - lse_r(n)) sum to 1
+                    T = clamp_g ? 1.0 : (Tg - Po) / e;   // fraction of the local mass (rescaled below)
+                } else {
                     T = clamp_g ? W : (Tg - Po) / e;
                     if (!clamp_g && fmin(Tg - Po, Po + Ao - Tg) * nrm <= (double)p.eps_draw) flag_draw(p, b, 0);
                 }
+                if (clamp_g) flag_draw(p, b, 4);
             }
-            if (p.dbg_mass) p.dbg_mass[b] = zero_g ? 0.0 : (resid ? Tot : 1.0);
+            if (pn) flag_draw(p, b, 2);
+            if (p.dbg_mass) p.dbg_mass[b] = pn ? 0.0 : (resid0 ? Tot : 1.0);
         }
         s_own = own;
+        s_zero = zero_g;
         s_scale = scale;
+        s_T = T;
+        s_lse = lse_use;
+        sh[1] = W;
+    }
+    __syncthreads();
+    if (p.xr2 && !s_own) {   // another rank owns this draw
+        if (threadIdx.x == 0) p.next_token[b] = -1;
+        return;
+    }
+    const bool resid = resid0 && !s_zero;
+    const float lsef = (float)s_lse, corr = lse_corr(s_lse);
+    if (s_zero) {
+        // R6 on the owner rank: this request's p_n chunk masses with the rank-local
+        // lse (k_mass summed the residual), same reduction order as k_mass
+        for (int c = 0; c < p.nchunks; ++c) {
+            float v[kSubTiles];
+#pragma unroll
+            for (int s2 = 0; s2 < kSubTiles; ++s2) v[s2] = chunk_weight(p, lrow, c, s2, lsef, corr, false, qrow);
+            warp_totals16(v, wt);
+            __syncthreads();
+            __shared__ double sst0[kSubTiles];
+            if (threadIdx.x < kSubTiles) {
+                double st = 0.0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
+                sst0[threadIdx.x] = st;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < kSubTiles; ++k) acc = acc + sst0[k];
+                cm[c] = acc;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            double W = 0.0;
+            for (int c = 0; c < p.nchunks; ++c) W = W + cm[c];
+            sh[1] = W;
+            s_T = s_T * W;   // fraction of the local mass -> local units
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double W = sh[1];
+        const double T = s_T;
+        double P = 0.0, Pc = 0.0;
+        int csel = -1, lastpos = -1;
         for (int c = 0; c < p.nchunks; ++c) {
             const double wc = cm[c];
             if (wc > 0.0) lastpos = c;
@@ -613,26 +683,18 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
             P = P + wc;
         }
         int clamp = 0;
-        if (zero_g || !(W > 0.0)) clamp = 2;               // zero mass (R6) -> fallback
+        if (!(W > 0.0)) clamp = 2;               // zero mass (R6, unsharded) -> fp64 fallback
         else if (csel < 0) { clamp = 1; csel = lastpos; Pc = 0.0; }
         sh[0] = T - Pc;
-        sh[1] = W;
         shi[0] = csel;
         shi[1] = clamp;
-        if (!p.stage_mode && p.dbg_lse && !resid) p.dbg_lse[m.row_off[b] + gam] = (float)lse;
+        if (!p.stage_mode && p.dbg_lse && !resid0) p.dbg_lse[m.row_off[b] + gam] = (float)lse;
     }
     __syncthreads();
     const int clamp = shi[1];
-    if (p.xr2 && !s_own) {   // another rank owns this draw (or zero mass everywhere)
-        if (threadIdx.x == 0) {
-            p.next_token[b] = -1;
-            if (clamp == 2) flag_draw(p, b, 2);
-        }
-        return;
-    }
     if (clamp == 2) {
         if (threadIdx.x == 0) {
-            p.next_token[b] = 0;
+            p.next_token[b] = p.xr2 ? -1 : 0;
             if (p.dbg_mass) p.dbg_mass[b] = 0.0;
             if (p.dbg_flags) p.dbg_flags[b] = 2;
             flag_draw(p, b, 2);

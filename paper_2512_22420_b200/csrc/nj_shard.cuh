@@ -2,24 +2,29 @@
 // §8a row a7, §8e "vocab-sharded").  Rank r of G owns the contiguous vocab
 // shard [v_begin, v_end) of W_lm (rank order = ascending token id, R5).  The
 // kernels here pack / merge the small per-rank summaries that the host
-// exchanges between the phases of nj_verify (NCCL allgather / allreduce-MAX,
-// or device copies inside an nj_group):
+// exchanges between the phases of nj_verify -- FOUR collectives per step
+// (NCCL allgather x3 + allreduce-MAX, or device copies inside an nj_group):
 //
-//   X1  per draft row g : (lse_r(g), l_g(x_g) if x_g is in this shard else NaN)
-//       -> every rank merges lse(g) = logsumexp_r lse_r(g) in rank order and
-//          takes the owner's draft logit: identical acceptance decisions
-//          everywhere (k_accept with xr1).
-//   X2  per request b   : (lse used for the sample row, local mass W_r)
-//       residual rows use the global lse from X1 (so W_r are natural masses);
-//       bonus rows use the rank-local lse (W_r ~ 1 in local units) and are
+//   X1 (allgather)  per draft row g: (lse_r(g), l_g(x_g) if x_g is in this
+//       shard else NaN) -> every rank merges lse(g) = logsumexp_r lse_r(g) in
+//       rank order and takes the owner's draft logit: identical acceptance
+//       decisions everywhere (k_accept with xr1).  Acceptance near-ties are
+//       therefore known identically on every rank right after X1, and the
+//       certified fp64 fallback's first stage (fp64 logits + per-row local
+//       lse / owned draft logit of the queued requests) runs before X2.
+//   X2 (allgather)  per request b: (lse used for the sample row, local mass
+//       W_r, rank-local lse of the sample row) ++ the fallback's per-row
+//       (lse_r, owned draft logit).  Residual rows use the global lse from X1
+//       (so W_r are natural masses); bonus rows use the rank-local lse and are
 //       rescaled by exp(lse_r - M).  The inverse CDF (R5) over the global
-//       ascending order is then: T = u * sum_r A_r, owner = the rank whose
-//       exclusive prefix interval holds T, local target (T - P_owner) /
-//       exp(lse_owner - M)  (k_locate with xr2).
-//   X3  allreduce-MAX of [next_token (-1 on non-owners) | flags] (k_xfinish).
-// The certified fallback (R11/R12) repeats the same three exchanges in fp64
-// for the queued requests (X4: per-row (lse_r, owned draft logit); X5:
-// per-request local residual / p masses; X6: MAX of [token | flags]).
+//       ascending order: T = u * sum_r A_r, owner = the rank whose exclusive
+//       prefix interval holds T, local target (T - P_owner) / exp(lse_owner - M)
+//       (k_locate with xr2).  Zero residual mass on every rank (R6) switches
+//       every rank, identically, to p_n with masses exp(lse_r(n) - M).
+//   X3 (allgather)  [next_token (-1 on non-owners) | flags] ++ the fallback's
+//       fp64 local masses; every rank takes the MAX over ranks locally.
+//   X4 (allreduce-MAX) the fallback's tokens (owner rank, -1 elsewhere).
+#pragma once
 #pragma once
 #include "nj_sampler.cuh"
 
@@ -27,18 +32,22 @@ namespace nj {
 
 // Merge of the X1 entries of draft row g: lse = M + log sum_r exp(lse_r - M)
 // (rank order), dl = the owner's draft logit (exactly one rank is not NaN).
-__device__ __forceinline__ double xmerge_lse(const double* xr, int nranks, int ld, int g, double& dl) {
+// (rank stride `rs` doubles between the ranks' blocks of entries)
+__device__ __forceinline__ double xmerge_lse_s(const double* xr, int nranks, int64_t rs, int g, double& dl) {
     double M = -INFINITY;
     dl = __longlong_as_double(0x7ff8000000000000ll);
     for (int r = 0; r < nranks; ++r) {
-        const double* e = xr + ((int64_t)r * ld + g) * 2;
+        const double* e = xr + (int64_t)r * rs + (int64_t)g * 2;
         M = fmax(M, __ldcg(&e[0]));
         const double d = __ldcg(&e[1]);
         if (!isnan(d)) dl = d;
     }
     double S = 0.0;
-    for (int r = 0; r < nranks; ++r) S += exp(__ldcg(&xr[((int64_t)r * ld + g) * 2]) - M);
+    for (int r = 0; r < nranks; ++r) S += exp(__ldcg(&xr[(int64_t)r * rs + (int64_t)g * 2]) - M);
     return M + log(S);
+}
+__device__ __forceinline__ double xmerge_lse(const double* xr, int nranks, int ld, int g, double& dl) {
+    return xmerge_lse_s(xr, nranks, (int64_t)ld * 2, g, dl);
 }
 
 // X1 pack: warp per draft row.
@@ -53,38 +62,47 @@ __global__ void k_xpack1(const float* part_m, const float* part_s, int pld, int 
     }
 }
 
-// X2 pack: warp per request: lse of the sample row as used by k_mass, and the
-// rank's mass sum_c cmass (fixed order, as k_locate sums it).
+// X2 pack: warp per request: lse of the sample row as used by k_mass, the
+// rank's mass sum_c cmass (fixed order, as k_locate sums it), and the
+// rank-local lse of the sample row from K-C's statistics (R6 across shards).
 __global__ void k_xpack2(const MassParams p, int B, double* xs2) {
     const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     if (b >= B) return;
+    const double lloc = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
     double l = __ldcg(&p.s_lse[b]);
-    if (isnan(l)) l = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
+    if (isnan(l)) l = lloc;
     if (lane_id() == 0) {
         double W = 0.0;
         for (int c = 0; c < p.nchunks; ++c) W = W + __ldcg(&p.cmass[(int64_t)b * p.nchunks + c]);
-        xs2[2 * b] = l;
-        xs2[2 * b + 1] = W;
+        xs2[3 * b] = l;
+        xs2[3 * b + 1] = W;
+        xs2[3 * b + 2] = lloc;
     }
 }
 
-// After X3: outputs, flags and the canonical (ascending request) fallback
-// queue, identical on every rank.  One block.
-__global__ void k_xfinish(const int32_t* x3, int B, int32_t* next_token, int32_t* req_flags, int32_t* fb_count,
-                          int32_t* fb_list, int32_t* dbg_flags, int certify) {
-    for (int b = threadIdx.x; b < B; b += blockDim.x) {
-        next_token[b] = x3[b];
-        const int32_t f = x3[B + b] | req_flags[b];
-        req_flags[b] = f;
-        if (dbg_flags) dbg_flags[b] = f & 0xff;
-    }
-    __syncthreads();
+// The fallback queue in canonical (ascending request) order, identical on every
+// rank (acceptance flags come from the merged X1 data).  One block.
+__global__ void k_qcanon(const int32_t* req_flags, int B, int32_t* fb_count, int32_t* fb_list, int force_all) {
     if (threadIdx.x == 0) {
         int n = 0;
-        if (certify)
-            for (int b = 0; b < B; ++b)
-                if (req_flags[b] & 0x100) fb_list[n++] = b;
+        for (int b = 0; b < B; ++b)
+            if (force_all || (req_flags[b] & 0x100)) fb_list[n++] = b;
         *fb_count = n;
+    }
+}
+
+// After X3: next_token / flags = max / or over the ranks' gathered entries
+// (rank stride rs int32s, tokens at [0, B), flags at [mb, mb + B)).  One block.
+__global__ void k_xfinish2(const int32_t* x3r, int nranks, int64_t rs, int mb, int B, int32_t* next_token,
+                           int32_t* dbg_flags) {
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+        int32_t t = -1, f = 0;
+        for (int r = 0; r < nranks; ++r) {
+            t = max(t, x3r[(int64_t)r * rs + b]);
+            f |= x3r[(int64_t)r * rs + mb + b];
+        }
+        next_token[b] = t;
+        if (dbg_flags) dbg_flags[b] = f & 0xff;
     }
 }
 
@@ -125,8 +143,8 @@ __global__ void __launch_bounds__(256) k_fbx_stats(const FbParams p, const ReqMe
 
 // FBX-2: merged fp64 lse, acceptance (identical on every rank), local masses
 // of the residual / bonus distribution and of p_n (zero-mass rule R6).
-__global__ void __launch_bounds__(256) k_fbx_accept(const FbParams p, const ReqMeta m, const double* r4, int nranks,
-                                                    int slots, int qcap, double* s5, int32_t* fbn, double* fblse) {
+__global__ void __launch_bounds__(256) k_fbx_accept(const FbParams p, const ReqMeta m, const double* r4, int64_t rs4,
+                                                    int nranks, int slots, double* s5, int32_t* fbn, double* fblse) {
     __shared__ double sh[32];
     __shared__ double s_lse;
     __shared__ int s_n;
@@ -140,7 +158,7 @@ __global__ void __launch_bounds__(256) k_fbx_accept(const FbParams p, const ReqM
             double lse_n = 0.0;
             for (int i = 0; i <= gam; ++i) {
                 double dl;
-                const double lse = xmerge_lse(r4, nranks, qcap * slots, k * slots + i, dl);
+                const double lse = xmerge_lse_s(r4, nranks, rs4, k * slots + i, dl);
                 if (i == gam) { lse_n = lse; break; }
                 const double pd = exp(dl - lse);
                 const double qx = (double)p.q[(int64_t)(g0 + i) * p.ldq + p.draft_tokens[g0 + i]];
@@ -177,9 +195,9 @@ __global__ void __launch_bounds__(256) k_fbx_accept(const FbParams p, const ReqM
 // FBX-3: owner rank of the draw (prefix over ranks in rank order) scans its
 // local fp64 weights in ascending id.  x6[k] = global token or -1,
 // x6[qcap + k] = flag bits (2 zero mass, 4 clamp).
-__global__ void __launch_bounds__(256) k_fbx_locate(const FbParams p, const ReqMeta m, const double* r5, int nranks,
-                                                    int rank, int qcap, const int32_t* fbn, const double* fblse,
-                                                    int32_t* x6) {
+__global__ void __launch_bounds__(256) k_fbx_locate(const FbParams p, const ReqMeta m, const double* r5, int64_t rs5,
+                                                    int nranks, int rank, int qcap, const int32_t* fbn,
+                                                    const double* fblse, int32_t* x6) {
     __shared__ double sh[32];
     __shared__ double s_t, sbase;
     __shared__ int s_own, s_clamp, s_zero, st;
@@ -192,16 +210,16 @@ __global__ void __launch_bounds__(256) k_fbx_locate(const FbParams p, const ReqM
         const double ln = fblse[k];
         if (threadIdx.x == 0) {
             double Tot = 0.0;
-            for (int r = 0; r < nranks; ++r) Tot += r5[((int64_t)r * qcap + k) * 2];
+            for (int r = 0; r < nranks; ++r) Tot += r5[(int64_t)r * rs5 + (int64_t)k * 2];
             const int zero = !(Tot > 0.0);
             const int col = zero ? 1 : 0;
-            if (zero) { Tot = 0.0; for (int r = 0; r < nranks; ++r) Tot += r5[((int64_t)r * qcap + k) * 2 + 1]; }
+            if (zero) { Tot = 0.0; for (int r = 0; r < nranks; ++r) Tot += r5[(int64_t)r * rs5 + (int64_t)k * 2 + 1]; }
             const double T = (double)p.u[ro + gam] * Tot;
             double P = 0.0;
             int own = -1, last = -1;
             double Pown = 0.0;
             for (int r = 0; r < nranks; ++r) {
-                const double A = r5[((int64_t)r * qcap + k) * 2 + col];
+                const double A = r5[(int64_t)r * rs5 + (int64_t)k * 2 + col];
                 if (A > 0.0) {
                     last = r;
                     if (own < 0 && T < P + A) { own = r; Pown = P; }

@@ -144,3 +144,47 @@ def test_split_requests_balanced():
         rows = [int((g[a:b] + 1).sum()) for a, b in spans]
         assert sum(rows) == int((g + 1).sum())
         assert max(rows) - min(rows) <= 6 + 1
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_protocol_zero_residual_mass(G):
+    """R6 across shards: q_0 = p_0 rounded UP to fp32 (so max(0, p - q) == 0
+    everywhere) and u_0 = 1 (forced rejection): every rank switches to p_0 with
+    masses e^{lse_r(0) - M}, and the drawn token equals the unsharded oracle's
+    (which draws from p_0, R6)."""
+    import threading
+    import scipy.special
+    for seed in range(3):
+        b = make_batch(1, 1, V=700, d=24, seed=seed + 50)
+        n = b.to_numpy()
+        from oracle.verify_np import bf16_to_f64
+        p0 = scipy.special.softmax(bf16_to_f64(n["hidden_bits"][:1]) @ bf16_to_f64(n["W_bits"]).T, axis=1)[0]
+        q = np.nextafter(p0.astype(np.float32), np.float32(2.0)).reshape(1, -1)
+        u = np.array([1.0, 0.1 + 0.25 * seed])
+        args = (n["hidden_bits"], n["W_bits"], n["draft_tokens"], q, n["gamma"], u)
+        ref = oracle.verify(*args)
+        assert ref["flags"][0] & oracle.F_ZERO_MASS and ref["accept_len"][0] == 0
+        bar = threading.Barrier(G)
+        slots = [None] * G
+        res = [None] * G
+
+        def coll(rank, a, red):
+            bar.wait()
+            slots[rank] = a
+            bar.wait()
+            out = red(list(slots))
+            bar.wait()
+            return out
+
+        def body(rank):
+            gather = lambda a: coll(rank, a, lambda xs: xs)
+            allmax = lambda a: coll(rank, a, lambda xs: np.max(np.stack(xs), axis=0))
+            res[rank] = sharded_ref.rank_step(rank, G, *args, gather, allmax)
+
+        th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for acc, tok in res:
+            assert acc[0] == 0 and tok[0] == ref["next_token"][0]
