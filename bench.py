@@ -765,7 +765,7 @@ def bench_c5(args, ws, rank, local):
             "config": {"workload": "qwen7b_c5_vocab_sharded", "B": B, "gamma": g, "N_per_step": b.N, "d": D_Q,
                        "V": V_Q, "V_per_rank_max": max(shard_range(V_Q, ws, r)[1] - shard_range(V_Q, ws, r)[0]
                                                       for r in range(ws)),
-                       "parallelism": f"vocab-sharded x{ws} (NCCL allgather x2 + allreduce-MAX per step)",
+                       "parallelism": f"vocab-sharded x{ws} (4 NCCL collectives per step: allgather x3 + allreduce-MAX)",
                        "l2": (f"W shard {(ve - vb) * D_Q * 2 / 2 ** 20:.0f} MiB x {nW} rotating copies "
                               "(> L2 between reuses); streamed from HBM every step"),
                        "launch": "CUDA graph replay per step" if graph_ok else "eager launches",

@@ -749,7 +749,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         ap.xr1 = c->xr1; ap.nranks = c->nranks; ap.xld = pl.G;
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, a.meta);
         NJ_LAUNCHED(c, "k_accept", st);
-        k_qcanon<<<1, 32, 0, st>>>(c->req_flags(), pl.B, c->fb_count(), c->fb_list(), c->force_fb);
+        k_qcanon<<<1, 1024, 0, st>>>(c->req_flags(), pl.B, c->fb_count(), c->fb_list(), c->force_fb);
         NJ_LAUNCHED(c, "k_qcanon", st);
         a.gridC = c->grid;
         {

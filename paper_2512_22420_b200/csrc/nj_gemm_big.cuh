@@ -291,6 +291,11 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
             uint32_t tp0 = 0u, tp1 = 0u;   // and its phase
             int abuf = 0;
             uint32_t aph = 0;
+            int mst = 0;
+            const bool tsx = p.ts != nullptr && cta == 0;   // debug timeline (NJ_PHASE_TS), uniform
+            auto stamp = [&](int idx) {
+                if (tsx && lane == 0) p.ts[idx] = globaltimer();
+            };
             int row0, trows, row0L, trowsL, trowsP, c;
             for (int it = 0; next_item(it, row0, trows, row0L, trowsL, trowsP, c); ++it) {
                 const int team = it % TEAMS;
@@ -301,16 +306,20 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                 uint32_t dt = 0;
                 for (int kg = 0; kg < ngk; ++kg) {
                     const int ng = min(GK, p.num_kb - kg * GK);
+                    if (tsx && mst < 1300) stamp(4096 + 3 * mst);
                     if (p.spin & 1) mbar_wait_w_spin(&full[s], ph);
                     else mbar_wait_w(&full[s], ph);
+                    if (tsx && mst < 1300) stamp(4096 + 3 * mst + 1);
                     tc_fence_after();
                     uint8_t* st = ring + (size_t)s * stageBytes;
                     for (int g = 0; g < ng; ++g) {
                         if (kin == 0) {
                             abuf = team ? NBT + tb1 : tb0;
                             aph = team ? tp1 : tp0;
+                            if (tsx && ngrp < 2000) stamp(12288 + 2 * ngrp);
                             if (p.spin & 1) mbar_wait_w_spin(&aempty[abuf], aph ^ 1);
                             else mbar_wait_w(&aempty[abuf], aph ^ 1);
+                            if (tsx && ngrp < 2000) stamp(12288 + 2 * ngrp + 1);
                             tc_fence_after();
                             dt = tbase + (uint32_t)(abuf * p.bstride);
                         }
@@ -337,6 +346,8 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                     if (p.dbg & 16) mbar_arrive_w(&empty[s]);   // probe (CG = 1, no MMAs): plain arrive
                     else if (CG == 2) mma_commit_mc2_w(&empty[s], 3);
                     else mma_commit_w(&empty[s]);
+                    if (tsx && mst < 1300) stamp(4096 + 3 * mst + 2);
+                    ++mst;
                     if (++s == S) { s = 0; ph ^= 1; }
                 }
             }

@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, con
     const int b = blockIdx.x;
     const double lse = sample_lse(p, b);
     const bool resid0 = p.s_resid[b] != 0;
-    const float* qrow = p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin;
+    const float* qrow = resid0 ? p.q + (int64_t)p.s_qrow[b] * p.ldq + p.v_begin : nullptr;
     const float* lrow = logits_row(p, b);
     __shared__ double sh[4];
     __shared__ int shi[4];

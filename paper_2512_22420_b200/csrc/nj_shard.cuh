@@ -82,11 +82,23 @@ __global__ void k_xpack2(const MassParams p, int B, double* xs2) {
 
 // The fallback queue in canonical (ascending request) order, identical on every
 // rank (acceptance flags come from the merged X1 data).  One block.
-__global__ void k_qcanon(const int32_t* req_flags, int B, int32_t* fb_count, int32_t* fb_list, int force_all) {
-    if (threadIdx.x == 0) {
+// One block of 1024 threads (B <= kMaxB): thread b's position is the exclusive
+// count of flagged requests before it (warp ballots + a scan of warp totals).
+__global__ void __launch_bounds__(1024) k_qcanon(const int32_t* req_flags, int B, int32_t* fb_count,
+                                                 int32_t* fb_list, int force_all) {
+    __shared__ int wtot[32];
+    const int b = threadIdx.x;
+    const bool f = b < B && (force_all || (__ldcg(&req_flags[b]) & 0x100));
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    const int lane = (int)lane_id(), w = (int)warp_id();
+    if (lane == 0) wtot[w] = __popc(m);
+    __syncthreads();
+    int off = 0;
+    for (int k = 0; k < w; ++k) off += wtot[k];
+    if (f) fb_list[off + __popc(m & ((1u << lane) - 1u))] = b;
+    if (b == 0) {
         int n = 0;
-        for (int b = 0; b < B; ++b)
-            if (force_all || (req_flags[b] & 0x100)) fb_list[n++] = b;
+        for (int k = 0; k < (int)(blockDim.x / 32); ++k) n += wtot[k];
         *fb_count = n;
     }
 }
