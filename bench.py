@@ -292,11 +292,21 @@ def bench_nj(args, ws, rank, local):
     from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
+    # more ranks than GPUs (a 1-GPU box exercising the N > 1 code path): ranks share
+    # the devices round-robin and the host-side plumbing runs over gloo; the timing
+    # is then contended and is flagged, never a scaling number
+    ndev = torch.cuda.device_count()
+    over = ws > ndev
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = None if over else dev   # device of the plumbing collectives' tensors
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if over:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     B, gamma, path = CONFIGS[args.config]
     path = PATH_NAMES.index(args.path or path)
     strong = args.scaling == "strong" and ws > 1
@@ -382,10 +392,10 @@ def bench_nj(args, ws, rank, local):
     acc_tok = sum(per_batch[i % nb][0] for i in range(args.steps))
     rejected = sum(per_batch[i % nb][1] for i in range(args.steps))
     N, G = batches[0].N, batches[0].G
-    t_max = njdist.max_over_ranks(ms, dev)
+    t_max = njdist.max_over_ranks(ms, cdev)
     tok_all = acc_tok
     if ws > 1:
-        t = torch.tensor([float(acc_tok)], dtype=torch.float64, device=dev)
+        t = torch.tensor([float(acc_tok)], dtype=torch.float64, device=cdev)
         dist.all_reduce(t)
         tok_all = float(t.item())
     value = N_global * args.steps / (t_max / 1e3)
@@ -444,7 +454,7 @@ def bench_nj(args, ws, rank, local):
             v.verify_host(hh, W, th, qh, b.gamma, uh, ah, nh)
         s1.record(stream)
         torch.cuda.synchronize()
-        e_ms = njdist.max_over_ranks(s0.elapsed_time(s1), dev)
+        e_ms = njdist.max_over_ranks(s0.elapsed_time(s1), cdev)
         # bytes that cross the host link per step: the copied hidden / tokens / uniforms,
         # plus the draft-probability bytes the kernels read in place (zero copy):
         # q_i(x_i) of every draft and the sample row of every rejected request
@@ -477,6 +487,8 @@ def bench_nj(args, ws, rank, local):
             "step_ms": step_stats(per), "step_ms_eager": step_stats(per_eager),
             "accepted_tokens_per_s": tok_all / (t_max / 1e3),
             "realised_tokens_per_request": acc_tok / (args.steps * max(Bl, 1)),
+            "oversubscribed": (f"{ws} ranks on {ndev} GPU(s): ranks share devices, timing contended "
+                               "(code-path check, not a scaling number)") if over else None,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(launches * args.steps)}
     emit(line)
