@@ -122,14 +122,14 @@ def test_c1_golden_fixed_uniforms(path):
 
 # ----------------------------------------------------------------- production GEMM, element-wise
 @pytest.mark.parametrize("V,d,R,ks", [(1024, 128, 20, 0), (1000, 64, 37, 0), (QV, QD, 40, 0), (QV, QD, 300, 0),
-                                      (QV, QD, 40, 8)])
+                                      (QV, QD, 40, 8), (QV, QD, 40, 14)])
 def test_production_gemm_logits_vs_oracle(V, d, R, ks):
     """nj_lmhead_logits runs k_gemm_big (the kernel the staged / two-pass paths
     and nj_propose launch) and returns fp32 logits; every element of every row
     is compared with the oracle's fp64 logits (R = 300: two token chunks), and
     the full p rows via ln p = l - logsumexp(l): within BJ's 2e-3 and within the
     measured bound of DESIGN.md §6 (restart every 4 k-blocks: |d ln p| <= 2e-5;
-    every 8: <= 4e-5)."""
+    every 8: <= 4e-5; every 14, the certified K-A: <= 6e-5)."""
     W = w_full() if V == QV else make_weight(V, d, 1, DEV)
     g = torch.Generator(device=DEV).manual_seed(R + ks)
     h = (torch.randn(R, d, device=DEV, generator=g) *
@@ -146,7 +146,7 @@ def test_production_gemm_logits_vs_oracle(V, d, R, ks):
     lse_g = np.logaddexp.reduce(got, axis=1)
     lse_r = np.logaddexp.reduce(ref, axis=1)
     dlnp = np.abs((got - lse_g[:, None]) - (ref - lse_r[:, None]))
-    bound = 4e-5 if ks == 8 else 2e-5
+    bound = {8: 4e-5, 14: 6e-5}.get(ks, 2e-5)   # measured maxima 6.8e-6 / 1.0e-5 / 1.9e-5 (ks 4 / 8 / 14)
     print(f"[gemm] V={V} R={R} ks={ks}: max|dl|={dl.max():.3g} max|d ln p|={dlnp.max():.3g}")
     assert dlnp.max() <= 2e-3
     assert dlnp.max() <= bound, dlnp.max()

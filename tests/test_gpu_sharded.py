@@ -110,7 +110,7 @@ def test_group_c5_full_size():
     W = make_weight(QV, QD, 0, DEV)
     b = make_batch(32, 2, V=QV, d=QD, seed=55, device=DEV, W=W)
     acc, nxt, dd = run_group(b, 8)
-    check(b, acc, nxt, dd, lnp_tol=2e-5)
+    check(b, acc, nxt, dd, lnp_tol=4e-5)   # sharded K-A restarts every 14 k-blocks (certified)
 
 
 @pytest.mark.parametrize("G", [8, 2])
