@@ -494,16 +494,23 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                         float tm[16];
                         if (ref_ok) {
                             bool ovf = false;
+                            float rl = 0.f;   // the reference of this lane's column after the scatter
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
+                                // one warp-wide read per column: every lane uses the same r_j,
+                                // and the lane that ends with column j keeps exactly that value
+                                // (other warps may update the shared row state meanwhile)
+                                const float rjv = rsrc[2 * j];
+                                if (j == (lane >> 1)) rl = rjv;
                                 const bool in = full || (valid && hh * 16 + j < myc);
-                                const float dd = acc[hh * 16 + j] - rsrc[2 * j];
+                                const float dd = acc[hh * 16 + j] - rjv;
                                 ovf |= in && dd > 64.f;
                                 tm[j] = in ? __expf(dd) : 0.f;
                             }
+                            ovf |= rl == -INFINITY;   // a column's state was reset meanwhile: full pass
                             if (!__any_sync(0xffffffffu, ovf)) {
                                 ws = warp_scatter16(tm, [](float a, float b) { return a + b; });
-                                wm = rsrc[2 * (lane >> 1)];
+                                wm = rl;
                                 done = true;
                             }
                         }
@@ -528,26 +535,28 @@ k_gemm_big(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ C
                                 else ms_merge(r.x, r.y, wm, ws);
                                 sc = r;
                             } else {
-                                sc = make_float2(wm, ws);
+                                // several chunks: merge (wm, ws) straight into the CTA's row
+                                // state with a 64-bit CAS loop (lock-free; the 4 lane-quadrant
+                                // warps of the slice need no barrier); with the shared
+                                // reference the merge is a plain add
+                                unsigned long long* ps = reinterpret_cast<unsigned long long*>(
+                                    &tstate[c0 + e * cw + hh * 16 + (lane >> 1)]);
+                                unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(ps), assumed;
+                                do {
+                                    assumed = old;
+                                    float cm = __uint_as_float((uint32_t)(assumed & 0xffffffffull));
+                                    float cs = __uint_as_float((uint32_t)(assumed >> 32));
+                                    if (cm == wm) cs += ws;
+                                    else ms_merge(cm, cs, wm, ws);
+                                    const unsigned long long nv = ((unsigned long long)__float_as_uint(cs) << 32) |
+                                                                  (unsigned long long)__float_as_uint(cm);
+                                    old = atomicCAS(ps, assumed, nv);
+                                } while (old != assumed);
                             }
                         }
                     }
                 }
                 if (tsi) p.ts[14336 + 4 * it + 2] = globaltimer();
-                if (one_chunk) continue;
-                named_bar(1 + team * EPT + e, 128);
-                const int ht = (wi & 3) * 32 + lane;   // 0..127 within the slice's 4 warps
-                if (ht < kBigNC && ht < myc) {
-                    const int col = c0 + e * cw + ht;
-                    float2 st = tstate[col];
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        const float2 o = scratch[((team * EPT + e) * 4 + w) * kBigNC + ht];
-                        ms_merge(st.x, st.y, o.x, o.y);
-                    }
-                    tstate[col] = st;
-                }
-                named_bar(1 + team * EPT + e, 128);
             }
         }
     }
