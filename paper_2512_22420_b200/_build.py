@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnj.so")
 SOURCES = ["nj_api.cu", "nj_bandit.cpp"]
-HEADERS = ["nj_ptx.cuh", "nj_gemm.cuh", "nj_fused.cuh", "nj_sampler.cuh", "nj_gemm_big.cuh", "nj_shard.cuh"]
+HEADERS = ["nj_ptx.cuh", "nj_gemm.cuh", "nj_fused.cuh", "nj_sampler.cuh", "nj_gemm_big.cuh", "nj_lmhead.cuh", "nj_shard.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

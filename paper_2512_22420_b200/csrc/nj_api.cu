@@ -61,7 +61,22 @@ bool encode_2d(CUtensorMap* m, const void* base, int64_t rows, int64_t d, int bo
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr int kStagedMaxN = kBigMaxRowG;   // staged path: rows of one GEMM pass (<= 2 token chunks of 256)
+// 2-D fp32 row-major tensor [rows][cols] with row pitch ld (elements), box {16, 32},
+// SWIZZLE_64B: k_lmhead's logits stores (nj_lmhead.cuh)
+bool encode_out(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld) {
+    EncodeTiledFn fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {16, 32};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr int kStagedMaxN = kBigMaxRowG;   // staged path on k_gemm_big (NJ_LM=0): rows of one GEMM pass
+constexpr int kStagedMaxRows = 2048;        // staged path on k_lmhead: rows of one GEMM pass (logits_st rows)
 
 inline int round16(int x) { return (x + 15) & ~15; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -88,6 +103,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1;   // k_lmhead
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -109,6 +125,16 @@ Knobs read_knobs() {
     k.big_s = env_int("NJ_BIG_S", -1);
     k.w_evict_first = env_int("NJ_W_EVICT_FIRST", -1);
     k.mass_probe = env_int("NJ_MASS_PROBE", 0);
+    k.lm = env_int("NJ_LM", 1);
+    k.lm_cg = env_int("NJ_LM_CG", 0);
+    k.lm_tw = std::min(256, std::max(16, env_int("NJ_LM_TW", 256) & ~15));
+    k.lm_gk = env_int("NJ_LM_GK", 0);
+    k.lm_s = env_int("NJ_LM_S", 0);
+    k.lm_dbg = env_int("NJ_LM_DBG", 0);
+    k.lm_nbuf = env_int("NJ_LM_NBUF", 0);   // probes only (TMEM holds 512 / stride buffers)
+    k.lm_ks = env_int("NJ_LM_KS", 0);
+    k.lm_tma_out = env_int("NJ_LM_TMA_OUT", 1);
+    k.lm_pf = env_int("NJ_LM_PF", -1);
     return k;
 }
 
@@ -168,7 +194,7 @@ struct nj_ctx {
     double *wpart = nullptr, *s_lse = nullptr, *cmass = nullptr, *fb_logits = nullptr, *lse_tmp = nullptr;
     uint16_t *hd = nullptr, *hs = nullptr;
     float* logits_s = nullptr;
-    float* logits_st = nullptr;    // staged path: [min(Nmax, kStagedMaxN)][V_local]
+    float* logits_st = nullptr;    // staged path: [staged_rows][V_local]
     int32_t *s_resid = nullptr, *s_qrow = nullptr;
     int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
     uint32_t* bar = nullptr;       // count, gen
@@ -197,6 +223,10 @@ struct nj_ctx {
     // W tensor-map cache
     const void* w_cached = nullptr;
     CUtensorMap tmW128{}, tmW16{};
+    const void* lm_w_cached = nullptr;   // k_lmhead W map (box rows vary with the tile width)
+    int lm_wbox = 0;
+    CUtensorMap tmWlm{};
+    int staged_rows = 0;                 // rows of logits_st
 
     int32_t* fb_count() { return fb_block; }
     int32_t* fb_list() { return fb_block + 1; }
@@ -284,20 +314,21 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
     pl.npad = round16(pl.N);
     const bool fused_ok = pl.N <= kFusedMaxN && c->max_tiles <= 16 && (c->max_tiles + 1) * pl.npad <= 512 &&
                           !c->sharded();
-    const bool staged_ok = pl.N <= kStagedMaxN && c->logits_st != nullptr && !c->sharded();
+    const bool staged_ok = pl.N <= c->staged_rows && c->logits_st != nullptr && !c->sharded();
     int path = c->path_opt;
     if (c->sharded() && path == NJ_PATH_AUTO) path = NJ_PATH_TWOPASS;   // the phased sharded driver
     // k_gemm_big's cost is ~per (vocab tile, token chunk) item whatever the chunk
     // width (<= 256): staged (ceil(N/256) chunks in one pass) wins only when it
     // needs fewer chunks than K-A + K-C (ceil(G/256) + ceil(B/256))
     const auto nch = [](int r) { return (r + kBigMaxT - 1) / kBigMaxT; };
-    const bool staged_pays = pl.N <= kBigMaxT || nch(pl.N) < nch(pl.G) + nch(pl.B);
+    // k_lmhead (default): one pass over all rows always beats streaming W twice
+    const bool staged_pays = c->kn.lm || pl.N <= kBigMaxT || nch(pl.N) < nch(pl.G) + nch(pl.B);
     if (path == NJ_PATH_AUTO)
         path = fused_ok ? NJ_PATH_FUSED : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
         return set_err(c, NJ_EUNSUPPORTED, "fused path needs N <= %d and TMEM room (N=%d)", kFusedMaxN, pl.N);
     if (path == NJ_PATH_STAGED && !staged_ok)
-        return set_err(c, NJ_EUNSUPPORTED, "staged path needs N <= %d (N=%d)", kStagedMaxN, pl.N);
+        return set_err(c, NJ_EUNSUPPORTED, "staged path needs N <= %d (N=%d)", c->staged_rows, pl.N);
     pl.path = path;
     return NJ_OK;
 }
@@ -509,6 +540,118 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     }
     NJ_LAUNCHED(c, "k_gemm_big", st);
     if (grid_used) *grid_used = grid;
+    return NJ_OK;
+}
+
+// k_lmhead (nj_lmhead.cuh): CTA group and tile width from a cost model of one
+// unit's (pair's / CTA's) work -- per k-block and SM, max(MMA cycles 2 * w,
+// L2 -> SM operand bytes / ~50 B per cycle) over its ntile x nchunks items,
+// plus ~1.5 us of per-item output -- then the ring depth from shared memory.
+struct LmPlan {
+    int cg, tile_w, w, nunits, nchunks;
+};
+LmPlan lm_plan(const nj_ctx* c, int R) {
+    LmPlan best{};
+    double best_t = 1e30;
+    const int nkb = (c->cfg.d + kBK - 1) / kBK;
+    for (int cg = 1; cg <= 2; ++cg) {
+        if (c->kn.lm_cg && c->kn.lm_cg != cg) continue;
+        const int nch = (R + kLmTok * cg - 1) / (kLmTok * cg);
+        const int ngroups = std::max(1, std::min(c->num_sms / cg / nch, c->U));   // units = groups x chunks
+        const int nunits = ngroups * nch;
+        const int upu = (c->U + ngroups - 1) / ngroups;   // 16-id units of the largest range
+        const int rows = std::min(upu * kUnit, c->V_local);
+        const int ntile = (rows + c->kn.lm_tw - 1) / c->kn.lm_tw;
+        const int w = ((rows + ntile - 1) / ntile + 15) & ~15;
+        const double mma = 2.0 * w, l2 = (kLmHBytes + (double)(w / cg) * 128.0) / 50.0;
+        if (nch > c->num_sms / cg) continue;   // (R > 148 chunks: never at kStagedMaxRows)
+        const double t = (double)ntile * (nkb * std::max(mma, l2) + 3000.0);
+        if (t < best_t * 0.98) {   // ties: the first (single-CTA) candidate
+            best_t = t;
+            best = LmPlan{cg, w, w, nunits, nch};
+        }
+    }
+    return best;
+}
+
+template <int MODE>
+nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_t* W, int R, LmheadParams& p,
+                    int* nparts) {
+    if (R <= 0) return NJ_OK;
+    const LmPlan pl = lm_plan(c, R);
+    const int CG = pl.cg;
+    p.R = R;
+    p.nchunks = pl.nchunks;
+    p.V_local = c->V_local;
+    p.U = c->U;
+    p.num_kb = (c->cfg.d + kBK - 1) / kBK;
+    p.v_begin = c->cfg.v_begin;
+    p.part_ld = c->pld;
+    if (p.inv_t == 0.f) p.inv_t = (float)c->inv_t;
+    if (p.ks <= 0) p.ks = c->gemm_ks;
+    p.tile_w = pl.tile_w;
+    p.wbox = (pl.w + CG - 1) / CG;
+    p.bstride = std::max(32, (pl.w + 31) & ~31);
+    p.nbuf = std::max(2, std::min(kLmMaxBuf, 512 / p.bstride));
+    if (c->kn.lm_nbuf > 0) p.nbuf = std::min(kLmMaxBuf, c->kn.lm_nbuf);
+    if (c->kn.lm_ks > 0) p.ks = c->kn.lm_ks;
+    p.dbg = c->kn.lm_dbg;
+    p.ts = nullptr;
+    if (c->kn.phase_ts) {
+        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
+        NJ_CUDA(c, cudaMemsetAsync(c->phase_ts, 0, 16 * 1024 * sizeof(unsigned long long), st));
+        p.ts = c->phase_ts;
+    }
+    // one chunk: W is streamed once (evict_first); several: the other chunks of a
+    // tile re-read it from L2 one item later (evict_last)
+    p.w_evict_first = pl.nchunks == 1 ? 1 : 0;
+    p.pf = c->kn.lm_pf >= 0 ? c->kn.lm_pf : 0;
+    if (c->kn.w_evict_first >= 0) p.w_evict_first = c->kn.w_evict_first;
+    if (c->lm_w_cached != W || c->lm_wbox != p.wbox) {
+        if (!encode_2d(&c->tmWlm, W, c->V_local, c->cfg.d, p.wbox))
+            return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (W, k_lmhead)");
+        c->lm_w_cached = W;
+        c->lm_wbox = p.wbox;
+    }
+    CUtensorMap tmH, tmL{};
+    if (!encode_2d(&tmH, h, R, c->cfg.d, kLmTok)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
+    constexpr bool STATE = (MODE & (LM_STATS | LM_ARGMAX)) != 0, CAP = (MODE & LM_CAPTURE) != 0,
+                   WR = (MODE & LM_WRITE) != 0;
+    p.tma_out = WR && c->kn.lm_tma_out && (p.ld_out & 3) == 0 && (reinterpret_cast<uintptr_t>(p.logits) & 15) == 0;
+    if (p.tma_out && !encode_out(&tmL, p.logits, R, c->V_local, p.ld_out))
+        return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (logits)");
+    const size_t nloc = kLmTok;
+    size_t tail = (p.tma_out ? (size_t)kLmEpiWarps * 2 * 2048 : 0) + (STATE ? 4 * nloc * 8 : 0) + (CAP ? nloc * 8 : 0);
+    tail = align_up(tail, 8) + (2 * 8 + 2 * kLmMaxBuf) * 8 + 8;
+    const size_t kb_bytes = (size_t)kLmHBytes + (size_t)p.wbox * 128;
+    p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : 1;
+    while (p.gk > 1 && (kSmemLimit - tail - 1024) / ((size_t)p.gk * kb_bytes) < 2) --p.gk;
+    const size_t stage = (size_t)p.gk * kb_bytes;
+    int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
+    if (c->kn.lm_s > 0) S = std::min(S, std::max(2, c->kn.lm_s));
+    if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_lmhead: not enough shared memory (R=%d)", R);
+    p.nstages = S;
+    const size_t smem = (size_t)S * stage + tail;
+    const int grid = pl.nunits * CG;
+    if (CG == 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kLmThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        NJ_CUDA(c, cudaLaunchKernelEx(&cfg, k_lmhead<MODE, 2>, c->tmWlm, tmH, tmL, p));
+    } else {
+        k_lmhead<MODE, 1><<<grid, kLmThreads, smem, st>>>(c->tmWlm, tmH, tmL, p);
+    }
+    NJ_LAUNCHED(c, "k_lmhead", st);
+    if (nparts) *nparts = pl.nunits / pl.nchunks;   // one partial per group and row
     return NJ_OK;
 }
 
@@ -949,7 +1092,8 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     A(hd, (size_t)c->Gmax * cfg->d);
     A(hs, (size_t)MB * cfg->d);
     A(logits_s, (size_t)MB * c->V_local);
-    A(logits_st, (size_t)std::min(c->Nmax, kStagedMaxN) * c->V_local);
+    c->staged_rows = std::min(c->Nmax, c->kn.lm ? kStagedMaxRows : kStagedMaxN);
+    A(logits_st, (size_t)c->staged_rows * c->V_local);
     A(s_resid, (size_t)MB);
     A(s_qrow, (size_t)MB);
     A(fb_block, (size_t)1 + 2 * MB);
@@ -975,6 +1119,10 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_gemm_big<false, true, true, 2>);
     e = e ? e : set_smem_attr(k_gemm_big<true, true, false, 2>);
     e = e ? e : set_smem_attr(k_gemm_big<true, true, true, 2>);
+    e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS | LM_CAPTURE, 1>);
+    e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS | LM_CAPTURE, 2>);
+    e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 1>);
+    e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 2>);
     if (const char* ev = getenv("NJ_MASS_NST")) c->mass_nst = std::min(4, std::max(2, atoi(ev)));
     e = e ? e : cudaFuncSetAttribute(k_mass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(2, c->cfg.max_batch));
     e = e ? e : cudaFuncSetAttribute(k_mass<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(3, c->cfg.max_batch));
@@ -1130,13 +1278,26 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         gp.use_row_g = 1;
         gp.w_evict_first = pl.N <= kBigMaxT ? 1 : 0;   // two chunks re-read W tiles from L2
         if (c->kn.w_evict_first >= 0) gp.w_evict_first = c->kn.w_evict_first;
-        for (int b = 0; b < pl.B; ++b)
-            for (int r = pl.row_off[b]; r < pl.row_off[b + 1]; ++r)
-                gp.row_g[r] = r + 1 < pl.row_off[b + 1] ? r - b : -1;
+        if (!c->kn.lm)
+            for (int b = 0; b < pl.B; ++b)
+                for (int r = pl.row_off[b]; r < pl.row_off[b + 1]; ++r)
+                    gp.row_g[r] = r + 1 < pl.row_off[b + 1] ? r - b : -1;
         std::pair<cudaEvent_t, cudaEvent_t> ev;
         if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
         int gridA = c->grid;
-        if ((s = launch_lmhead<true, true, true>(c, st, hidden, pl.N, gp, false, &gridA)) != NJ_OK) return s;
+        if (c->kn.lm) {
+            LmheadParams lp{};
+            lp.logits = c->logits_st; lp.ld_out = c->V_local;
+            lp.part_m = c->part_m; lp.part_s = c->part_s;
+            lp.tok = draft_tokens; lp.dl = c->dl;
+            lp.cap_staged = 1;
+            lp.B = pl.B;
+            for (int b = 0; b <= pl.B; ++b) lp.row_off[b] = pl.row_off[b];
+            if ((s = launch_lm<LM_WRITE | LM_STATS | LM_CAPTURE>(c, st, hidden, W_lm, pl.N, lp, &gridA)) != NJ_OK)
+                return s;
+        } else if ((s = launch_lmhead<true, true, true>(c, st, hidden, pl.N, gp, false, &gridA)) != NJ_OK) {
+            return s;
+        }
         if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
         AcceptParams ap{};
         ap.part_m = c->part_m; ap.part_s = c->part_s; ap.grid = gridA; ap.pld = c->pld; ap.dl = c->dl;
@@ -1316,7 +1477,7 @@ nj_status nj_verify_greedy(nj_ctx* c, void* stream, const uint16_t* hidden, cons
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     // all N rows through the LM-head GEMM in blocks of the staged logits buffer
     // (one W stream per block), fp32 logits -> row argmax
-    const int cap = std::min(c->Nmax, kStagedMaxN);
+    const int cap = std::min(c->Nmax, kStagedMaxN);   // k_gemm_big blocks
     NJ_CUDA(c, cudaMemsetAsync(c->amax, 0, (size_t)pl.N * sizeof(unsigned long long), st));
     for (int r0 = 0; r0 < pl.N; r0 += cap) {
         const int R = std::min(cap, pl.N - r0);
@@ -1395,8 +1556,20 @@ nj_status nj_lmhead_logits(nj_ctx* c, void* stream, const uint16_t* hidden, cons
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     k_gather_rows<<<n_rows, 128, 0, st>>>(hidden, c->cfg.d, rows, c->hd);
     NJ_LAUNCHED(c, "k_gather_rows", st);
-    // the production LM-head GEMM (k_gemm_big, as the staged / two-pass paths and
-    // nj_propose launch it) writing fp32 logits; statistics go to scratch partials
+    // the production LM-head GEMM (k_lmhead as the staged path launches it; k_gemm_big
+    // with NJ_LM=0, as the two-pass path and nj_propose launch it) writing fp32
+    // logits; statistics go to scratch partials
+    if (c->kn.lm) {
+        LmheadParams lp{};
+        lp.logits = logits;
+        lp.ld_out = ld_out;
+        lp.part_m = c->part_m;
+        lp.part_s = c->part_s;
+        lp.ks = ks;
+        lp.inv_t = 1.f;
+        int np = 0;
+        return launch_lm<LM_WRITE | LM_STATS>(c, st, c->hd, W_lm, n_rows, lp, &np);
+    }
     GemmBigParams gp{};
     gp.logits = logits;
     gp.ld_out = ld_out;

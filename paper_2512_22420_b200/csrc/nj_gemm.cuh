@@ -136,5 +136,6 @@ __device__ __forceinline__ void push_fallback(int32_t* fb_count, int32_t* fb_lis
 
 #include "nj_fused.cuh"
 #include "nj_gemm_big.cuh"
+#include "nj_lmhead.cuh"
 
 }  // namespace nj

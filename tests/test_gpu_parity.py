@@ -262,10 +262,11 @@ def test_twopass_c3_large_batch_sampled():
 
 
 def test_twopass_above_staged_limit():
-    """N > 512 (AUTO picks two-pass): B=140, gamma=3 -> N=560, K-A over 420 rows in 2 chunks."""
+    """Two-pass at N > 512: B=140, gamma=3 -> N=560, K-A over 420 rows in 2 chunks
+    (AUTO takes the staged k_lmhead pass up to 2048 rows; two-pass stays the
+    path above that and of the vocab-sharded mode)."""
     b = make_batch(140, 3, V=QV, d=QD, seed=31, device=DEV, W=w_full())
-    acc, nxt, dd, v = run(b)
-    assert v.plan(b.gamma)[0] == NJ_PATH_TWOPASS
+    acc, nxt, dd, v = run(b, NJ_PATH_TWOPASS)
     check(b, acc, nxt, dd)
 
 
@@ -278,7 +279,7 @@ def test_staged_two_chunks_full_size():
     check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
 
 
-# ----------------------------------------------------------------- staged path (48 < N <= 512)
+# ----------------------------------------------------------------- staged path (48 < N <= 2048)
 @pytest.mark.parametrize("B,g,V,d", [(1, 3, 32, 16), (20, "mixed:5", 8192, 512), (40, "mixed:5", 8192, 512),
                                      (64, 3, 1000, 64), (9, 5, 777, 40), (60, 0, 4096, 128),
                                      (100, "mixed:5", 4096, 256)])
@@ -289,12 +290,13 @@ def test_staged_small(B, g, V, d):
         check(b, acc, nxt, dd, lse_tol=1e-4)
 
 
-@pytest.mark.parametrize("B,g", [(16, 3), (32, 3), (64, 3), (256, 0), (50, "mixed:5")])
+@pytest.mark.parametrize("B,g", [(16, 3), (32, 3), (64, 3), (256, 0), (50, "mixed:5"), (96, 2), (33, 3),
+                                 (128, 3), (170, 5)])
 def test_staged_full_size(B, g):
-    """C3 points in the memory-bound band at the Qwen shape, every request vs the oracle."""
+    """C3 points at the Qwen shape from the memory-bound band through the ridge
+    to the tensor-bound band (one k_lmhead pass: CTA or CTA-pair tiles, 1-6
+    token chunks, ragged last chunk), every request vs the oracle."""
     b = make_batch(B, g, V=QV, d=QD, seed=B + 17, device=DEV, W=w_full())
-    if b.N > 512:
-        pytest.skip("staged path is N <= 512")
     acc, nxt, dd, v = run(b)
     assert v.plan(b.gamma)[0] == (NJ_PATH_FUSED if b.N <= 48 else NJ_PATH_STAGED)
     check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
