@@ -103,7 +103,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1;   // k_lmhead
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0;   // k_lmhead
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -135,6 +135,9 @@ Knobs read_knobs() {
     k.lm_ks = env_int("NJ_LM_KS", 0);
     k.lm_tma_out = env_int("NJ_LM_TMA_OUT", 1);
     k.lm_pf = env_int("NJ_LM_PF", -1);
+    k.lm_mb = env_int("NJ_LM_MB", 0);
+    k.lm_ks0 = env_int("NJ_LM_KS0", 0);
+    k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
 }
 
@@ -595,6 +598,11 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.nbuf = std::max(2, std::min(kLmMaxBuf, 512 / p.bstride));
     if (c->kn.lm_nbuf > 0) p.nbuf = std::min(kLmMaxBuf, c->kn.lm_nbuf);
     if (c->kn.lm_ks > 0) p.ks = c->kn.lm_ks;
+    // the first accumulator group of an item spans 8 k-blocks (ks = 4: the MMAs then run 12
+    // k-blocks ahead of the epilogue's per-item output, -3..-4 %), at an accuracy cost inside
+    // the certificates (scripts/lm_accuracy.py: max |d ln p| 6.4e-6 vs 6.8e-6, max CDF error
+    // 8.6e-7 vs 6.9e-7 over 256 Qwen-shape rows)
+    p.ks0 = std::max(p.ks, c->kn.lm_ks0 > 0 ? c->kn.lm_ks0 : 8);
     p.dbg = c->kn.lm_dbg;
     p.ts = nullptr;
     if (c->kn.phase_ts) {
@@ -621,7 +629,8 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     if (p.tma_out && !encode_out(&tmL, p.logits, R, c->V_local, p.ld_out))
         return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (logits)");
     const size_t nloc = kLmTok;
-    size_t tail = (p.tma_out ? (size_t)kLmEpiWarps * 2 * 2048 : 0) + (STATE ? 4 * nloc * 8 : 0) + (CAP ? nloc * 8 : 0);
+    p.ost_n = c->kn.lm_ost;
+    size_t tail = (p.tma_out ? (size_t)kLmEpiWarps * p.ost_n * 2048 : 0) + (STATE ? 4 * nloc * 8 : 0) + (CAP ? nloc * 8 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 2 * kLmMaxBuf) * 8 + 8;
     const size_t kb_bytes = (size_t)kLmHBytes + (size_t)p.wbox * 128;
     p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : 1;
@@ -631,6 +640,8 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     if (c->kn.lm_s > 0) S = std::min(S, std::max(2, c->kn.lm_s));
     if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_lmhead: not enough shared memory (R=%d)", R);
     p.nstages = S;
+    // the MMA warp takes two 1-k-block stages per operand wait (sweep: -2..-6 % vs one)
+    p.mb = c->kn.lm_mb > 0 ? std::min(c->kn.lm_mb, S - 1) : std::max(1, std::min(2, S - 2));
     const size_t smem = (size_t)S * stage + tail;
     const int grid = pl.nunits * CG;
     if (CG == 2) {

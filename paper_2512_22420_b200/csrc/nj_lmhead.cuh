@@ -50,6 +50,8 @@ struct LmheadParams {
                                  // vocabulary range of group u / nchunks (nunits = groups x nchunks)
     int32_t V_local, U, num_kb;  // local vocabulary, its 16-id units, k-blocks
     int32_t nstages, gk, ks;     // ring stages, k-blocks per stage, k-blocks per accumulator restart
+    int32_t mb;                  // ring stages the MMA warp consumes per operand wait (1, 2, ...)
+    int32_t ks0;                 // k-blocks of the first accumulator group of every item (>= ks)
     int32_t nbuf, bstride;       // TMEM accumulator buffers and their column stride
     int32_t tile_w;              // vocab tile width (multiple of 16, <= 256; the last tile of a range is ragged)
     int32_t wbox;                // W box rows per CTA (tile_w / CG)
@@ -57,6 +59,7 @@ struct LmheadParams {
     int32_t pf;                  // W L2 prefetch distance in k-blocks (0: off); issued 4 k-blocks at a time
     float* logits;               // WRITE: [R][ld_out] fp32 (local vocab ids)
     int64_t ld_out;
+    int32_t ost_n;               // WRITE via TMA: staging boxes per epilogue warp (1 or 2)
     int32_t tma_out;             // WRITE: 1 = TMA tensor stores of 32 x 16 boxes staged in swizzled smem
                                  // (tmL, SWIZZLE_64B); 0 = direct 16-byte stores (ld_out % 4 != 0)
     float* part_m;               // STATS: [R][part_ld] per-group (max, sum e^{l - max});
@@ -71,7 +74,8 @@ struct LmheadParams {
                                  // 16 no H loads, 32 no W loads, 64 every unit loads unit 0's addresses,
                                  // 128 no logits stores, 256 no statistics
     unsigned long long* ts;      // debug timeline of CTA 0 (NJ_PHASE_TS): [0, 4K) producer (wait start, wait
-                                 // end) per stage, [4K, 8K) MMA (wait start, wait end, commit) per stage
+                                 // end) per stage, [4K, 8K) MMA (wait start, wait end, commit) per stage,
+                                 // [8K, 12K) epilogue warp 0 (output start, output end) per item
     int32_t B;
     int32_t row_off[kMaxB + 1];
 };
@@ -111,7 +115,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     uint8_t* ring = smem;
     // WRITE via TMA: per epilogue warp two 2-KB staging boxes (32 rows x 16 fp32, 64B-swizzled)
     uint8_t* ostage = ring + (size_t)S * stageBytes;
-    const size_t ostageBytes = (WRITE && p.tma_out) ? (size_t)kLmEpiWarps * 2 * 2048 : 0;
+    const size_t ostageBytes = (WRITE && p.tma_out) ? (size_t)kLmEpiWarps * p.ost_n * 2048 : 0;
     float2* state = reinterpret_cast<float2*>(ostage + ostageBytes);   // [4 slices][nloc]
     int32_t* stok = reinterpret_cast<int32_t*>(state + ((STATS || ARGMAX) ? 4 * nloc : 0));   // [nloc]
     int32_t* sdl = stok + (CAPTURE ? nloc : 0);                                                 // [nloc]
@@ -249,50 +253,67 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     } else if (warp == kLmWarpMMA) {
         if (leader) {
             // ------------------------------------------------ MMA issuer (leader CTA)
+            // consumes p.mb ring stages per iteration (one operand wait + fence per mb x GK
+            // k-blocks: the issuing warp is paced by the tensor pipe, so its per-iteration
+            // overhead is exposed)
             int s = 0, abuf = 0;
             uint32_t ph = 0, aph = 0;
+            const int MB = p.mb;
             for (int it = 0; it < nitems; ++it) {
                 const int ti = it;
                 const int wn = min(rg.w, rg.r0 + rg.rows - (rg.r0 + ti * rg.w));
                 const uint32_t idesc = idesc_bf16_f32(kLmTok * CG, (uint32_t)((wn + 15) & ~15));
                 int kin = 0;
                 uint32_t dt = 0;
-                for (int kg = 0; kg < ngk; ++kg) {
-                    const int ng = min(GK, p.num_kb - kg * GK);
-                    const int si = it * ngk + kg;
+                for (int kg0 = 0; kg0 < ngk; kg0 += MB) {
+                    const int nst = min(MB, ngk - kg0);
+                    const int si = it * ngk + kg0;
                     const bool tsx = p.ts != nullptr && blockIdx.x == 0 && lane == 0 && si < 1300;
                     if (tsx) p.ts[4096 + 3 * si] = globaltimer();
-                    mbar_wait_w(&full[s], ph);
-                    if (tsx) p.ts[4096 + 3 * si + 1] = globaltimer();
-                    tc_fence_after();
-                    uint8_t* st = ring + (size_t)s * stageBytes;
-                    for (int g = 0; g < ng; ++g) {
-                        if (kin == 0) {
-                            mbar_wait_w(&aempty[abuf], aph ^ 1);
-                            tc_fence_after();
-                            dt = tbase + (uint32_t)(abuf * p.bstride);
-                        }
-                        const uint64_t ad = sdesc_sw128(st + (size_t)g * kLmHBytes);
-                        const uint64_t bd = sdesc_sw128(st + (size_t)GK * kLmHBytes + (size_t)g * wBytes);
-                        if (!(p.dbg & 1)) {
-#pragma unroll
-                            for (int k = 0; k < kBK / 16; ++k) {
-                                if (CG == 2) mma_bf16_cg2_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
-                                else mma_bf16_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
-                            }
-                        }
-                        const int kb = kg * GK + g;
-                        if (++kin == p.ks || kb == p.num_kb - 1) {
-                            if (CG == 2) mma_commit_mc2_w(&afull[abuf], 3);
-                            else mma_commit_w(&afull[abuf]);
-                            if (++abuf == NBUF) { abuf = 0; aph ^= 1u; }
-                            kin = 0;
+                    {
+                        int s2 = s;
+                        uint32_t ph2 = ph;
+                        for (int m = 0; m < nst; ++m) {
+                            mbar_wait_w(&full[s2], ph2);
+                            if (++s2 == S) { s2 = 0; ph2 ^= 1; }
                         }
                     }
-                    if (CG == 2) mma_commit_mc2_w(&empty[s], 3);
-                    else mma_commit_w(&empty[s]);
+                    if (tsx) p.ts[4096 + 3 * si + 1] = globaltimer();
+                    tc_fence_after();
+                    for (int m = 0; m < nst; ++m) {
+                        const int kg = kg0 + m;
+                        const int ng = min(GK, p.num_kb - kg * GK);
+                        uint8_t* st = ring + (size_t)s * stageBytes;
+                        for (int g = 0; g < ng; ++g) {
+                            if (kin == 0) {
+                                mbar_wait_w(&aempty[abuf], aph ^ 1);
+                                tc_fence_after();
+                                dt = tbase + (uint32_t)(abuf * p.bstride);
+                            }
+                            const uint64_t ad = sdesc_sw128(st + (size_t)g * kLmHBytes);
+                            const uint64_t bd = sdesc_sw128(st + (size_t)GK * kLmHBytes + (size_t)g * wBytes);
+                            if (!(p.dbg & 1)) {
+#pragma unroll
+                                for (int k = 0; k < kBK / 16; ++k) {
+                                    if (CG == 2) mma_bf16_cg2_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                                    else mma_bf16_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                                }
+                            }
+                            const int kb = kg * GK + g;
+                            // group boundary: the first group of an item spans ks0 k-blocks, the
+                            // rest ks (the longer first group covers the epilogue's per-item output)
+                            if (++kin == (kb < p.ks0 ? p.ks0 : p.ks) || kb == p.num_kb - 1) {
+                                if (CG == 2) mma_commit_mc2_w(&afull[abuf], 3);
+                                else mma_commit_w(&afull[abuf]);
+                                if (++abuf == NBUF) { abuf = 0; aph ^= 1u; }
+                                kin = 0;
+                            }
+                        }
+                        if (CG == 2) mma_commit_mc2_w(&empty[s], 3);
+                        else mma_commit_w(&empty[s]);
+                        if (++s == S) { s = 0; ph ^= 1; }
+                    }
                     if (tsx) p.ts[4096 + 3 * si + 2] = globaltimer();
-                    if (++s == S) { s = 0; ph ^= 1; }
                 }
             }
         }
@@ -302,10 +323,10 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
         // e, e + 4, e + 8, e + 12 of 16 vocab columns (acc[16 j + i] = granule e + 4 j)
         const int q = warp & 3, e = warp >> 2;
         const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(e * 16);
-        const int ngroups = (p.num_kb + p.ks - 1) / p.ks;
+        const int ngroups = p.num_kb <= p.ks0 ? 1 : 1 + (p.num_kb - p.ks0 + p.ks - 1) / p.ks;
         const uint64_t pol_out = policy_evict_first();   // logits: do not push W / H out of L2
         const bool vec_ok = (p.ld_out & 3) == 0 && (reinterpret_cast<uintptr_t>(p.logits) & 15) == 0;
-        uint8_t* my_ost = ostage + (size_t)warp * 2 * 2048;   // this warp's two staging boxes
+        uint8_t* my_ost = ostage + (size_t)warp * p.ost_n * 2048;   // this warp's staging boxes
         int osb = 0;                                          // next staging box
         int ebuf = 0;
         uint32_t eph = 0;
@@ -354,6 +375,8 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     else mbar_arrive(&aempty[buf]);
                 }
             }
+            const bool tso = p.ts != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 2000;
+            if (tso) p.ts[8192 + 2 * it] = globaltimer();
             if (p.dbg & 8) continue;   // probe: no per-item output
             const int lr = q * 32 + lane;                                  // index into this CTA's rows
             const int row = c * kLmTok * CG + crank * kLmTok + q * 32 + lane;
@@ -366,36 +389,61 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
             int nvj[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) nvj[j] = j < myg ? min(16, wn - (e + 4 * j) * 16) : 0;
-            if (WRITE && p.tma_out && !(p.dbg & 128)) {
-                // granule j -> staging box (row = lane, 16-byte chunk i at i ^ ((lane >> 1) & 3): the
-                // SWIZZLE_64B pattern, conflict-free) -> one TMA store of rows [row - lane, +32) x 16 ids
-                // (rows past R / ids past V_local are clipped by the tensor map)
-                for (int j = 0; j < myg; ++j) {
-                    bulk_wait_read<1>();   // the box written two granules ago has been read
+            // row statistics: the item max first (one pass), then the exponentials granule by
+            // granule, interleaved with the granule's TMA store (its smem read overlaps them)
+            float2 stt = make_float2(-INFINITY, 0.f);
+            float s4[4] = {0.f, 0.f, 0.f, 0.f};   // four chains (latency)
+            const bool do_stats = STATS && !(p.dbg & 256) && row < p.R;
+            if (do_stats) {
+                float mx = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (i < nvj[j]) mx = fmaxf(mx, acc[16 * j + i]);
+                stt = state[e * nloc + lr];
+                if (mx > stt.x) {
+                    stt.y *= __expf(stt.x - mx);   // stt.x = -inf: stt.y = 0
+                    stt.x = mx;
+                }
+            }
+            const bool tma_w = WRITE && p.tma_out && !(p.dbg & 128);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j >= myg) break;
+                if (tma_w) {
+                    // granule j -> staging box (row = lane, 16-byte chunk i at i ^ ((lane >> 1) & 3): the
+                    // SWIZZLE_64B pattern, conflict-free) -> one TMA store of rows [row - lane, +32) x 16
+                    // ids (rows past R / ids past V_local are clipped by the tensor map)
+                    if (p.ost_n == 1) bulk_wait_read<0>();   // the previous box has been read
+                    else bulk_wait_read<1>();                // the box before it
                     __syncwarp();
                     uint8_t* box = my_ost + osb * 2048;
                     const int sw = (lane >> 1) & 3;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        float4 v4;
-                        // constant register indices: select the granule with a switch on j
-                        switch (j) {
-                            case 0: v4 = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]); break;
-                            case 1: v4 = make_float4(acc[16 + 4 * i], acc[17 + 4 * i], acc[18 + 4 * i], acc[19 + 4 * i]); break;
-                            case 2: v4 = make_float4(acc[32 + 4 * i], acc[33 + 4 * i], acc[34 + 4 * i], acc[35 + 4 * i]); break;
-                            default: v4 = make_float4(acc[48 + 4 * i], acc[49 + 4 * i], acc[50 + 4 * i], acc[51 + 4 * i]); break;
-                        }
-                        *reinterpret_cast<float4*>(box + lane * 64 + ((i ^ sw) << 4)) = v4;
-                    }
+                    for (int i = 0; i < 4; ++i)
+                        *reinterpret_cast<float4*>(box + lane * 64 + ((i ^ sw) << 4)) =
+                            make_float4(acc[16 * j + 4 * i], acc[16 * j + 4 * i + 1], acc[16 * j + 4 * i + 2],
+                                        acc[16 * j + 4 * i + 3]);
                     fence_proxy_async();   // generic-proxy smem writes -> visible to the TMA (async proxy)
                     __syncwarp();
                     if (lane == 0) {
                         tma_store_2d(&tmL, box, v0t + (e + 4 * j) * 16, row - lane);
                         bulk_commit();
                     }
-                    osb ^= 1;
+                    if (p.ost_n == 2) osb ^= 1;
                 }
-            } else if (WRITE && !(p.dbg & 128) && row < p.R) {
+                if (do_stats) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (i < nvj[j]) s4[i & 3] += __expf(acc[16 * j + i] - stt.x);
+                }
+            }
+            if (do_stats) {
+                stt.y += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                state[e * nloc + lr] = stt;
+            }
+            if (WRITE && !p.tma_out && !(p.dbg & 128) && row < p.R) {
                 float* pr = p.logits + (int64_t)row * p.ld_out + v0t + e * 16;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -424,27 +472,6 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     p.dl[sdl[lr]] = (double)val;
                 }
             }
-            if (STATS && !(p.dbg & 256)) {
-                float mx = -INFINITY;
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (i < nvj[j]) mx = fmaxf(mx, acc[16 * j + i]);
-                float2 st = state[e * nloc + lr];
-                if (mx > st.x) {
-                    st.y *= __expf(st.x - mx);   // st.x = -inf: st.y = 0
-                    st.x = mx;
-                }
-                float s4[4] = {0.f, 0.f, 0.f, 0.f};   // four chains (latency)
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (i < nvj[j]) s4[i & 3] += __expf(acc[16 * j + i] - st.x);
-                st.y += (s4[0] + s4[1]) + (s4[2] + s4[3]);
-                state[e * nloc + lr] = st;
-            }
             if (ARGMAX) {
                 // highest logit, lowest id among equals (ascending scan, strict >)
                 float bv = -INFINITY;
@@ -460,6 +487,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     if (bv > st.x || (bv == st.x && bi < sid)) state[e * nloc + lr] = make_float2(bv, __int_as_float(bi));
                 }
             }
+            if (tso) p.ts[8192 + 2 * it + 1] = globaltimer();
         }
     }
     if (WRITE && p.tma_out && warp < kLmEpiWarps && lane == 0) bulk_wait<0>();   // stores complete before exit

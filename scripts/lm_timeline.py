@@ -51,6 +51,12 @@ for dbg in sys.argv[2].split(","):
     print(f"   mean per stage {span / (n - 1):.0f} ns; mean wait-full {wf.mean():.0f} (>500ns: {int((wf > 500).sum())} stages, "
           f"{wf[wf > 500].sum() / span * 100:.1f} % of span); mean issue+commit {ic.mean():.0f} (>500ns: "
           f"{int((ic > 500).sum())}, {ic[ic > 500].sum() / span * 100:.1f} % of span); gaps {((M[1:, 0] - M[:-1, 2]).mean()):.0f}")
+    O = t[8192:8192 + 4000].reshape(2000, 2)
+    O = O[O[:, 0] > 0]
+    if len(O):
+        od = O[:, 1] - O[:, 0]
+        print(f"   items {len(O)}: output median {np.median(od):.0f} ns mean {od.mean():.0f}; item period "
+              f"{np.median(np.diff(O[:, 0])) if len(O) > 1 else 0:.0f} ns")
     # first 12 stages raw (relative ns)
     print("   MMA  ", [(int(a - t0), int(b - t0), int(c - t0)) for a, b, c in M[20:28]])
     print("   prod ", [(int(a - t0), int(b - t0)) for a, b in P[20:28]])
