@@ -1134,6 +1134,8 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS | LM_CAPTURE, 2>);
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 1>);
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 2>);
+    e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 1>);
+    e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 2>);
     if (const char* ev = getenv("NJ_MASS_NST")) c->mass_nst = std::min(4, std::max(2, atoi(ev)));
     e = e ? e : cudaFuncSetAttribute(k_mass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(2, c->cfg.max_batch));
     e = e ? e : cudaFuncSetAttribute(k_mass<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(3, c->cfg.max_batch));
@@ -1488,6 +1490,28 @@ nj_status nj_verify_greedy(nj_ctx* c, void* stream, const uint16_t* hidden, cons
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     // all N rows through the LM-head GEMM in blocks of the staged logits buffer
     // (one W stream per block), fp32 logits -> row argmax
+    if (c->kn.lm) {
+        // k_lmhead with the row argmax in its epilogue (no logits written), blocks of
+        // kStagedMaxRows rows, per-group partials merged into the argmax keys
+        for (int r0 = 0; r0 < pl.N; r0 += kStagedMaxRows) {
+            const int R = std::min(kStagedMaxRows, pl.N - r0);
+            LmheadParams lp{};
+            lp.part_m = c->part_m;
+            lp.part_s = c->part_s;
+            lp.inv_t = 1.f;
+            int np = 0;
+            std::pair<cudaEvent_t, cudaEvent_t> ev;
+            if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
+            if ((s = launch_lm<LM_ARGMAX>(c, st, hidden + (size_t)r0 * c->cfg.d, W_lm, R, lp, &np)) != NJ_OK) return s;
+            if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
+            k_argmax_merge<<<(R + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, np, R, c->amax + r0);
+            NJ_LAUNCHED(c, "k_argmax_merge", st);
+        }
+        const ReqMeta meta = make_meta(pl);
+        k_greedy_decide<<<(B + 127) / 128, 128, 0, st>>>(meta, draft_tokens, c->amax, accept_len, next_token);
+        NJ_LAUNCHED(c, "k_greedy_decide", st);
+        return NJ_OK;
+    }
     const int cap = std::min(c->Nmax, kStagedMaxN);   // k_gemm_big blocks
     NJ_CUDA(c, cudaMemsetAsync(c->amax, 0, (size_t)pl.N * sizeof(unsigned long long), st));
     for (int r0 = 0; r0 < pl.N; r0 += cap) {
@@ -1526,13 +1550,20 @@ nj_status nj_propose(nj_ctx* c, void* stream, const uint16_t* hidden, const uint
     // draft LM head: fp32 logits straight into q_out + per-CTA (max, sum) partials
     int grid = c->grid;
     {
-        GemmBigParams gp{};
-        gp.logits = q_out; gp.ld_out = ldq;
-        gp.part_m = c->part2_m; gp.part_s = c->part2_s;
-        const bool rr = B > kBigMaxT;
         std::pair<cudaEvent_t, cudaEvent_t> ev;
         if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
-        if ((s = launch_lmhead<true, true, false>(c, st, hidden, B, gp, rr, &grid)) != NJ_OK) return s;
+        if (c->kn.lm) {
+            LmheadParams lp{};
+            lp.logits = q_out; lp.ld_out = ldq;
+            lp.part_m = c->part2_m; lp.part_s = c->part2_s;
+            if ((s = launch_lm<LM_WRITE | LM_STATS>(c, st, hidden, W_lm, B, lp, &grid)) != NJ_OK) return s;
+        } else {
+            GemmBigParams gp{};
+            gp.logits = q_out; gp.ld_out = ldq;
+            gp.part_m = c->part2_m; gp.part_s = c->part2_s;
+            const bool rr = B > kBigMaxT;
+            if ((s = launch_lmhead<true, true, false>(c, st, hidden, B, gp, rr, &grid)) != NJ_OK) return s;
+        }
         if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
     }
     k_lse_rows<<<(B + 7) / 8, 256, 0, st>>>(c->part2_m, c->part2_s, c->pld, grid, B, c->row_lse);

@@ -63,7 +63,7 @@ struct LmheadParams {
     int32_t tma_out;             // WRITE: 1 = TMA tensor stores of 32 x 16 boxes staged in swizzled smem
                                  // (tmL, SWIZZLE_64B); 0 = direct 16-byte stores (ld_out % 4 != 0)
     float* part_m;               // STATS: [R][part_ld] per-group (max, sum e^{l - max});
-    float* part_s;               // ARGMAX: (max, id as int bits)
+    float* part_s;               // ARGMAX: (order-preserving uint32 of the max as float bits, id as int bits)
     int32_t part_ld;
     const int32_t* tok;          // CAPTURE: draft tokens (global ids)
     double* dl;                  // CAPTURE: fp64 draft logits
@@ -156,7 +156,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     }
     if (STATS || ARGMAX)
         for (int i = threadIdx.x; i < 4 * nloc; i += kLmThreads)
-            state[i] = make_float2(-INFINITY, ARGMAX ? __int_as_float(0x7fffffff) : 0.f);
+            state[i] = ARGMAX ? make_float2(__uint_as_float(0u), __int_as_float(0x7fffffff)) : make_float2(-INFINITY, 0.f);
     if (CAPTURE)
         for (int i = threadIdx.x; i < nloc; i += kLmThreads) {
             const int row = cfix * kLmTok * CG + crank * kLmTok + i;
@@ -473,18 +473,26 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                 }
             }
             if (ARGMAX) {
-                // highest logit, lowest id among equals (ascending scan, strict >)
-                float bv = -INFINITY;
+                // highest logit, lowest id among equals: values compared as order-preserving
+                // uint32 (the key of k_argmax_rows / the oracle's argmax, -0 < +0), ascending
+                // scan with strict > inside the item, (ord, -id) merge into the row state
+                uint32_t bo = 0u;
                 int bi = -1;
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
-                        if (i < nvj[j] && acc[16 * j + i] > bv) { bv = acc[16 * j + i]; bi = v0t + (e + 4 * j) * 16 + i; }
+                        if (i < nvj[j]) {
+                            const uint32_t u = __float_as_uint(acc[16 * j + i]);
+                            const uint32_t o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+                            if (bi < 0 || o > bo) { bo = o; bi = v0t + (e + 4 * j) * 16 + i; }
+                        }
                 if (bi >= 0) {
-                    float2 st = state[e * nloc + lr];
+                    const float2 st = state[e * nloc + lr];
+                    const uint32_t so = __float_as_uint(st.x);
                     const int sid = __float_as_int(st.y);
-                    if (bv > st.x || (bv == st.x && bi < sid)) state[e * nloc + lr] = make_float2(bv, __int_as_float(bi));
+                    if (bo > so || (bo == so && bi < sid))
+                        state[e * nloc + lr] = make_float2(__uint_as_float(bo), __int_as_float(bi));
                 }
             }
             if (tso) p.ts[8192 + 2 * it + 1] = globaltimer();
@@ -501,7 +509,8 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
             for (int e = 1; e < 4; ++e) {
                 const float2 b = state[e * nloc + i];
                 if (ARGMAX) {
-                    if (b.x > a.x || (b.x == a.x && __float_as_int(b.y) < __float_as_int(a.y))) a = b;
+                    const uint32_t ao = __float_as_uint(a.x), bo = __float_as_uint(b.x);
+                    if (bo > ao || (bo == ao && __float_as_int(b.y) < __float_as_int(a.y))) a = b;
                 } else {
                     ms_merge(a.x, a.y, b.x, b.y);
                 }

@@ -521,6 +521,27 @@ __global__ void __launch_bounds__(256) k_argmax_rows(const float* __restrict__ l
 // u q(x) < p(x) accepts x_i iff x_i == a_i; the residual max(0, p - q) of the
 // first rejected row n is one-hot at a_n, and the bonus row gives a_gamma, so
 // next_token = a_n in every case.  Thread per request.
+// k_lmhead ARGMAX partials (per row, one per unit group: ordered value bits, id) -> the
+// row's 64-bit argmax key (same ordering as argmax_key); warp per row
+__global__ void k_argmax_merge(const float* __restrict__ pm, const float* __restrict__ ps, int pld, int nparts,
+                               int n, unsigned long long* __restrict__ keys) {
+    const int r = blockIdx.x * (blockDim.x / 32) + (int)(threadIdx.x >> 5);
+    if (r >= n) return;
+    unsigned long long best = 0ull;
+    for (int c = (int)(threadIdx.x & 31); c < nparts; c += 32) {
+        const uint32_t o = __float_as_uint(pm[(int64_t)r * pld + c]);
+        const int id = __float_as_int(ps[(int64_t)r * pld + c]);
+        if (o == 0u) continue;   // a group without ids of this row
+        const unsigned long long k = ((unsigned long long)o << 32) | (unsigned long long)(0xffffffffu - (uint32_t)id);
+        best = k > best ? k : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, best, o);
+        best = k2 > best ? k2 : best;
+    }
+    if ((threadIdx.x & 31) == 0) keys[r] = best;
+}
 __device__ __forceinline__ int argmax_of_key(unsigned long long k) {
     return (int)(0xffffffffu - (uint32_t)(k & 0xffffffffull));
 }
