@@ -341,7 +341,11 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
             for (int j = 0; j < kLmNC; ++j) acc[j] = 0.f;
             for (int g = 0; g < ngroups; ++g) {
                 const int buf = ebuf;
+                const int gi = it * ngroups + g;
+                const bool tsg = p.ts != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0 && gi < 1000;
+                if (tsg) p.ts[12288 + 2 * gi] = globaltimer();
                 mbar_wait(&afull[buf], eph);
+                if (tsg) p.ts[12288 + 2 * gi + 1] = globaltimer();
                 if (++ebuf == NBUF) { ebuf = 0; eph ^= 1; }
                 tc_fence_after();
                 const uint32_t ta = lane_base + (uint32_t)(buf * p.bstride);
@@ -374,6 +378,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     if (CG == 2) mbar_arrive_cluster(mapa_shared(&aempty[buf], 0));
                     else mbar_arrive(&aempty[buf]);
                 }
+                if (tsg) p.ts[14336 + gi] = globaltimer();
             }
             const bool tso = p.ts != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0 && it < 2000;
             if (tso) p.ts[8192 + 2 * it] = globaltimer();

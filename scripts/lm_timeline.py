@@ -36,7 +36,9 @@ for dbg in sys.argv[2].split(","):
     t = ts.astype(np.int64)
     P = t[:4000].reshape(2000, 2)
     M = t[4096:4096 + 3 * 1300].reshape(1300, 3)
-    n = int((M[:, 0] > 0).sum())
+    M = M[M[:, 0] > 0]          # (MB > 1 stamps every MB-th stage)
+    P = P[P[:, 0] > 0]
+    n = min(len(M), len(P))
     M = M[:n]
     P = P[:n]
     t0 = M[0, 0]
@@ -51,12 +53,22 @@ for dbg in sys.argv[2].split(","):
     print(f"   mean per stage {span / (n - 1):.0f} ns; mean wait-full {wf.mean():.0f} (>500ns: {int((wf > 500).sum())} stages, "
           f"{wf[wf > 500].sum() / span * 100:.1f} % of span); mean issue+commit {ic.mean():.0f} (>500ns: "
           f"{int((ic > 500).sum())}, {ic[ic > 500].sum() / span * 100:.1f} % of span); gaps {((M[1:, 0] - M[:-1, 2]).mean()):.0f}")
-    O = t[8192:8192 + 4000].reshape(2000, 2)
+    O = t[8192:8192 + 4000].reshape(2000, 2)[:1900]
     O = O[O[:, 0] > 0]
     if len(O):
         od = O[:, 1] - O[:, 0]
         print(f"   items {len(O)}: output median {np.median(od):.0f} ns mean {od.mean():.0f}; item period "
               f"{np.median(np.diff(O[:, 0])) if len(O) > 1 else 0:.0f} ns")
+    Gs = t[12288:12288 + 2000].reshape(1000, 2)
+    ng = int((Gs[:, 0] > 0).sum())
+    Gs = Gs[:ng]
+    A = t[14336:14336 + ng]
+    if ng > 2:
+        wait = Gs[:, 1] - Gs[:, 0]
+        drain = A - Gs[:len(A), 1]
+        print(f"   epilogue warp0 groups {ng}: afull wait median {np.median(wait):.0f} ns mean {wait.mean():.0f}; "
+              f"drain (wait end -> arrive) median {np.median(drain):.0f} ns mean {drain.mean():.0f}; group period "
+              f"{np.median(np.diff(Gs[:, 1])):.0f} ns")
     # first 12 stages raw (relative ns)
     print("   MMA  ", [(int(a - t0), int(b - t0), int(c - t0)) for a, b, c in M[20:28]])
     print("   prod ", [(int(a - t0), int(b - t0)) for a, b in P[20:28]])

@@ -49,6 +49,14 @@ for name, B, g, V, d, path, fb in [("fused", 6, "mixed:5", 2048, 128, NJ_PATH_FU
     b = make_batch(B, g, V=V, d=d, seed=B, device=dev)
     run(b, path, fb)
     print(name, "ok", flush=True)
+# k_lmhead in both CTA-group modes, several token chunks, ragged vocab / rows (staged path)
+import os  # noqa: E402
+for cg in ("1", "2"):
+    os.environ["NJ_LM_CG"] = cg
+    b = make_batch(75, 3, V=4093, d=256, seed=11, device=dev)   # N = 300: 3 (CTA) / 2 (pair) chunks
+    run(b, NJ_PATH_STAGED)
+    print("staged k_lmhead cg" + cg, "ok", flush=True)
+os.environ.pop("NJ_LM_CG", None)
 b = make_batch(6, "mixed:4", V=2048, d=128, seed=5, device=dev)
 grp = ShardGroup(128, 2048, max_batch=6, gamma_max=5, nshards=4)
 acc = torch.empty(6, dtype=torch.int32, device=dev)
