@@ -103,7 +103,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0;   // k_lmhead
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0;   // k_lmhead
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -137,6 +137,9 @@ Knobs read_knobs() {
     k.lm_pf = env_int("NJ_LM_PF", -1);
     k.lm_mb = env_int("NJ_LM_MB", 0);
     k.lm_ks0 = env_int("NJ_LM_KS0", 0);
+    k.lm_arv1 = env_int("NJ_LM_ARV1", 0);
+    k.lm_w = std::min(256, env_int("NJ_LM_W", 0) & ~15);   // probe: fixed tile width (ragged last tile)
+    k.lm_fence = env_int("NJ_LM_FENCE", 0);
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
 }
@@ -565,7 +568,7 @@ LmPlan lm_plan(const nj_ctx* c, int R) {
         const int upu = (c->U + ngroups - 1) / ngroups;   // 16-id units of the largest range
         const int rows = std::min(upu * kUnit, c->V_local);
         const int ntile = (rows + c->kn.lm_tw - 1) / c->kn.lm_tw;
-        const int w = ((rows + ntile - 1) / ntile + 15) & ~15;
+        const int w = c->kn.lm_w > 0 ? c->kn.lm_w : ((rows + ntile - 1) / ntile + 15) & ~15;
         const double mma = 2.0 * w, l2 = (kLmHBytes + (double)(w / cg) * 128.0) / 50.0;
         if (nch > c->num_sms / cg) continue;   // (R > 148 chunks: never at kStagedMaxRows)
         const double t = (double)ntile * (nkb * std::max(mma, l2) + 3000.0);
@@ -603,6 +606,8 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     // the certificates (scripts/lm_accuracy.py: max |d ln p| 6.4e-6 vs 6.8e-6, max CDF error
     // 8.6e-7 vs 6.9e-7 over 256 Qwen-shape rows)
     p.ks0 = std::max(p.ks, c->kn.lm_ks0 > 0 ? c->kn.lm_ks0 : 8);
+    p.arv1 = c->kn.lm_arv1;
+    p.fence_full = c->kn.lm_fence;
     p.dbg = c->kn.lm_dbg;
     p.ts = nullptr;
     if (c->kn.phase_ts) {
@@ -633,7 +638,9 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     size_t tail = (p.tma_out ? (size_t)kLmEpiWarps * p.ost_n * 2048 : 0) + (STATE ? 4 * nloc * 8 : 0) + (CAP ? nloc * 8 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 2 * kLmMaxBuf) * 8 + 8;
     const size_t kb_bytes = (size_t)kLmHBytes + (size_t)p.wbox * 128;
-    p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : 1;
+    // CTA pair, one token chunk (R <= 256): 2-k-block ring stages (W streamed once; -7 % at R = 256);
+    // several: 1-k-block stages, the MMA warp taking two per operand wait (equal or better there)
+    p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : (pl.nchunks == 1 && CG == 2 ? 2 : 1);
     while (p.gk > 1 && (kSmemLimit - tail - 1024) / ((size_t)p.gk * kb_bytes) < 2) --p.gk;
     const size_t stage = (size_t)p.gk * kb_bytes;
     int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);

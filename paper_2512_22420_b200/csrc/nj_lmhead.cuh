@@ -52,6 +52,8 @@ struct LmheadParams {
     int32_t nstages, gk, ks;     // ring stages, k-blocks per stage, k-blocks per accumulator restart
     int32_t mb;                  // ring stages the MMA warp consumes per operand wait (1, 2, ...)
     int32_t ks0;                 // k-blocks of the first accumulator group of every item (>= ks)
+    int32_t arv1;                // 1: one accumulator-release arrival per CTA (named barrier first)
+    int32_t fence_full;          // probe: tcgen05.fence::after_thread_sync after every operand wait
     int32_t nbuf, bstride;       // TMEM accumulator buffers and their column stride
     int32_t tile_w;              // vocab tile width (multiple of 16, <= 256; the last tile of a range is ragged)
     int32_t wbox;                // W box rows per CTA (tile_w / CG)
@@ -146,7 +148,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
         tma_prefetch_desc(&tmH);
         if (WRITE && p.tma_out) tma_prefetch_desc(&tmL);
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int g = 0; g < NBUF; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], kLmEpiWarps * CG); }
+        for (int g = 0; g < NBUF; ++g) { mbar_init(&afull[g], 1); mbar_init(&aempty[g], (p.arv1 ? 1 : kLmEpiWarps) * CG); }
         fence_barrier_init();
         fence_proxy_async();
     }
@@ -279,7 +281,9 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                         }
                     }
                     if (tsx) p.ts[4096 + 3 * si + 1] = globaltimer();
-                    tc_fence_after();
+                    // (no tcgen05 fence here: the operands are TMA-written shared memory that the
+                    // MMAs read through the async proxy; the full barrier's completion orders them)
+                    if (p.fence_full) tc_fence_after();
                     for (int m = 0; m < nst; ++m) {
                         const int kg = kg0 + m;
                         const int ng = min(GK, p.num_kb - kg * GK);
@@ -373,10 +377,19 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     }
                 }
                 tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if (CG == 2) mbar_arrive_cluster(mapa_shared(&aempty[buf], 0));
-                    else mbar_arrive(&aempty[buf]);
+                if (p.arv1) {
+                    // one arrival per CTA: the 16 epilogue warps meet at a named barrier first
+                    named_bar(1, kLmEpiWarps * 32);
+                    if (warp == 0 && lane == 0) {
+                        if (CG == 2) mbar_arrive_cluster(mapa_shared(&aempty[buf], 0));
+                        else mbar_arrive(&aempty[buf]);
+                    }
+                } else {
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (CG == 2) mbar_arrive_cluster(mapa_shared(&aempty[buf], 0));
+                        else mbar_arrive(&aempty[buf]);
+                    }
                 }
                 if (tsg) p.ts[14336 + gi] = globaltimer();
             }

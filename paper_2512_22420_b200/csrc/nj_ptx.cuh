@@ -216,8 +216,12 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
     return r;
 }
+// Relaxed: the arrivals this is used for only release TMEM reads (ordered by
+// tcgen05.wait::ld + tcgen05.fence::before_thread_sync), no shared / global data.
+// (.release.cluster compiles to MEMBAR.ALL.GPU, which waits for every prior global
+// and TMA store of the thread: ~1 us per accumulator release in k_lmhead's epilogue.)
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
