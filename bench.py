@@ -414,7 +414,7 @@ def bench_nj(args, ws, rank, local):
                 "frac": achieved / hbm, "algorithmic_bytes_per_launch": byts}
     else:
         R = N if p_used == NJ_PATH_STAGED else G / max(kn // args.steps, 1)
-        name = "k_gemm_big<logits,stats,capture> (staged, all N rows)" if p_used == NJ_PATH_STAGED else \
+        name = "k_lmhead<logits,stats,capture> (staged, all N rows)" if p_used == NJ_PATH_STAGED else \
             "k_gemm_big<stats,capture> (K-A, draft rows)"
         if R < ridge:
             byts = 2 * V_Q * D_Q + 2 * R * D_Q
@@ -866,7 +866,7 @@ def bench_propose(args, ws, rank, local):
     hbm, _, _, peak_src = load_peaks()
     kern_ms = kms / max(kn, 1)
     byts = 2 * DV * DD + 2 * B * DD + 4 * B * DV   # W once, hidden, fp32 logits written
-    roof = {"kernel": "k_gemm_big<logits,stats> (draft LM head)", "bound": "hbm",
+    roof = {"kernel": "k_lmhead<logits,stats> (draft LM head)", "bound": "hbm",
             "achieved": byts / (kern_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": byts / (kern_ms / 1e3) / 1e9 / hbm, "algorithmic_bytes_per_launch": byts,
             "peak_source": peak_src, "kernel_ms_avg": kern_ms,
@@ -948,7 +948,7 @@ def bench_greedy(args, ws, rank, local):
     acc = torch.empty(B, dtype=torch.int32, device=dev)
     nxt = torch.empty(B, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
-    nblk = -(-b.N // 512)
+    nblk = -(-b.N // 2048)   # k_lmhead blocks of <= kStagedMaxRows rows (argmax epilogue, no logits)
 
     def step():
         v.verify_greedy(b.hidden, W, b.draft_tokens, b.gamma, acc, nxt)
@@ -1000,13 +1000,13 @@ def bench_greedy(args, ws, rank, local):
     R = b.N / nblk
     ridge = tf_burst * 1e12 / (hbm * 1e9)
     if R < ridge:
-        byts = 2 * V_Q * D_Q + 2 * R * D_Q + 4 * R * V_Q
-        roof = {"kernel": "k_gemm_big<logits,stats> (all rows)", "bound": "hbm", "achieved": byts / (kern_ms / 1e3) / 1e9,
+        byts = 2 * V_Q * D_Q + 2 * R * D_Q
+        roof = {"kernel": "k_lmhead<argmax> (all rows)", "bound": "hbm", "achieved": byts / (kern_ms / 1e3) / 1e9,
                 "peak": hbm, "unit": "GB/s", "frac": byts / (kern_ms / 1e3) / 1e9 / hbm,
                 "algorithmic_bytes_per_launch": byts}
     else:
         fl = 2.0 * R * V_Q * D_Q
-        roof = {"kernel": "k_gemm_big<logits,stats> (all rows)", "bound": "tensor",
+        roof = {"kernel": "k_lmhead<argmax> (all rows)", "bound": "tensor",
                 "achieved": fl / (kern_ms / 1e3) / 1e12, "peak": tf_burst, "unit": "TFLOP/s",
                 "frac": fl / (kern_ms / 1e3) / 1e12 / tf_burst, "algorithmic_flops_per_launch": fl}
     roof.update({"peak_source": peak_src, "kernel_ms_avg": kern_ms,

@@ -549,35 +549,24 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     return NJ_OK;
 }
 
-// k_lmhead (nj_lmhead.cuh): CTA group and tile width from a cost model of one
-// unit's (pair's / CTA's) work -- per k-block and SM, max(MMA cycles 2 * w,
-// L2 -> SM operand bytes / ~50 B per cycle) over its ntile x nchunks items,
-// plus ~1.5 us of per-item output -- then the ring depth from shared memory.
+// k_lmhead (nj_lmhead.cuh): CTA group from the measured per-chunk cost (B200, Qwen
+// shape, scripts/time_lm.py): a CTA-pair chunk of 256 token rows costs ~255 us, a
+// single-CTA chunk of 128 rows ~145 us (more operand bytes per FLOP), whatever the
+// number of chunks; R <= 128 is W-stream bound and single-CTA (226 vs 264 us at
+// R = 128).  The tile width is the balanced width of the largest vocabulary range.
 struct LmPlan {
     int cg, tile_w, w, nunits, nchunks;
 };
 LmPlan lm_plan(const nj_ctx* c, int R) {
-    LmPlan best{};
-    double best_t = 1e30;
-    const int nkb = (c->cfg.d + kBK - 1) / kBK;
-    for (int cg = 1; cg <= 2; ++cg) {
-        if (c->kn.lm_cg && c->kn.lm_cg != cg) continue;
-        const int nch = (R + kLmTok * cg - 1) / (kLmTok * cg);
-        const int ngroups = std::max(1, std::min(c->num_sms / cg / nch, c->U));   // units = groups x chunks
-        const int nunits = ngroups * nch;
-        const int upu = (c->U + ngroups - 1) / ngroups;   // 16-id units of the largest range
-        const int rows = std::min(upu * kUnit, c->V_local);
-        const int ntile = (rows + c->kn.lm_tw - 1) / c->kn.lm_tw;
-        const int w = c->kn.lm_w > 0 ? c->kn.lm_w : ((rows + ntile - 1) / ntile + 15) & ~15;
-        const double mma = 2.0 * w, l2 = (kLmHBytes + (double)(w / cg) * 128.0) / 50.0;
-        if (nch > c->num_sms / cg) continue;   // (R > 148 chunks: never at kStagedMaxRows)
-        const double t = (double)ntile * (nkb * std::max(mma, l2) + 3000.0);
-        if (t < best_t * 0.98) {   // ties: the first (single-CTA) candidate
-            best_t = t;
-            best = LmPlan{cg, w, w, nunits, nch};
-        }
-    }
-    return best;
+    int cg = R <= kLmTok ? 1 : (1.13 * kLmTok * ((R + kLmTok - 1) / kLmTok) < 2.0 * kLmTok * ((R + 2 * kLmTok - 1) / (2 * kLmTok)) ? 1 : 2);
+    if (c->kn.lm_cg == 1 || c->kn.lm_cg == 2) cg = c->kn.lm_cg;
+    const int nch = (R + kLmTok * cg - 1) / (kLmTok * cg);
+    const int ngroups = std::max(1, std::min(c->num_sms / cg / nch, c->U));   // units = groups x chunks
+    const int upu = (c->U + ngroups - 1) / ngroups;   // 16-id units of the largest range
+    const int rows = std::min(upu * kUnit, c->V_local);
+    const int ntile = (rows + c->kn.lm_tw - 1) / c->kn.lm_tw;
+    const int w = c->kn.lm_w > 0 ? c->kn.lm_w : ((rows + ntile - 1) / ntile + 15) & ~15;
+    return LmPlan{cg, w, w, ngroups * nch, nch};
 }
 
 template <int MODE>
