@@ -210,6 +210,7 @@ struct nj_ctx {
     int mass_occ = 1;                 // resident k_mass CTAs per SM at mass_nst
     int32_t* scratch_i = nullptr;  // [MB]
     int32_t* s_row = nullptr;      // [MB] staged path: sample row of each request
+    int32_t* g2row = nullptr;      // [Gmax] staged sharded step: packed row of each draft row
     // vocab-sharded mode (nj_shard.cuh): rank / ranks, NCCL comm or nj_group member
     int nranks = 1, rank = 0;
     void* ncomm = nullptr;
@@ -320,9 +321,10 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
     pl.npad = round16(pl.N);
     const bool fused_ok = pl.N <= kFusedMaxN && c->max_tiles <= 16 && (c->max_tiles + 1) * pl.npad <= 512 &&
                           !c->sharded();
-    const bool staged_ok = pl.N <= c->staged_rows && c->logits_st != nullptr && !c->sharded();
+    // staged: unsharded, or the vocab-sharded step on k_lmhead (one W-shard pass, §9)
+    const bool staged_ok = pl.N <= c->staged_rows && c->logits_st != nullptr && (!c->sharded() || c->kn.lm);
     int path = c->path_opt;
-    if (c->sharded() && path == NJ_PATH_AUTO) path = NJ_PATH_TWOPASS;   // the phased sharded driver
+    if (c->sharded() && path == NJ_PATH_AUTO) path = staged_ok ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;   // phased driver
     // k_gemm_big's cost is ~per (vocab tile, token chunk) item whatever the chunk
     // width (<= 256): staged (ceil(N/256) chunks in one pass) wins only when it
     // needs fewer chunks than K-A + K-C (ceil(G/256) + ceil(B/256))
@@ -867,6 +869,31 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)MB) * sizeof(int32_t), st));
         if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
         a.gridA = c->grid;
+        if (pl.path == NJ_PATH_STAGED) {
+            // staged step (k_lmhead over all N rows of the shard: logits, per-row statistics,
+            // owned draft logits), then X1 from the draft rows' statistics
+            if (pl.G > 0) NJ_CUDA(c, cudaMemsetAsync(c->dl, 0xFF, (size_t)pl.G * sizeof(double), st));   // NaN: not owned
+            LmheadParams lp{};
+            lp.logits = c->logits_st; lp.ld_out = c->V_local;
+            lp.part_m = c->part_m; lp.part_s = c->part_s;
+            lp.tok = a.tok; lp.dl = c->dl;
+            lp.cap_staged = 1;
+            lp.B = pl.B;
+            for (int b = 0; b <= pl.B; ++b) lp.row_off[b] = pl.row_off[b];
+            std::pair<cudaEvent_t, cudaEvent_t> ev;
+            if ((s = prof_begin(c, st, ev)) != NJ_OK) return s;
+            if ((s = launch_lm<LM_WRITE | LM_STATS | LM_CAPTURE>(c, st, a.hidden, a.W, pl.N, lp, &a.gridA)) != NJ_OK)
+                return s;
+            if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
+            if (pl.G > 0) {
+                k_draft_rows<<<(pl.B + 127) / 128, 128, 0, st>>>(a.meta, c->g2row);
+                NJ_LAUNCHED(c, "k_draft_rows", st);
+                k_xpack1<<<(pl.G + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, a.gridA, c->dl, pl.G, c->xs1,
+                                                          c->g2row);
+                NJ_LAUNCHED(c, "k_xpack1", st);
+            }
+            return NJ_OK;
+        }
         if (pl.G > 0) {
             NJ_CUDA(c, cudaMemsetAsync(c->dl, 0xFF, (size_t)pl.G * sizeof(double), st));   // NaN: not owned
             k_gather_drafts<<<pl.G, 128, 0, st>>>(a.hidden, c->cfg.d, a.meta, c->hd);
@@ -887,7 +914,8 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
                     return s;
                 if ((s = prof_end(c, st, ev)) != NJ_OK) return s;
             }
-            k_xpack1<<<(pl.G + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, a.gridA, c->dl, pl.G, c->xs1);
+            k_xpack1<<<(pl.G + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, a.gridA, c->dl, pl.G, c->xs1,
+                                                      nullptr);
             NJ_LAUNCHED(c, "k_xpack1", st);
         }
         return NJ_OK;
@@ -904,12 +932,18 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         ap.certify = a.certify; ap.force_fallback = c->force_fb;
         ap.eps_acc = c->eps_acc_ka_cert * (float)std::max(1.0, c->inv_t);
         ap.xr1 = c->xr1; ap.nranks = c->nranks; ap.xld = pl.G;
+        const bool staged = pl.path == NJ_PATH_STAGED;
+        if (staged) {   // sample row of request b = row s_row[b] of the staged logits (no K-C);
+                        // a residual row keeps X1's merged lse, a bonus row this rank's lse from its
+                        // own row statistics (rescaled across ranks by X2, R15)
+            ap.staged = 1; ap.s_row = c->s_row; ap.hs = nullptr;
+        }
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, a.meta);
         NJ_LAUNCHED(c, "k_accept", st);
         k_qcanon<<<1, 1024, 0, st>>>(c->req_flags(), pl.B, c->fb_count(), c->fb_list(), c->force_fb);
         NJ_LAUNCHED(c, "k_qcanon", st);
         a.gridC = c->grid;
-        {
+        if (!staged) {
             GemmBigParams gp{};
             gp.logits = c->logits_s; gp.ld_out = c->V_local;
             gp.part_m = c->part2_m; gp.part_s = c->part2_s;
@@ -921,6 +955,10 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
         mp.logits = c->logits_s; mp.ld = c->V_local; mp.V_local = c->V_local; mp.v_begin = c->cfg.v_begin;
         mp.nchunks = c->nchunks; mp.s_resid = c->s_resid; mp.s_qrow = c->s_qrow; mp.s_lse = c->s_lse;
         mp.part2_m = c->part2_m; mp.part2_s = c->part2_s; mp.grid2 = a.gridC; mp.pld2 = c->pld;
+        if (staged) {
+            mp.logits = c->logits_st; mp.s_row = c->s_row;
+            mp.part2_m = c->part_m; mp.part2_s = c->part_s; mp.grid2 = a.gridA; mp.part2_by_row = 1;
+        }
         mp.q = a.q; mp.ldq = a.ldq; mp.u = a.u; mp.stage_mode = 0; mp.cmass = c->cmass;
         mp.accept_len = a.acc; mp.next_token = x3i;
         mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
@@ -1109,6 +1147,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     A(scratch_i, (size_t)MB);
     A(s_row, (size_t)MB);
     A(amax, (size_t)c->Nmax);
+    A(g2row, (size_t)c->Gmax);
 #undef A
     if (c->ncomm && (s = alloc_shard_ws(c)) != NJ_OK) { nj_destroy(c); return s; }
     if (cudaMemset(c->bar, 0, 2 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(c->fb_done, 0, sizeof(int32_t)) != cudaSuccess ||

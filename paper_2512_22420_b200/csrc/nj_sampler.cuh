@@ -233,6 +233,7 @@ struct MassParams {
     const float* part2_s;
     int32_t grid2;
     int32_t pld2;          // part2 row stride (>= grid2)
+    int32_t part2_by_row;  // 1: part2 row of request b is s_row[b] (vocab-sharded staged step)
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -271,12 +272,13 @@ __device__ __forceinline__ void flag_draw(const MassParams& p, int b, int32_t bi
     else if (p.certify || (bits & 2)) push_fallback(p.fb_count, p.fb_list, p.req_flags, b, bits);
 }
 
+__device__ __forceinline__ int part2_row(const MassParams& p, int b) { return p.part2_by_row ? p.s_row[b] : b; }
 __device__ __forceinline__ double sample_lse(const MassParams& p, int b) {
     __shared__ double s_l;
     double l = p.s_lse[b];
     if (isnan(l)) {
         if (warp_id() == 0) {
-            const double v = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
+            const double v = warp_lse(p.part2_m, p.part2_s, p.pld2, part2_row(p, b), p.grid2);
             if (lane_id() == 0) s_l = v;
         }
         __syncthreads();
@@ -318,7 +320,7 @@ __global__ void k_sample_lse(const MassParams p, int B, double* s_lse) {   // s_
     const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     if (b >= B) return;
     if (!isnan(__ldcg(&p.s_lse[b]))) return;
-    const double v = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
+    const double v = warp_lse(p.part2_m, p.part2_s, p.pld2, part2_row(p, b), p.grid2);
     if (lane_id() == 0) s_lse[b] = v;
 }
 

@@ -52,10 +52,10 @@ __device__ __forceinline__ double xmerge_lse(const double* xr, int nranks, int l
 
 // X1 pack: warp per draft row.
 __global__ void k_xpack1(const float* part_m, const float* part_s, int pld, int grid, const double* dl, int G,
-                         double* xs1) {
+                         double* xs1, const int32_t* g2row) {
     const int g = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     if (g >= G) return;
-    const double l = warp_lse(part_m, part_s, pld, g, grid);
+    const double l = warp_lse(part_m, part_s, pld, g2row ? g2row[g] : g, grid);
     if (lane_id() == 0) {
         xs1[2 * g] = l;
         xs1[2 * g + 1] = __ldcg(&dl[g]);
@@ -65,10 +65,17 @@ __global__ void k_xpack1(const float* part_m, const float* part_s, int pld, int 
 // X2 pack: warp per request: lse of the sample row as used by k_mass, the
 // rank's mass sum_c cmass (fixed order, as k_locate sums it), and the
 // rank-local lse of the sample row from K-C's statistics (R6 across shards).
+// staged sharded step: the packed-row index of every draft row (row of draft g of
+// request b is g + b), for k_xpack1 over per-row statistics
+__global__ void k_draft_rows(const ReqMeta m, int32_t* g2row) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= m.B) return;
+    for (int r = m.row_off[b]; r + 1 < m.row_off[b + 1]; ++r) g2row[r - b] = r;
+}
 __global__ void k_xpack2(const MassParams p, int B, double* xs2) {
     const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     if (b >= B) return;
-    const double lloc = warp_lse(p.part2_m, p.part2_s, p.pld2, b, p.grid2);
+    const double lloc = warp_lse(p.part2_m, p.part2_s, p.pld2, part2_row(p, b), p.grid2);
     double l = __ldcg(&p.s_lse[b]);
     if (isnan(l)) l = lloc;
     if (lane_id() == 0) {

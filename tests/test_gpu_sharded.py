@@ -12,8 +12,9 @@ import torch
 
 import oracle
 import parity
-from paper_2512_22420_b200 import (NJ_FLAG_FALLBACK, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NcclComm, NJError,
-                                   ShardGroup, Verifier, nccl_unique_id, shard_range)
+from paper_2512_22420_b200 import (NJ_FLAG_FALLBACK, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PATH, NJ_PATH_AUTO,
+                                   NJ_PATH_TWOPASS, NcclComm, NJError, ShardGroup, Verifier, nccl_unique_id,
+                                   shard_range)
 from synth.inputs import make_batch, make_weight
 
 pytestmark = pytest.mark.gpu
@@ -21,8 +22,11 @@ DEV = torch.device("cuda:0") if torch.cuda.is_available() else None
 QV, QD = 152064, 3584
 
 
-def run_group(b, G, certify=True, force_fb=False, gamma_max=5):
+def run_group(b, G, certify=True, force_fb=False, gamma_max=5, path=NJ_PATH_AUTO):
+    """AUTO = the staged sharded step (k_lmhead over all rows of each shard) for
+    N <= 2048; NJ_PATH_TWOPASS = the K-A / K-C form."""
     grp = ShardGroup(b.hidden.shape[1], b.W.shape[0], max_batch=b.B, gamma_max=gamma_max, nshards=G)
+    grp.set_option(NJ_OPT_PATH, path)
     grp.set_option(NJ_OPT_CERTIFY, int(certify))
     grp.set_option(NJ_OPT_FORCE_FALLBACK, int(force_fb))
     acc = torch.full((b.B,), -7, dtype=torch.int32, device=DEV)
@@ -66,11 +70,12 @@ def test_shard_ranges_partition():
         assert all(vb % 128 == 0 and ve > vb for vb, ve in rs)
 
 
+@pytest.mark.parametrize("path", [NJ_PATH_AUTO, NJ_PATH_TWOPASS])
 @pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
-def test_group_small(G):
+def test_group_small(G, path):
     for seed in range(3):
         b = make_batch(12, "mixed:5", V=2048, d=128, seed=40 + seed, device=DEV, q_vocab=2040)
-        acc, nxt, dd = run_group(b, G)
+        acc, nxt, dd = run_group(b, G, path=path)
         check(b, acc, nxt, dd, lnp_tol=2e-5)
 
 
@@ -96,11 +101,12 @@ def test_group_equals_unsharded_gpu():
             assert (acc == acc0.cpu().numpy()).all() and (nxt == nxt0.cpu().numpy()).all()
 
 
-def test_group_forced_fp64_fallback():
+@pytest.mark.parametrize("path", [NJ_PATH_AUTO, NJ_PATH_TWOPASS])
+def test_group_forced_fp64_fallback(path):
     """Every request through the sharded fp64 fallback (three more exchanges)."""
     for G in (2, 4):
         b = make_batch(10, "mixed:3", V=2048, d=64, seed=21 + G, device=DEV)
-        acc, nxt, dd = run_group(b, G, force_fb=True)
+        acc, nxt, dd = run_group(b, G, force_fb=True, path=path)
         check(b, acc, nxt, dd)
         assert (dd["flags"] & NJ_FLAG_FALLBACK).all()
 
@@ -113,14 +119,15 @@ def test_group_c5_full_size():
     check(b, acc, nxt, dd, lnp_tol=4e-5)   # sharded K-A restarts every 14 k-blocks (certified)
 
 
-@pytest.mark.parametrize("G", [8, 2])
-def test_group_c5_bench_batch(G):
+@pytest.mark.parametrize("G,path", [(8, NJ_PATH_AUTO), (2, NJ_PATH_AUTO), (8, NJ_PATH_TWOPASS)])
+def test_group_c5_bench_batch(G, path):
     """BASELINE configs[4] exactly: B = 256, gamma = 2 (N = 768) split over G
-    vocab shards, every request against the (unsharded) oracle."""
+    vocab shards (the staged sharded step, and the two-pass form at G = 8),
+    every request against the (unsharded) oracle."""
     W = make_weight(QV, QD, 0, DEV)
     b = make_batch(256, 2, V=QV, d=QD, seed=0, device=DEV, W=W)
-    acc, nxt, dd = run_group(b, G)
-    check(b, acc, nxt, dd, lnp_tol=4e-5, name=f"c5 bench batch G={G}")
+    acc, nxt, dd = run_group(b, G, path=path)
+    check(b, acc, nxt, dd, lnp_tol=4e-5, name=f"c5 bench batch G={G} path={path}")
 
 
 def test_nccl_single_rank():
