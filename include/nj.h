@@ -211,13 +211,15 @@ nj_status nj_plan(nj_ctx* ctx, const int32_t* gamma_per_req, int32_t B,
 
 /* ---- test-only stage exports (used by tests/ for stage-isolated parity) ---- */
 
-/* LM-head logits (BJ step 1) through the PRODUCTION GEMM kernel (k_gemm_big,
- * the one the staged / two-pass paths and nj_propose launch):
+/* LM-head logits (BJ step 1) through the PRODUCTION GEMM kernel (k_lmhead, the
+ * one the staged path, nj_propose and the sharded staged step launch; k_gemm_big,
+ * the two-pass path's, when the context was created with NJ_LM=0):
  *   logits[r, x] = Σ_k W[x,k]·hidden[rows[r],k]   for x in [0, v_end-v_begin),
  * fp32, row-major with pitch ld_out (>= V_local).  rows: device int32
  * [n_rows], 1 <= n_rows <= min(max_batch·gamma_max, 1536).  ks: k-blocks (64
  * deep) per TMEM accumulator restart; 0 = the sample-row GEMM's
- * default (4), 8 = the two-pass draft-row GEMM's.  Test-only (element-wise
+ * default (4; k_lmhead's first group of an item spans max(ks, 8)), 8 = the
+ * two-pass draft-row GEMM's.  Test-only (element-wise
  * parity of the GEMM against the fp64 oracle). */
 nj_status nj_lmhead_logits(nj_ctx* ctx, void* stream,
                            const uint16_t* hidden, const uint16_t* W_lm,
