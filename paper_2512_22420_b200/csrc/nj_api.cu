@@ -103,7 +103,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0;   // k_lmhead
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0;   // k_lmhead
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -140,6 +140,7 @@ Knobs read_knobs() {
     k.lm_arv1 = env_int("NJ_LM_ARV1", 0);
     k.lm_w = std::min(256, env_int("NJ_LM_W", 0) & ~15);   // probe: fixed tile width (ragged last tile)
     k.lm_fence = env_int("NJ_LM_FENCE", 0);
+    k.lm_mma4 = env_int("NJ_LM_MMA4", 0);
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
 }
@@ -599,6 +600,7 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.ks0 = std::max(p.ks, c->kn.lm_ks0 > 0 ? c->kn.lm_ks0 : 8);
     p.arv1 = c->kn.lm_arv1;
     p.fence_full = c->kn.lm_fence;
+    p.mma4 = c->kn.lm_mma4;
     p.dbg = c->kn.lm_dbg;
     p.ts = nullptr;
     if (c->kn.phase_ts) {

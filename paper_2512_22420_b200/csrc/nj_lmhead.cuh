@@ -54,6 +54,7 @@ struct LmheadParams {
     int32_t ks0;                 // k-blocks of the first accumulator group of every item (>= ks)
     int32_t arv1;                // 1: one accumulator-release arrival per CTA (named barrier first)
     int32_t fence_full;          // probe: tcgen05.fence::after_thread_sync after every operand wait
+    int32_t mma4;                // 1: a k-block's four MMAs issued from one asm block under one elect
     int32_t nbuf, bstride;       // TMEM accumulator buffers and their column stride
     int32_t tile_w;              // vocab tile width (multiple of 16, <= 256; the last tile of a range is ragged)
     int32_t wbox;                // W box rows per CTA (tile_w / CG)
@@ -297,10 +298,14 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                             const uint64_t ad = sdesc_sw128(st + (size_t)g * kLmHBytes);
                             const uint64_t bd = sdesc_sw128(st + (size_t)GK * kLmHBytes + (size_t)g * wBytes);
                             if (!(p.dbg & 1)) {
+                                if (p.mma4) {
+                                    mma_kblock_w<CG>(dt, ad, bd, idesc, kin != 0);
+                                } else {
 #pragma unroll
-                                for (int k = 0; k < kBK / 16; ++k) {
-                                    if (CG == 2) mma_bf16_cg2_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
-                                    else mma_bf16_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                                    for (int k = 0; k < kBK / 16; ++k) {
+                                        if (CG == 2) mma_bf16_cg2_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                                        else mma_bf16_w(dt, ad + 2 * k, bd + 2 * k, idesc, (kin | k) != 0);
+                                    }
                                 }
                             }
                             const int kb = kg * GK + g;
