@@ -478,18 +478,27 @@ k_fused_verify(const __grid_constant__ CUtensorMap tmW128, const __grid_constant
         }
     if (p.q_prefetch) {
         // every draft row's q slice [r0, r0+rows) -> smem, fire-and-forget; it lands
-        // while this CTA runs phase 2 (issued after the barrier: its fence would wait on it)
+        // while this CTA runs phase 2 (issued after the barrier: its fence would wait on it).
+        // Issued by the warps the lse merge leaves idle (rows j = 4 warp + lane / 8 >= N),
+        // in parallel with the merge; by every thread when all warps merge (N > 44).
         const int G = p.G;
-        if (p.q_vec16) {
-            const int n4 = (rows + 3) >> 2;
-            for (int i = threadIdx.x; i < G * n4; i += kFusedThreads) {
-                const int g = i / n4, x = (i - g * n4) * 4;
-                cp_async16(qsl + (size_t)g * rows_cap + x, p.q + (int64_t)g * p.ldq + p.v_begin + r0 + x);
-            }
-        } else {
-            for (int i = threadIdx.x; i < G * rows; i += kFusedThreads) {
-                const int g = i / rows, x = i - g * rows;
-                cp_async4(qsl + (size_t)g * rows_cap + x, p.q + (int64_t)g * p.ldq + p.v_begin + r0 + x);
+        const int w0 = (N + 3) / 4;                       // first warp without lse rows
+        const int nw = kFusedThreads / 32 - w0;
+        const bool split = nw > 0;
+        const int t0 = split ? (int)threadIdx.x - w0 * 32 : (int)threadIdx.x;
+        const int nt = split ? nw * 32 : kFusedThreads;
+        if (t0 >= 0) {
+            if (p.q_vec16) {
+                const int n4 = (rows + 3) >> 2;
+                for (int i = t0; i < G * n4; i += nt) {
+                    const int g = i / n4, x = (i - g * n4) * 4;
+                    cp_async16(qsl + (size_t)g * rows_cap + x, p.q + (int64_t)g * p.ldq + p.v_begin + r0 + x);
+                }
+            } else {
+                for (int i = t0; i < G * rows; i += nt) {
+                    const int g = i / rows, x = i - g * rows;
+                    cp_async4(qsl + (size_t)g * rows_cap + x, p.q + (int64_t)g * p.ldq + p.v_begin + r0 + x);
+                }
             }
         }
         cp_async_commit();
