@@ -41,6 +41,8 @@ CONFIGS = {
     "c3_b256_g5": (256, 5, "auto"),
     "c3_b256_mixed": (256, "mixed:5", "auto"),
     "c3_b16_g2": (16, 2, "auto"),
+    "c3_b12_g3": (12, 3, "auto"),
+    "c3_b8_g5": (8, 5, "auto"),
     "c5": (256, 2, "auto"),                # BASELINE configs[4] (vocab-sharded run: bench_c5)
 }
 

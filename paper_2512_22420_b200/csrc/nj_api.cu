@@ -76,6 +76,8 @@ bool encode_out(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, i
 }
 
 constexpr int kStagedMaxN = kBigMaxRowG;   // staged path on k_gemm_big (NJ_LM=0): rows of one GEMM pass
+constexpr int kFusedAutoMaxN = 24;          // AUTO takes the fused kernel up to this many rows
+constexpr int kInlineLseRows = 64;          // staged path: N up to which k_accept merges row statistics inline
 constexpr int kStagedMaxRows = 2048;        // staged path on k_lmhead: rows of one GEMM pass (logits_st rows)
 
 inline int round16(int x) { return (x + 15) & ~15; }
@@ -103,7 +105,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0;   // k_lmhead
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -141,6 +143,8 @@ Knobs read_knobs() {
     k.lm_w = std::min(256, env_int("NJ_LM_W", 0) & ~15);   // probe: fixed tile width (ragged last tile)
     k.lm_fence = env_int("NJ_LM_FENCE", 0);
     k.lm_mma4 = env_int("NJ_LM_MMA4", 0);
+    k.small = env_int("NJ_SMALL", 1);
+    k.small_pdl = env_int("NJ_SMALL_PDL", 1);
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
 }
@@ -333,13 +337,29 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
     // k_lmhead (default): one pass over all rows always beats streaming W twice
     const bool staged_pays = c->kn.lm || pl.N <= kBigMaxT || nch(pl.N) < nch(pl.G) + nch(pl.B);
     if (path == NJ_PATH_AUTO)
-        path = fused_ok ? NJ_PATH_FUSED : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
+        // fused for the smallest batches only: above kFusedAutoMaxN rows k_lmhead + the sampler
+        // kernels are faster (B200: N = 32 203-208 vs 207-210 us, N = 48 210-215 vs 240-248 us;
+        // N = 4 fused 193 vs 203 us)
+        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm)) ? NJ_PATH_FUSED
+               : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
         return set_err(c, NJ_EUNSUPPORTED, "fused path needs N <= %d and TMEM room (N=%d)", kFusedMaxN, pl.N);
     if (path == NJ_PATH_STAGED && !staged_ok)
         return set_err(c, NJ_EUNSUPPORTED, "staged path needs N <= %d (N=%d)", c->staged_rows, pl.N);
     pl.path = path;
     return NJ_OK;
+}
+
+// k_sample_small (nj_sampler.cuh) takes the unsharded staged path's sampler when
+// one cluster of kSmallCl CTAs per request fits the SMs
+size_t small_sampler_smem(const nj_ctx* c) {   // the CTA's chunks, logits + q
+    return (size_t)((c->nchunks + kSmallCl - 1) / kSmallCl) * 2 * kChunk * sizeof(float);
+}
+bool small_sampler_ok(const nj_ctx* c, const Plan& pl) {
+    // (B <= 12: 16 clusters of 8 did not all fit at once -- B = 16 was slower than the 5 launches)
+    return c->kn.small && pl.path == NJ_PATH_STAGED && !c->sharded() && pl.B <= 12 && pl.B * kSmallCl <= c->num_sms &&
+           c->nchunks <= kSmallMaxChunks && c->cfg.gamma_max + 1 <= kSmallMaxRows && c->cfg.gamma_max <= 32 &&
+           small_sampler_smem(c) <= 200 * 1024;
 }
 
 ReqMeta make_meta(const Plan& pl) {
@@ -619,8 +639,9 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
         c->lm_w_cached = W;
         c->lm_wbox = p.wbox;
     }
+    p.hbox = (CG == 1 && pl.nchunks == 1) ? std::min(kLmTok, (R + 7) & ~7) : kLmTok;
     CUtensorMap tmH, tmL{};
-    if (!encode_2d(&tmH, h, R, c->cfg.d, kLmTok)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
+    if (!encode_2d(&tmH, h, R, c->cfg.d, p.hbox)) return set_err(c, NJ_ECUDA, "cuTensorMapEncodeTiled failed (H)");
     constexpr bool STATE = (MODE & (LM_STATS | LM_ARGMAX)) != 0, CAP = (MODE & LM_CAPTURE) != 0,
                    WR = (MODE & LM_WRITE) != 0;
     p.tma_out = WR && c->kn.lm_tma_out && (p.ld_out & 3) == 0 && (reinterpret_cast<uintptr_t>(p.logits) & 15) == 0;
@@ -630,7 +651,7 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.ost_n = c->kn.lm_ost;
     size_t tail = (p.tma_out ? (size_t)kLmEpiWarps * p.ost_n * 2048 : 0) + (STATE ? 4 * nloc * 8 : 0) + (CAP ? nloc * 8 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 2 * kLmMaxBuf) * 8 + 8;
-    const size_t kb_bytes = (size_t)kLmHBytes + (size_t)p.wbox * 128;
+    const size_t kb_bytes = (size_t)p.hbox * 128 + (size_t)p.wbox * 128;
     // CTA pair, one token chunk (R <= 256): 2-k-block ring stages (W streamed once; -7 % at R = 256);
     // several: 1-k-block stages, the MMA warp taking two per operand wait (equal or better there)
     p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : (pl.nchunks == 1 && CG == 2 ? 2 : 1);
@@ -1172,6 +1193,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 1>);
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 2>);
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 1>);
+    e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 2>);
     if (const char* ev = getenv("NJ_MASS_NST")) c->mass_nst = std::min(4, std::max(2, atoi(ev)));
     e = e ? e : cudaFuncSetAttribute(k_mass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(2, c->cfg.max_batch));
@@ -1256,13 +1278,18 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
     if (c->sharded()) {
         // gather + K-A + pack1; accept, qcanon, K-C, sample_lse, mass, pack2, fb_logits, fbx_stats;
         // locate, fbx_accept; xfinish2, fbx_locate; fbx_write
-        n = (pl.G > 0 ? 1 + ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 8 + 2 + 2 + 1;
+        if (pl.path == NJ_PATH_STAGED)   // k_lmhead (+ draft_rows + pack1); accept, qcanon, sample_lse,
+                                         // mass, pack2, fb_logits, fbx_stats; ...
+            n = 1 + (pl.G > 0 ? 2 : 0) + 7 + 2 + 2 + 1;
+        else
+            n = (pl.G > 0 ? 1 + ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 8 + 2 + 2 + 1;
         if (path_out) *path_out = pl.path;
         if (launches_out) *launches_out = n;
         return NJ_OK;
     }
     if (pl.path == NJ_PATH_FUSED) n = 1;
-    else if (pl.path == NJ_PATH_STAGED) n = 5;   // GEMM, row lse, accept, mass, locate
+    else if (pl.path == NJ_PATH_STAGED)   // GEMM, [row lse,] accept, mass, locate | GEMM, k_sample_small
+        n = small_sampler_ok(c, pl) ? 2 : pl.N > kInlineLseRows ? 5 : 4;
     else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 4;   // gather+KA, row lse, KB, KC, KD1, KD2
     n += 1;   // k_fb (every call; exits at once on an empty queue)
     if (path_out) *path_out = pl.path;
@@ -1358,9 +1385,40 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         ap.dbg_lse = dbg ? dbg->lse : nullptr; ap.dbg_pdraft = dbg ? dbg->p_draft : nullptr;
         ap.certify = certify; ap.force_fallback = c->force_fb; ap.eps_acc = c->eps_acc * (float)std::max(1.0, c->inv_t);
         ap.staged = 1; ap.s_row = c->s_row;
-        k_lse_rows<<<(pl.N + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.N, c->row_lse);
-        NJ_LAUNCHED(c, "k_lse_rows", st);
-        ap.pre_lse = c->row_lse;
+        if (small_sampler_ok(c, pl)) {
+            // small batch: acceptance, chunk masses and the draw in one clustered launch
+            MassParams mp{};
+            mp.logits = c->logits_st; mp.ld = c->V_local; mp.V_local = c->V_local; mp.v_begin = c->cfg.v_begin;
+            mp.nchunks = c->nchunks; mp.q = draft_probs; mp.ldq = ldq; mp.u = uniforms;
+            mp.accept_len = accept_len; mp.next_token = next_token;
+            mp.fb_count = c->fb_count(); mp.fb_list = c->fb_list(); mp.req_flags = c->req_flags();
+            mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
+            mp.dbg_lse = dbg ? dbg->lse : nullptr;
+            mp.certify = certify; mp.eps_draw = c->eps_draw;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(pl.B * kSmallCl);
+            cfg.blockDim = dim3(kSampThreads);
+            cfg.dynamicSmemBytes = small_sampler_smem(c);
+            cfg.stream = st;
+            cudaLaunchAttribute at[2];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kSmallCl;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[1].val.programmaticStreamSerializationAllowed = c->kn.small_pdl ? 1 : 0;
+            cfg.attrs = at;
+            cfg.numAttrs = 2;
+            NJ_CUDA(c, cudaLaunchKernelEx(&cfg, k_sample_small, ap, mp, meta));
+            NJ_LAUNCHED(c, "k_sample_small", st);
+            goto fallback;
+        }
+        // small batches: k_accept merges its rows' statistics itself (one launch fewer)
+        if (pl.N > kInlineLseRows) {
+            k_lse_rows<<<(pl.N + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.N, c->row_lse);
+            NJ_LAUNCHED(c, "k_lse_rows", st);
+            ap.pre_lse = c->row_lse;
+        }
         k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
         NJ_LAUNCHED(c, "k_accept", st);
         MassParams mp{};
@@ -1447,6 +1505,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
         NJ_LAUNCHED(c, "k_locate", st);
     }
+fallback:
     // the fp64 fallback runs on every call (an empty queue exits at once): with
     // certification it recomputes flagged decisions, and it always takes the
     // zero-residual-mass draws (R6), which must come from p_n

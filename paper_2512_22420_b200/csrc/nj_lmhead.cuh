@@ -58,6 +58,7 @@ struct LmheadParams {
     int32_t nbuf, bstride;       // TMEM accumulator buffers and their column stride
     int32_t tile_w;              // vocab tile width (multiple of 16, <= 256; the last tile of a range is ragged)
     int32_t wbox;                // W box rows per CTA (tile_w / CG)
+    int32_t hbox;                // H box rows (128, or R rounded up to 8 for a single CTA chunk)
     int32_t w_evict_first;
     int32_t pf;                  // W L2 prefetch distance in k-blocks (0: off); issued 4 k-blocks at a time
     float* logits;               // WRITE: [R][ld_out] fp32 (local vocab ids)
@@ -113,7 +114,11 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.nstages, GK = p.gk;
     const uint32_t wBytes = (uint32_t)p.wbox * 128u;                 // this CTA's W box per k-block
-    const size_t stageBytes = (size_t)GK * (kLmHBytes + wBytes);
+    // H box: 128 token rows, or fewer (a multiple of 8) when the launch has fewer rows
+    // (single chunk): the MMA still reads 128 rows, the ones past the box are garbage
+    // rows of unused TMEM lanes (never output)
+    const uint32_t hBytes = (uint32_t)p.hbox * 128u;
+    const size_t stageBytes = (size_t)GK * (hBytes + wBytes);
     const int nloc = kLmTok;                                          // this CTA's token rows (one chunk)
     uint8_t* ring = smem;
     // WRITE via TMA: per epilogue warp two 2-KB staging boxes (32 rows x 16 fp32, 64B-swizzled)
@@ -211,15 +216,15 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                 if (tsx) p.ts[2 * si + 1] = globaltimer();
                 uint8_t* st = ring + (size_t)s * stageBytes;
                 const bool ldh = !(p.dbg & 16), ldw = !(p.dbg & 32);   // probes
-                const uint32_t kbb = (ldh ? (uint32_t)kLmHBytes : 0u) + (ldw ? wBytes : 0u);
+                const uint32_t kbb = (ldh ? hBytes : 0u) + (ldw ? wBytes : 0u);
                 if (CG == 1) {
                     if (kbb) mbar_arrive_expect_tx_w(&full[s], (uint32_t)ng * kbb);
                     else mbar_arrive_w(&full[s]);
                     for (int g = 0; g < ng; ++g) {
                         const int kb = kg * GK + g;
-                        if (ldh) tma_load_2d_w(st + (size_t)g * kLmHBytes, &tmH, &full[s], kb * kBK, hrow, pol_h);
+                        if (ldh) tma_load_2d_w(st + (size_t)g * hBytes, &tmH, &full[s], kb * kBK, hrow, pol_h);
                         if (ldw)
-                            tma_load_2d_w(st + (size_t)GK * kLmHBytes + (size_t)g * wBytes, &tmW, &full[s], kb * kBK,
+                            tma_load_2d_w(st + (size_t)GK * hBytes + (size_t)g * wBytes, &tmW, &full[s], kb * kBK,
                                           wrow, pol_w);
                     }
                 } else {
@@ -231,9 +236,9 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     const uint32_t fbs = mapa_shared(&full[s], 0);
                     for (int g = 0; g < ng; ++g) {
                         const int kb = kg * GK + g;
-                        if (ldh) tma_load_2d_cg2_w(st + (size_t)g * kLmHBytes, &tmH, fbs, kb * kBK, hrow, pol_h);
+                        if (ldh) tma_load_2d_cg2_w(st + (size_t)g * hBytes, &tmH, fbs, kb * kBK, hrow, pol_h);
                         if (ldw)
-                            tma_load_2d_cg2_w(st + (size_t)GK * kLmHBytes + (size_t)g * wBytes, &tmW, fbs, kb * kBK,
+                            tma_load_2d_cg2_w(st + (size_t)GK * hBytes + (size_t)g * wBytes, &tmW, fbs, kb * kBK,
                                               wrow, pol_w);
                     }
                 }
@@ -295,8 +300,8 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                                 tc_fence_after();
                                 dt = tbase + (uint32_t)(abuf * p.bstride);
                             }
-                            const uint64_t ad = sdesc_sw128(st + (size_t)g * kLmHBytes);
-                            const uint64_t bd = sdesc_sw128(st + (size_t)GK * kLmHBytes + (size_t)g * wBytes);
+                            const uint64_t ad = sdesc_sw128(st + (size_t)g * hBytes);
+                            const uint64_t bd = sdesc_sw128(st + (size_t)GK * hBytes + (size_t)g * wBytes);
                             if (!(p.dbg & 1)) {
                                 if (p.mma4) {
                                     mma_kblock_w<CG>(dt, ad, bd, idesc, kin != 0);
@@ -332,6 +337,8 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
         // e, e + 4, e + 8, e + 12 of 16 vocab columns (acc[16 j + i] = granule e + 4 j)
         const int q = warp & 3, e = warp >> 2;
         const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(e * 16);
+        // a lane quadrant whose 32 token rows are all past R drains nothing (it still releases)
+        const bool quad_empty = cfix * kLmTok * CG + crank * kLmTok + q * 32 >= p.R;
         const int ngroups = p.num_kb <= p.ks0 ? 1 : 1 + (p.num_kb - p.ks0 + p.ks - 1) / p.ks;
         const uint64_t pol_out = policy_evict_first();   // logits: do not push W / H out of L2
         const bool vec_ok = (p.ld_out & 3) == 0 && (reinterpret_cast<uintptr_t>(p.logits) & 15) == 0;
@@ -358,7 +365,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                 if (++ebuf == NBUF) { ebuf = 0; eph ^= 1; }
                 tc_fence_after();
                 const uint32_t ta = lane_base + (uint32_t)(buf * p.bstride);
-                if (!(p.dbg & 2)) {
+                if (!(p.dbg & 2) && !quad_empty) {
                     if (myg >= 2) {
                         float v[32];
                         tmem_ld16x2(ta, ta + 64u, v);

@@ -469,6 +469,243 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
     }
     cp_async_wait_all();
 }
+// Small-batch staged sampler (unsharded staged path, B * kSmallCl <= SMs): the
+// acceptance tests (K-B), the chunk masses (K-D1) and the draw (K-D2) of request
+// b in ONE launch by a cluster of kSmallCl CTAs -- the request's chunks dealt over
+// the cluster, chunk masses exchanged through distributed shared memory.  The
+// arithmetic and its order are k_accept's, k_mass's and k_locate's (bit-identical
+// decisions, masses and draws); only the launches and the global round trips
+// between them are gone (~20 us of a ~205 us step at C2).
+constexpr int kSmallCl = 8;
+constexpr int kSmallMaxChunks = 64;
+constexpr int kSmallMaxRows = 16;   // gamma_max <= 15
+__global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParams ap, const MassParams p,
+                                                               const ReqMeta m) {
+    // launched with programmatic dependent launch: the CTAs start on SMs the GEMM's
+    // finished CTAs free, then wait here for the whole GEMM grid and its writes
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int b = (int)cluster_id_x();
+    const int rank = (int)cluster_ctarank();
+    const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
+    __shared__ double s_lrow[kSmallMaxRows];
+    __shared__ int s_n;
+    __shared__ double cml[kSmallMaxChunks];   // this CTA's chunk masses (slot = chunk)
+    __shared__ double cm[kSmallMaxChunks];    // every chunk mass of the request
+    __shared__ float wt[kSubTiles][8];
+    __shared__ double sst[kSubTiles];
+    __shared__ double spre[kSubTiles + 1];
+    __shared__ double sh_tp, sh_W;
+    __shared__ int sh_c, sh_clamp, ssel;
+    __shared__ int wpick[8];
+    // (1) lse of every row of the request from its per-row partials, one warp per row
+    for (int i = (int)warp_id(); i <= gam; i += kSampThreads / 32) {
+        const double l = warp_lse(ap.part_m, ap.part_s, ap.pld, ro + i, ap.grid);
+        if (lane_id() == 0) s_lrow[i] = l;
+    }
+    __syncthreads();
+    // (2) acceptance and first rejection: lane i of warp 0 tests draft i (k_accept's
+    //     expressions), the first failing lane is the rejection; a near-tie flag counts
+    //     only for tests up to it (k_accept stops there).  Every CTA of the cluster
+    //     decides identically, rank 0 writes.
+    if (warp_id() == 0) {
+        const int lane = (int)lane_id();
+        bool fail = false, near = false;
+        double pd = 0.0;
+        if (lane < gam) {
+            const int g = g0 + lane;
+            const double lse = s_lrow[lane], dlv = __ldcg(&ap.dl[g]);
+            pd = exp(dlv - lse);
+            const double qx = (double)ap.q[(int64_t)g * ap.ldq + ap.draft_tokens[g]];
+            const double uq = (double)ap.u[ro + lane] * qx;
+            near = fabs(uq - pd) <= (double)ap.eps_acc * pd;
+            fail = !(uq < pd);
+        }
+        const unsigned fm = __ballot_sync(0xffffffffu, fail);
+        const int n = fm ? __ffs(fm) - 1 : gam;
+        const bool flag = __ballot_sync(0xffffffffu, near && lane <= n) != 0u;
+        if (rank == 0) {
+            if (lane < gam) {
+                if (ap.dbg_lse) ap.dbg_lse[ro + lane] = (float)s_lrow[lane];
+                if (ap.dbg_pdraft) ap.dbg_pdraft[g0 + lane] = (float)pd;
+            }
+            if (lane == 0) {
+                ap.accept_len[b] = n;
+                if (ap.certify && (flag || ap.force_fallback))
+                    push_fallback(ap.fb_count, ap.fb_list, ap.req_flags, b, 0);
+            }
+        }
+        if (lane == 0) s_n = n;
+    }
+    __syncthreads();
+    const int n = s_n;
+    const bool resid = n < gam;
+    const float* lrow = p.logits + (int64_t)(ro + n) * p.ld;
+    const float* qrow = resid ? p.q + (int64_t)(g0 + n) * p.ldq + p.v_begin : nullptr;
+    const double lse = s_lrow[n];
+    const float lsef = (float)lse, corr = lse_corr(lse);
+    // (3) this CTA's chunk masses (k_mass's weights and reduction order); all of its
+    //     chunks (logits, and q for a residual row) staged with cp.async at once
+    extern __shared__ __align__(16) float stage[];   // [chunks of this CTA][2][kChunk]
+    {
+        int k = 0;
+        for (int c = rank; c < p.nchunks; c += kSmallCl, ++k) {
+            const int x0 = c * kChunk, nn = min(kChunk, p.V_local - x0);
+            mass_copy_chunk(stage + (size_t)k * 2 * kChunk, lrow + x0, nn);
+            if (resid) mass_copy_chunk(stage + (size_t)k * 2 * kChunk + kChunk, qrow + x0, nn);
+        }
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    int kk = 0;
+    for (int c = rank; c < p.nchunks; c += kSmallCl, ++kk) {
+        const float* sl = stage + (size_t)kk * 2 * kChunk;
+        const float* sq = sl + kChunk;
+        const int x0 = c * kChunk + (int)threadIdx.x;
+        float v[kSubTiles];
+#pragma unroll
+        for (int s2 = 0; s2 < kSubTiles; ++s2) {
+            const int o = s2 * kSampThreads + (int)threadIdx.x;
+            const bool in = x0 + s2 * kSampThreads < p.V_local;
+            const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
+            v[s2] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
+        }
+        warp_totals16(v, wt);
+        __syncthreads();
+        if (threadIdx.x < kSubTiles) {
+            double st = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
+            sst[threadIdx.x] = st;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < kSubTiles; ++k) acc = acc + sst[k];
+            cml[c] = acc;
+        }
+        __syncthreads();
+    }
+    // (4) every chunk mass from the CTA that owns it (distributed shared memory); the
+    //     second cluster barrier keeps each CTA's cml alive until all have read it
+    cluster_sync_all();
+    for (int c = threadIdx.x; c < p.nchunks; c += kSampThreads)
+        cm[c] = ld_shared_cluster_f64(mapa_shared(&cml[c], (uint32_t)(c % kSmallCl)));
+    __syncthreads();
+    cluster_sync_all();
+    // (5) the draw: k_locate's unsharded arithmetic; the CTA owning the located chunk finishes
+    if (threadIdx.x == 0) {
+        double W = 0.0;
+        for (int c = 0; c < p.nchunks; ++c) W = W + cm[c];
+        const double T = (double)p.u[ro + gam] * W;
+        double P = 0.0, Pc = 0.0;
+        int csel = -1, lastpos = -1;
+        for (int c = 0; c < p.nchunks; ++c) {
+            const double wc = cm[c];
+            if (wc > 0.0) lastpos = c;
+            if (csel < 0 && T < P + wc) { csel = c; Pc = P; }
+            P = P + wc;
+        }
+        int clamp = 0;
+        if (!(W > 0.0)) clamp = 2;               // zero mass (R6) -> fp64 fallback
+        else if (csel < 0) { clamp = 1; csel = lastpos; Pc = 0.0; }
+        sh_tp = T - Pc;
+        sh_c = csel;
+        sh_clamp = clamp;
+        sh_W = W;
+        if (rank == 0 && p.dbg_lse && !resid) p.dbg_lse[ro + gam] = (float)lse;
+    }
+    __syncthreads();
+    const int clamp = sh_clamp;
+    if (clamp == 2) {
+        if (rank == 0 && threadIdx.x == 0) {
+            p.next_token[b] = 0;
+            if (p.dbg_mass) p.dbg_mass[b] = 0.0;
+            if (p.dbg_flags) p.dbg_flags[b] = 2;
+            flag_draw(p, b, 2);
+        }
+        return;
+    }
+    const int c = sh_c;
+    if (c % kSmallCl != rank) return;
+    const double tp = sh_tp;
+    float w[kSubTiles], v[kSubTiles];
+    {   // the located chunk's weights again, from this CTA's staged copy (same expression)
+        const float* sl = stage + (size_t)(c / kSmallCl) * 2 * kChunk;
+        const float* sq = sl + kChunk;
+        const int x0 = c * kChunk + (int)threadIdx.x;
+#pragma unroll
+        for (int s2 = 0; s2 < kSubTiles; ++s2) {
+            const int o = s2 * kSampThreads + (int)threadIdx.x;
+            const bool in = x0 + s2 * kSampThreads < p.V_local;
+            const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
+            v[s2] = w[s2] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
+        }
+    }
+    warp_totals16(v, wt);
+    __syncthreads();
+    if (threadIdx.x < kSubTiles) {
+        double st = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
+        sst[threadIdx.x] = st;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double acc = 0.0;
+        int sel = -1, lastpos = -1;
+        for (int s2 = 0; s2 < kSubTiles; ++s2) {
+            spre[s2] = acc;
+            const double st = sst[s2];
+            if (st > 0.0) lastpos = s2;
+            acc = acc + st;
+            if (sel < 0 && tp < acc) sel = s2;
+        }
+        spre[kSubTiles] = acc;
+        if (clamp || sel < 0) sel = -1 - lastpos;
+        ssel = sel;
+    }
+    __syncthreads();
+    int s = ssel;
+    const bool clamped = s < 0;
+    if (clamped) s = -1 - s;
+    float ws = 0.f;
+#pragma unroll
+    for (int k = 0; k < kSubTiles; ++k)
+        if (k == s) ws = w[k];
+    const float is = warp_incl_scan(ws);
+    float ex = __shfl_up_sync(0xffffffffu, is, 1);
+    if (lane_id() == 0) ex = 0.f;
+    double Sq = 0.0;
+    for (int k = 0; k < (int)warp_id(); ++k) Sq = Sq + (double)wt[s][k];
+    const double lo = spre[s] + (Sq + (double)ex);
+    const double hi = spre[s] + (Sq + (double)is);
+    const int x = c * kChunk + s * kSampThreads + (int)threadIdx.x;
+    if (clamped) {
+        const unsigned mpos = __ballot_sync(0xffffffffu, ws > 0.f);
+        if (lane_id() == 0) wpick[warp_id()] = mpos ? (31 - __clz((int)mpos)) : -1;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int pick = -1;
+            for (int k = 7; k >= 0 && pick < 0; --k)
+                if (wpick[k] >= 0) pick = k * 32 + wpick[k];
+            p.next_token[b] = c * kChunk + s * kSampThreads + (pick < 0 ? 0 : pick) + p.v_begin;
+            if (p.dbg_mass) p.dbg_mass[b] = sh_W;
+            if (p.dbg_flags) p.dbg_flags[b] = 4;
+            flag_draw(p, b, 4);
+        }
+        return;
+    }
+    if (ws > 0.f && lo <= tp && tp < hi) {
+        p.next_token[b] = x + p.v_begin;
+        if (p.dbg_mass) p.dbg_mass[b] = sh_W;
+        if (p.dbg_flags) p.dbg_flags[b] = 0;
+        const double margin = fmin(tp - lo, hi - tp);
+        if (margin <= (double)p.eps_draw) flag_draw(p, b, 0);
+    }
+}
+
 constexpr size_t mass_smem(int nst, int B) { return (size_t)nst * 2 * kChunk * sizeof(float) + (size_t)B * 12; }
 
 // nj_verify_greedy: argmax over the vocabulary of

@@ -57,6 +57,11 @@ for cg in ("1", "2"):
     run(b, NJ_PATH_STAGED)
     print("staged k_lmhead cg" + cg, "ok", flush=True)
 os.environ.pop("NJ_LM_CG", None)
+# k_sample_small (staged, B <= 12: one cluster of 8 CTAs per request, DSMEM chunk masses),
+# 10 chunks of 4096 ids (several per CTA, ragged last chunk)
+b = make_batch(7, "mixed:5", V=40000, d=64, seed=13, device=dev)
+run(b, NJ_PATH_STAGED)
+print("staged small-batch sampler ok", flush=True)
 b = make_batch(6, "mixed:4", V=2048, d=128, seed=5, device=dev)
 grp = ShardGroup(128, 2048, max_batch=6, gamma_max=5, nshards=4)
 acc = torch.empty(6, dtype=torch.int32, device=dev)

@@ -175,12 +175,15 @@ def test_fused_toy_c1(seed):
     check(b, acc, nxt, dd, lnp_tol=1e-5, lse_tol=1e-5)
 
 
-def test_fused_c2_full_size():
+@pytest.mark.parametrize("path", [NJ_PATH_FUSED, NJ_PATH_AUTO])
+def test_fused_c2_full_size(path):
+    """BJ configs[1] (B = 8, gamma = 3) on the fused kernel and on the AUTO path
+    (k_lmhead staged step since kFusedAutoMaxN = 24)."""
     W = w_full()
     for seed in range(4):
         b = make_batch(8, 3, V=QV, d=QD, seed=100 + seed, device=DEV, W=W)
-        acc, nxt, dd, _ = run(b)
-        check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)   # 16-MMA partials, DESIGN.md §6
+        acc, nxt, dd, _ = run(b, path)
+        check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)   # restarted accumulators, DESIGN.md §6
 
 
 @pytest.mark.parametrize("B,g", [(8, "mixed:5"), (1, 0), (48, 0), (16, 2), (12, 3), (6, 5), (24, 1)])
@@ -298,7 +301,7 @@ def test_staged_full_size(B, g):
     token chunks, ragged last chunk), every request vs the oracle."""
     b = make_batch(B, g, V=QV, d=QD, seed=B + 17, device=DEV, W=w_full())
     acc, nxt, dd, v = run(b)
-    assert v.plan(b.gamma)[0] == (NJ_PATH_FUSED if b.N <= 48 else NJ_PATH_STAGED)
+    assert v.plan(b.gamma)[0] == (NJ_PATH_FUSED if b.N <= 24 else NJ_PATH_STAGED)   # kFusedAutoMaxN
     check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
 
 
