@@ -105,7 +105,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -145,6 +145,8 @@ Knobs read_knobs() {
     k.lm_mma4 = env_int("NJ_LM_MMA4", 0);
     k.small = env_int("NJ_SMALL", 1);
     k.small_pdl = env_int("NJ_SMALL_PDL", 1);
+    k.small_cl16 = env_int("NJ_SMALL_CL16", 1);
+    k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
 }
@@ -340,7 +342,9 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
         // fused for the smallest batches only: above kFusedAutoMaxN rows k_lmhead + the sampler
         // kernels are faster (B200: N = 32 203-208 vs 207-210 us, N = 48 210-215 vs 240-248 us;
         // N = 4 fused 193 vs 203 us)
-        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm)) ? NJ_PATH_FUSED
+        // q read in place from host memory (nj_verify_host, zero-copy): the fused kernel's
+        // all-in-flight async copies of the rejected rows beat the staged sampler's
+        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm || c->q_remote)) ? NJ_PATH_FUSED
                : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
         return set_err(c, NJ_EUNSUPPORTED, "fused path needs N <= %d and TMEM room (N=%d)", kFusedMaxN, pl.N);
@@ -352,14 +356,18 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
 
 // k_sample_small (nj_sampler.cuh) takes the unsharded staged path's sampler when
 // one cluster of kSmallCl CTAs per request fits the SMs
-size_t small_sampler_smem(const nj_ctx* c) {   // the CTA's chunks, logits + q
-    return (size_t)((c->nchunks + kSmallCl - 1) / kSmallCl) * 2 * kChunk * sizeof(float);
+// cluster size: 16 CTAs per request for B <= 8 (one cluster per GPC at a time), else 8
+int small_sampler_cl(const nj_ctx* c, int B) { return (B <= 8 && c->kn.small_cl16) ? 16 : kSmallCl; }
+size_t small_sampler_smem(const nj_ctx* c, int B) {   // the CTA's chunks, logits + q
+    const int cl = small_sampler_cl(c, B);
+    return (size_t)((c->nchunks + cl - 1) / cl) * 2 * kChunk * sizeof(float);
 }
 bool small_sampler_ok(const nj_ctx* c, const Plan& pl) {
     // (B <= 12: 16 clusters of 8 did not all fit at once -- B = 16 was slower than the 5 launches)
-    return c->kn.small && pl.path == NJ_PATH_STAGED && !c->sharded() && pl.B <= 12 && pl.B * kSmallCl <= c->num_sms &&
-           c->nchunks <= kSmallMaxChunks && c->cfg.gamma_max + 1 <= kSmallMaxRows && c->cfg.gamma_max <= 32 &&
-           small_sampler_smem(c) <= 200 * 1024;
+    const int cl = small_sampler_cl(c, pl.B);
+    return c->kn.small && pl.path == NJ_PATH_STAGED && !c->sharded() && pl.B <= 12 && pl.B * cl <= c->num_sms &&
+           c->nchunks <= kSmallMaxChunks && c->nchunks <= kSmallMaxPerCta * cl &&
+           c->cfg.gamma_max + 1 <= kSmallMaxRows && small_sampler_smem(c, pl.B) <= 200 * 1024;
 }
 
 ReqMeta make_meta(const Plan& pl) {
@@ -1194,6 +1202,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 2>);
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 1>);
     e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 2>);
     if (const char* ev = getenv("NJ_MASS_NST")) c->mass_nst = std::min(4, std::max(2, atoi(ev)));
     e = e ? e : cudaFuncSetAttribute(k_mass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(2, c->cfg.max_batch));
@@ -1370,6 +1379,12 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             lp.cap_staged = 1;
             lp.B = pl.B;
             for (int b = 0; b <= pl.B; ++b) lp.row_off[b] = pl.row_off[b];
+            // small batches: the q rows into L2 during the GEMM (the sampler reads the rejected
+            // ones right after); device-resident q of a 16-byte-aligned pitch only
+            if (c->kn.qpf && small_sampler_ok(c, pl) && pl.G > 0 && !c->q_remote && (ldq & 3) == 0 &&
+                (reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0 && (size_t)pl.G * ldq * 4 <= (32u << 20)) {
+                lp.qpf = draft_probs + c->cfg.v_begin; lp.qpf_ld = ldq; lp.qpf_rows = pl.G; lp.qpf_cols = c->V_local;
+            }
             if ((s = launch_lm<LM_WRITE | LM_STATS | LM_CAPTURE>(c, st, hidden, W_lm, pl.N, lp, &gridA)) != NJ_OK)
                 return s;
         } else if ((s = launch_lmhead<true, true, true>(c, st, hidden, pl.N, gp, false, &gridA)) != NJ_OK) {
@@ -1396,13 +1411,14 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             mp.dbg_lse = dbg ? dbg->lse : nullptr;
             mp.certify = certify; mp.eps_draw = c->eps_draw;
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(pl.B * kSmallCl);
+            const int cl = small_sampler_cl(c, pl.B);
+            cfg.gridDim = dim3(pl.B * cl);
             cfg.blockDim = dim3(kSampThreads);
-            cfg.dynamicSmemBytes = small_sampler_smem(c);
+            cfg.dynamicSmemBytes = small_sampler_smem(c, pl.B);
             cfg.stream = st;
             cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = kSmallCl;
+            at[0].val.clusterDim.x = cl;
             at[0].val.clusterDim.y = 1;
             at[0].val.clusterDim.z = 1;
             at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;

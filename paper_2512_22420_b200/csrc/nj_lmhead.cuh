@@ -80,6 +80,9 @@ struct LmheadParams {
     unsigned long long* ts;      // debug timeline of CTA 0 (NJ_PHASE_TS): [0, 4K) producer (wait start, wait
                                  // end) per stage, [4K, 8K) MMA (wait start, wait end, commit) per stage,
                                  // [8K, 12K) epilogue warp 0 (output start, output end) per item
+    const float* qpf;            // optional: draft-probability rows prefetched into L2 by the producer
+    int64_t qpf_ld;              //   warps (the staged sampler reads the rejected ones right after)
+    int32_t qpf_rows, qpf_cols;
     int32_t B;
     int32_t row_off[kMaxB + 1];
 };
@@ -193,6 +196,16 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     if (warp == kLmWarpTMA) {
         // ------------------------------------------------ TMA producer (both CTAs)
         // whole warp in convergent control flow, one elected lane issues
+        if (p.qpf && lane == 0) {
+            // this CTA's share of the q rows, 32 KB segments, spread over the grid
+            constexpr int kSeg = 8192;   // floats
+            const int nseg = (p.qpf_cols + kSeg - 1) / kSeg;
+            for (int i = (int)blockIdx.x; i < p.qpf_rows * nseg; i += (int)gridDim.x) {
+                const int r = i / nseg, sg = i - r * nseg;
+                const int c0 = sg * kSeg, n = min(kSeg, p.qpf_cols - c0) & ~3;
+                if (n > 0) bulk_prefetch_l2(p.qpf + (int64_t)r * p.qpf_ld + c0, (uint32_t)n * 4u);
+            }
+        }
         const uint64_t pol_w = p.w_evict_first ? policy_evict_first() : policy_evict_last();
         const uint64_t pol_h = policy_evict_last();
         int s = 0;

@@ -476,7 +476,8 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
 // arithmetic and its order are k_accept's, k_mass's and k_locate's (bit-identical
 // decisions, masses and draws); only the launches and the global round trips
 // between them are gone (~20 us of a ~205 us step at C2).
-constexpr int kSmallCl = 8;
+constexpr int kSmallCl = 8;         // CTAs per request (16 when B <= 8: one cluster per GPC)
+constexpr int kSmallMaxPerCta = 8;  // chunks per CTA (nchunks <= 8 * cluster size)
 constexpr int kSmallMaxChunks = 64;
 constexpr int kSmallMaxRows = 16;   // gamma_max <= 15
 __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParams ap, const MassParams p,
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int b = (int)cluster_id_x();
     const int rank = (int)cluster_ctarank();
+    const int CL = (int)cluster_nctarank();   // 8 or 16 CTAs per request
     const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
     __shared__ double s_lrow[kSmallMaxRows];
     __shared__ int s_n;
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     extern __shared__ __align__(16) float stage[];   // [chunks of this CTA][2][kChunk]
     {
         int k = 0;
-        for (int c = rank; c < p.nchunks; c += kSmallCl, ++k) {
+        for (int c = rank; c < p.nchunks; c += CL, ++k) {
             const int x0 = c * kChunk, nn = min(kChunk, p.V_local - x0);
             mass_copy_chunk(stage + (size_t)k * 2 * kChunk, lrow + x0, nn);
             if (resid) mass_copy_chunk(stage + (size_t)k * 2 * kChunk + kChunk, qrow + x0, nn);
@@ -557,8 +559,12 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
         cp_async_wait_all();
         __syncthreads();
     }
+    // every chunk's 16 sub-tile warp totals first (no barrier between chunks), then
+    // all sub-tile sums in parallel and each chunk total (k_mass's fp64 orders)
+    __shared__ float wtc[kSmallMaxPerCta][kSubTiles][8];
+    __shared__ double sstc[kSmallMaxPerCta][kSubTiles];
     int kk = 0;
-    for (int c = rank; c < p.nchunks; c += kSmallCl, ++kk) {
+    for (int c = rank; c < p.nchunks; c += CL, ++kk) {
         const float* sl = stage + (size_t)kk * 2 * kChunk;
         const float* sq = sl + kChunk;
         const int x0 = c * kChunk + (int)threadIdx.x;
@@ -570,28 +576,29 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
             const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
             v[s2] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
         }
-        warp_totals16(v, wt);
-        __syncthreads();
-        if (threadIdx.x < kSubTiles) {
-            double st = 0.0;
+        warp_totals16(v, wtc[kk]);
+    }
+    const int nmine = kk;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nmine * kSubTiles; t += kSampThreads) {
+        const int k2 = t / kSubTiles, s2 = t - k2 * kSubTiles;
+        double st = 0.0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) st = st + (double)wt[threadIdx.x][k];
-            sst[threadIdx.x] = st;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double acc = 0.0;
+        for (int k = 0; k < 8; ++k) st = st + (double)wtc[k2][s2][k];
+        sstc[k2][s2] = st;
+    }
+    __syncthreads();
+    for (int k2 = threadIdx.x; k2 < nmine; k2 += kSampThreads) {
+        double acc = 0.0;
 #pragma unroll
-            for (int k = 0; k < kSubTiles; ++k) acc = acc + sst[k];
-            cml[c] = acc;
-        }
-        __syncthreads();
+        for (int s2 = 0; s2 < kSubTiles; ++s2) acc = acc + sstc[k2][s2];
+        cml[rank + k2 * CL] = acc;
     }
     // (4) every chunk mass from the CTA that owns it (distributed shared memory); the
     //     second cluster barrier keeps each CTA's cml alive until all have read it
     cluster_sync_all();
     for (int c = threadIdx.x; c < p.nchunks; c += kSampThreads)
-        cm[c] = ld_shared_cluster_f64(mapa_shared(&cml[c], (uint32_t)(c % kSmallCl)));
+        cm[c] = ld_shared_cluster_f64(mapa_shared(&cml[c], (uint32_t)(c % CL)));
     __syncthreads();
     cluster_sync_all();
     // (5) the draw: k_locate's unsharded arithmetic; the CTA owning the located chunk finishes
@@ -628,11 +635,11 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
         return;
     }
     const int c = sh_c;
-    if (c % kSmallCl != rank) return;
+    if (c % CL != rank) return;
     const double tp = sh_tp;
     float w[kSubTiles], v[kSubTiles];
     {   // the located chunk's weights again, from this CTA's staged copy (same expression)
-        const float* sl = stage + (size_t)(c / kSmallCl) * 2 * kChunk;
+        const float* sl = stage + (size_t)(c / CL) * 2 * kChunk;
         const float* sq = sl + kChunk;
         const int x0 = c * kChunk + (int)threadIdx.x;
 #pragma unroll
