@@ -234,6 +234,7 @@ struct MassParams {
     int32_t grid2;
     int32_t pld2;          // part2 row stride (>= grid2)
     int32_t part2_by_row;  // 1: part2 row of request b is s_row[b] (vocab-sharded staged step)
+    int32_t pf_rows;       // k_sample_small: L2-prefetch the candidate rows while testing
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -491,6 +492,18 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
     __shared__ double s_lrow[kSmallMaxRows];
     __shared__ int s_n;
+    // every candidate sample row's (and its q row's) chunks of this CTA into L2 while
+    // the acceptance tests run; the staging after them then hits L2
+    if (p.pf_rows && threadIdx.x < 32) {
+        const int c = rank + (int)(threadIdx.x >> 2) * CL;   // lanes: (chunk slot, 4 rows each)
+        if (c < p.nchunks) {
+            const int x0 = c * kChunk, nn = min(kChunk, p.V_local - x0) & ~3;
+            for (int i = (int)(threadIdx.x & 3); i <= gam; i += 4) {
+                bulk_prefetch_l2(p.logits + (int64_t)(ro + i) * p.ld + x0, (uint32_t)nn * 4u);
+                if (i < gam) bulk_prefetch_l2(p.q + (int64_t)(g0 + i) * p.ldq + p.v_begin + x0, (uint32_t)nn * 4u);
+            }
+        }
+    }
     __shared__ double cml[kSmallMaxChunks];   // this CTA's chunk masses (slot = chunk)
     __shared__ double cm[kSmallMaxChunks];    // every chunk mass of the request
     __shared__ float wt[kSubTiles][8];
