@@ -36,8 +36,9 @@ def load():
         lib.njp_logits_ks.argtypes = [P, P, I32, I32, P, I32, P, I64, I32]
         lib.njp_stream_test.argtypes = [P, P, I32, I32, I32, I32, I32, P, I32, I32]
         lib.njp_mma_probe.argtypes = [P, I32, I32, I32, P]
+        lib.njp_mma_probe_cg2.argtypes = [P, I32, I32, I32, P]
         lib.njp_tmem_bw.argtypes = [P, I32, I32, I32, I32, I32, P]
-        for f in (lib.njp_logits_ks, lib.njp_stream_test, lib.njp_mma_probe, lib.njp_tmem_bw):
+        for f in (lib.njp_logits_ks, lib.njp_stream_test, lib.njp_mma_probe, lib.njp_mma_probe_cg2, lib.njp_tmem_bw):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -69,6 +70,10 @@ def stream_test(W, mode: int, group: int, nstages: int, H=None, hrows: int = 0, 
 
 def mma_probe(n: int, iters: int, mode: int, out):
     _ok(load().njp_mma_probe(_st(), n, iters, mode, out.data_ptr()), "njp_mma_probe")
+
+
+def mma_probe_cg2(n: int, iters: int, mode: int, out):
+    _ok(load().njp_mma_probe_cg2(_st(), n, iters, mode, out.data_ptr()), "njp_mma_probe_cg2")
 
 
 def tmem_bw(nwarps: int, x: int, inflight: int, cols: int, rounds: int, out):

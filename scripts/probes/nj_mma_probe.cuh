@@ -54,4 +54,50 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int n, int iters, int mode
     if (warp_id() == 0) tmem_dealloc(tbase, 256);
 }
 
+// The same issue loop for a CTA pair (cta_group::2, M = 256 over two SMs, each CTA
+// holding its 128 A rows and HALF of the N B rows): the leader issues, the
+// commit is multicast to both CTAs.  Reports the leader's cycles per group.
+__global__ void __launch_bounds__(128, 1) k_mma_probe_cg2(int n, int iters, int mode, long long* out) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sA = smem;                       // 16 KB
+    uint8_t* sB = smem + kTileBytesA;         // (n / 2) x 128 B
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 128 * 128);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    const bool leader = cluster_ctarank() == 0;
+    for (int i = threadIdx.x; i < (kTileBytesA + 128 * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    if (threadIdx.x == 0) { mbar_init(bar, 1); fence_barrier_init(); }
+    if (warp_id() == 0) tmem_alloc_cg2(slot, 256);
+    fence_proxy_async();
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tbase = *slot;
+    if (leader && threadIdx.x == 32) {
+        const uint32_t idesc = idesc_bf16_f32(256, (uint32_t)n);
+        const uint64_t ad = sdesc_sw128(sA), bd = sdesc_sw128(sB);
+        uint32_t ph = 0;
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_bf16_cg2(tbase, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+            if (mode == 1) {
+                mma_commit_mc2(bar, 3);
+                mbar_wait(bar, ph);
+                ph ^= 1;
+            } else if (mode == 2) {
+                mma_commit_mc2(bar, 3);
+            }
+        }
+        if (mode != 2) {
+            mma_commit_mc2(bar, 3);
+            mbar_wait(bar, ph);
+        }
+        out[blockIdx.x] = (clock64() - t0) / iters;
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();   // the peer's barrier / TMEM stay alive until the leader is done
+    if (warp_id() == 0) tmem_dealloc_cg2(tbase, 256);
+}
+
 }  // namespace nj

@@ -117,6 +117,29 @@ int njp_mma_probe(void* stream, int32_t n, int32_t iters, int32_t mode, int64_t*
     return cudaGetLastError() == cudaSuccess ? 0 : 3;
 }
 
+int njp_mma_probe_cg2(void* stream, int32_t n, int32_t iters, int32_t mode, int64_t* cycles_out) {
+    if (!cycles_out || n < 32 || n > 256 || n % 32 || iters < 1) return 1;
+    const size_t smem = kTileBytesA + 128 * 128 + 64;
+    if (cudaFuncSetAttribute(k_mma_probe_cg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return 3;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((num_sms() / 2) * 2);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, k_mma_probe_cg2, (int)n, (int)iters, (int)mode,
+                           reinterpret_cast<long long*>(cycles_out)) != cudaSuccess)
+        return 3;
+    return cudaGetLastError() == cudaSuccess ? 0 : 3;
+}
+
 // TMEM read bandwidth: one CTA per SM, nwarps (4..16) warps each reading its
 // slice of `cols` (<= 512) columns of its lane quadrant `rounds` times with
 // 32x32b.x{16,32} loads, `inflight` (1, 2, 4) per tcgen05.wait::ld.
