@@ -16,16 +16,39 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int n, int iters, int mode
     uint8_t* sA = smem;                       // 16 KB: 128 x 64 bf16 (contents irrelevant)
     uint8_t* sB = smem + kTileBytesA;         // n x 128 B
     uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 256 * 128);
-    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
     for (int i = threadIdx.x; i < (kTileBytesA + 256 * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
-    if (threadIdx.x == 0) { mbar_init(bar, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(bar, 1); mbar_init(bar + 1, 1); fence_barrier_init(); mbar_arrive(bar + 1); }
     if (warp_id() == 0) tmem_alloc(slot, 256);
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *slot;
-    if (threadIdx.x == 32) {
+    if (mode >= 4 && warp_id() == 1) {
+        // modes 4 / 5: the whole warp runs the loop (convergent), one elected lane issues
+        // (mma_bf16_w / mma_kblock_w, as k_gemm_big / k_lmhead do); commit per group
+        const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)n);
+        const uint64_t ad = sdesc_sw128(sA), bd = sdesc_sw128(sB);
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            if (mode == 6 || mode == 7) {
+                // an operand-ready wait on an already completed barrier before every k-block:
+                // 6 warp-uniform try_wait + vote (mbar_wait_w), 7 test_wait by every lane + vote
+                if (mode == 6) mbar_wait_w(bar + 1, 0);
+                else while (!__all_sync(0xffffffffu, mbar_test_wait(smem_u32(bar + 1), 0))) {}
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mma_bf16_w(tbase, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+            } else if (mode == 4) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mma_bf16_w(tbase, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
+            } else {
+                mma_kblock_w<1>(tbase, ad, bd, idesc, it != 0);
+            }
+            mma_commit_w(bar);
+        }
+        if (lane_id() == 0) out[blockIdx.x] = (clock64() - t0) / iters;
+    } else if (mode < 4 && threadIdx.x == 32) {
         const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)n);
         const uint64_t ad = sdesc_sw128(sA), bd = sdesc_sw128(sB);
         uint32_t ph = 0;

@@ -109,7 +109,7 @@ int njp_stream_test(void* stream, const uint16_t* W, int32_t V, int32_t d, int32
 // from resident smem operands; cycles_out[num_SMs] = cycles per group.
 int njp_mma_probe(void* stream, int32_t n, int32_t iters, int32_t mode, int64_t* cycles_out) {
     if (!cycles_out || n < 16 || n > 256 || n % 16 || iters < 1) return 1;
-    const size_t smem = kTileBytesA + 256 * 128 + 64;
+    const size_t smem = kTileBytesA + 256 * 128 + 64 + 16;
     if (cudaFuncSetAttribute(k_mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 3;
     k_mma_probe<<<num_sms(), 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
