@@ -670,9 +670,14 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     if (c->kn.lm_s > 0) S = std::min(S, std::max(2, c->kn.lm_s));
     if (S < 2) return set_err(c, NJ_EUNSUPPORTED, "k_lmhead: not enough shared memory (R=%d)", R);
     p.nstages = S;
+    p.nstages_mem = 0;
+    if ((p.dbg & 48) == 48 && c->kn.lm_s > S) {   // probe without loads: more barrier stages than memory
+        p.nstages_mem = S;
+        p.nstages = std::min(c->kn.lm_s, 8);
+    }
     // the MMA warp takes two 1-k-block stages per operand wait (sweep: -2..-6 % vs one)
     p.mb = c->kn.lm_mb > 0 ? std::min(c->kn.lm_mb, S - 1) : std::max(1, std::min(2, S - 2));
-    const size_t smem = (size_t)S * stage + tail;
+    const size_t smem = (size_t)(p.nstages_mem > 0 ? p.nstages_mem : p.nstages) * stage + tail;
     const int grid = pl.nunits * CG;
     if (CG == 2) {
         cudaLaunchConfig_t cfg = {};

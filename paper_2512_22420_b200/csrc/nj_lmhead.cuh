@@ -51,6 +51,7 @@ struct LmheadParams {
     int32_t V_local, U, num_kb;  // local vocabulary, its 16-id units, k-blocks
     int32_t nstages, gk, ks;     // ring stages, k-blocks per stage, k-blocks per accumulator restart
     int32_t mb;                  // ring stages the MMA warp consumes per operand wait (1, 2, ...)
+    int32_t nstages_mem;         // probe only (no-load runs): ring stages backed by shared memory (0: all)
     int32_t ks0;                 // k-blocks of the first accumulator group of every item (>= ks)
     int32_t arv1;                // 1: one accumulator-release arrival per CTA (named barrier first)
     int32_t fence_full;          // probe: tcgen05.fence::after_thread_sync after every operand wait
@@ -116,6 +117,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                    ARGMAX = MODE & LM_ARGMAX;
     extern __shared__ __align__(1024) uint8_t smem[];
     const int S = p.nstages, GK = p.gk;
+    const int SM_ = p.nstages_mem > 0 ? p.nstages_mem : S;   // ring stages backed by memory (probe: < S)
     const uint32_t wBytes = (uint32_t)p.wbox * 128u;                 // this CTA's W box per k-block
     // H box: 128 token rows, or fewer (a multiple of 8) when the launch has fewer rows
     // (single chunk): the MMA still reads 128 rows, the ones past the box are garbage
@@ -125,7 +127,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     const int nloc = kLmTok;                                          // this CTA's token rows (one chunk)
     uint8_t* ring = smem;
     // WRITE via TMA: per epilogue warp two 2-KB staging boxes (32 rows x 16 fp32, 64B-swizzled)
-    uint8_t* ostage = ring + (size_t)S * stageBytes;
+    uint8_t* ostage = ring + (size_t)SM_ * stageBytes;
     const size_t ostageBytes = (WRITE && p.tma_out) ? (size_t)kLmEpiWarps * p.ost_n * 2048 : 0;
     float2* state = reinterpret_cast<float2*>(ostage + ostageBytes);   // [4 slices][nloc]
     int32_t* stok = reinterpret_cast<int32_t*>(state + ((STATS || ARGMAX) ? 4 * nloc : 0));   // [nloc]
@@ -227,7 +229,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                 if (tsx) p.ts[2 * si] = globaltimer();
                 mbar_wait_w(&empty[s], ph ^ 1);
                 if (tsx) p.ts[2 * si + 1] = globaltimer();
-                uint8_t* st = ring + (size_t)s * stageBytes;
+                uint8_t* st = ring + (size_t)(s % SM_) * stageBytes;
                 const bool ldh = !(p.dbg & 16), ldw = !(p.dbg & 32);   // probes
                 const uint32_t kbb = (ldh ? hBytes : 0u) + (ldw ? wBytes : 0u);
                 if (CG == 1) {
@@ -306,7 +308,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     for (int m = 0; m < nst; ++m) {
                         const int kg = kg0 + m;
                         const int ng = min(GK, p.num_kb - kg * GK);
-                        uint8_t* st = ring + (size_t)s * stageBytes;
+                        uint8_t* st = ring + (size_t)(s % SM_) * stageBytes;
                         for (int g = 0; g < ng; ++g) {
                             if (kin == 0) {
                                 mbar_wait_w(&aempty[abuf], aph ^ 1);
