@@ -105,7 +105,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -146,7 +146,8 @@ Knobs read_knobs() {
     k.small = env_int("NJ_SMALL", 1);
     k.small_pdl = env_int("NJ_SMALL_PDL", 1);
     k.small_cl16 = env_int("NJ_SMALL_CL16", 1);
-    k.small_pf = env_int("NJ_SMALL_PF", 0);   // measured slower (C2 204.7 vs 200.5 us)
+    k.small_pf = env_int("NJ_SMALL_PF", 0);
+    k.lm_sleep = env_int("NJ_LM_SLEEP", 0);   // measured slower (C2 204.7 vs 200.5 us)
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
@@ -628,6 +629,7 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     // 8.6e-7 vs 6.9e-7 over 256 Qwen-shape rows)
     p.ks0 = std::max(p.ks, c->kn.lm_ks0 > 0 ? c->kn.lm_ks0 : 8);
     p.arv1 = c->kn.lm_arv1;
+    p.sleep_ns = c->kn.lm_sleep;
     p.fence_full = c->kn.lm_fence;
     p.mma4 = c->kn.lm_mma4;
     p.dbg = c->kn.lm_dbg;

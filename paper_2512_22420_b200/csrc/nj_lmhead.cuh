@@ -52,6 +52,7 @@ struct LmheadParams {
     int32_t nstages, gk, ks;     // ring stages, k-blocks per stage, k-blocks per accumulator restart
     int32_t mb;                  // ring stages the MMA warp consumes per operand wait (1, 2, ...)
     int32_t nstages_mem;         // probe only (no-load runs): ring stages backed by shared memory (0: all)
+    int32_t sleep_ns;            // epilogue accumulator waits: test_wait + nanosleep backoff (0: try_wait)
     int32_t ks0;                 // k-blocks of the first accumulator group of every item (>= ks)
     int32_t arv1;                // 1: one accumulator-release arrival per CTA (named barrier first)
     int32_t fence_full;          // probe: tcgen05.fence::after_thread_sync after every operand wait
@@ -77,7 +78,7 @@ struct LmheadParams {
     int32_t v_begin;
     int32_t dbg;                 // probe bits (results garbage): 1 no MMAs, 2 no TMEM drain, 8 no per-item output,
                                  // 16 no H loads, 32 no W loads, 64 every unit loads unit 0's addresses,
-                                 // 128 no logits stores, 256 no statistics
+                                 // 128 no logits stores, 256 no statistics, 512 no ring handshakes (with 48)
     unsigned long long* ts;      // debug timeline of CTA 0 (NJ_PHASE_TS): [0, 4K) producer (wait start, wait
                                  // end) per stage, [4K, 8K) MMA (wait start, wait end, commit) per stage,
                                  // [8K, 12K) epilogue warp 0 (output start, output end) per item
@@ -195,7 +196,9 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
+    const bool noring = (p.dbg & 512) != 0;   // probe: no ring handshakes at all (no loads either)
     if (warp == kLmWarpTMA) {
+      if (!noring) {
         // ------------------------------------------------ TMA producer (both CTAs)
         // whole warp in convergent control flow, one elected lane issues
         if (p.qpf && lane == 0) {
@@ -273,6 +276,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                 if (++s == S) { s = 0; ph ^= 1; }
             }
         }
+      }
     } else if (warp == kLmWarpMMA) {
         if (leader) {
             // ------------------------------------------------ MMA issuer (leader CTA)
@@ -296,7 +300,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     {
                         int s2 = s;
                         uint32_t ph2 = ph;
-                        for (int m = 0; m < nst; ++m) {
+                        for (int m = 0; m < nst && !noring; ++m) {
                             mbar_wait_w(&full[s2], ph2);
                             if (++s2 == S) { s2 = 0; ph2 ^= 1; }
                         }
@@ -338,8 +342,10 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                                 kin = 0;
                             }
                         }
-                        if (CG == 2) mma_commit_mc2_w(&empty[s], 3);
-                        else mma_commit_w(&empty[s]);
+                        if (!noring) {
+                            if (CG == 2) mma_commit_mc2_w(&empty[s], 3);
+                            else mma_commit_w(&empty[s]);
+                        }
                         if (++s == S) { s = 0; ph ^= 1; }
                     }
                     if (tsx) p.ts[4096 + 3 * si + 2] = globaltimer();
@@ -375,7 +381,8 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                 const int gi = it * ngroups + g;
                 const bool tsg = p.ts != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0 && gi < 1000;
                 if (tsg) p.ts[12288 + 2 * gi] = globaltimer();
-                mbar_wait(&afull[buf], eph);
+                if (p.sleep_ns > 0) mbar_wait_sleep(&afull[buf], eph, (uint32_t)p.sleep_ns);
+                else mbar_wait(&afull[buf], eph);
                 if (tsg) p.ts[12288 + 2 * gi + 1] = globaltimer();
                 if (++ebuf == NBUF) { ebuf = 0; eph ^= 1; }
                 tc_fence_after();
