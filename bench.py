@@ -660,10 +660,18 @@ def bench_c5(args, ws, rank, local):
     communicator."""
     import torch
 
-    from paper_2512_22420_b200 import NJ_OPT_PROFILE, NcclComm, Verifier, nccl_unique_id, shard_range
+    from paper_2512_22420_b200 import NJ_OPT_PROFILE, NJ_PATH_STAGED, NcclComm, Verifier, nccl_unique_id, shard_range
     from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
+    if local >= torch.cuda.device_count():
+        # NCCL needs one device per rank: the vocab-sharded step cannot oversubscribe a GPU
+        # (the request-sharded configs can); report instead of failing the launcher
+        if rank == 0 or local == torch.cuda.device_count():
+            emit({"metric": METRIC, "config": {"workload": "qwen7b_c5_vocab_sharded"}, "n_gpus": ws,
+                  "unavailable": f"c5 needs one GPU per rank (NCCL): {ws} ranks, "
+                                 f"{torch.cuda.device_count()} GPU(s) visible"})
+        return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -736,8 +744,10 @@ def bench_c5(args, ws, rank, local):
     toks = int((acc + 1).sum().item())
     hbm, tf_burst, _, peak_src = load_peaks()
     kern_ms = kms / max(kn, 1)
-    flops = 2.0 * b.G * (ve - vb) * D_Q
-    roof = {"kernel": "k_gemm_big<stats> (K-A, draft rows, this rank's shard)", "bound": "tensor",
+    staged = v.plan(b.gamma)[0] == NJ_PATH_STAGED   # the staged sharded step: k_lmhead over all N rows
+    flops = 2.0 * (b.N if staged else b.G) * (ve - vb) * D_Q
+    roof = {"kernel": ("k_lmhead<logits,stats,capture> (all N rows, this rank's shard)" if staged else
+                       "k_gemm_big<stats> (K-A, draft rows, this rank's shard)"), "bound": "tensor",
             "achieved": flops / (kern_ms / 1e3) / 1e12, "peak": tf_burst, "unit": "TFLOP/s",
             "frac": flops / (kern_ms / 1e3) / 1e12 / tf_burst, "algorithmic_flops_per_launch": flops,
             "peak_source": peak_src, "kernel_ms_avg": kern_ms, "kernel_share_of_step": kms / ms_eager,
@@ -806,6 +816,14 @@ def bench_propose(args, ws, rank, local):
     from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
+    if local >= torch.cuda.device_count():
+        # NCCL needs one device per rank: the vocab-sharded step cannot oversubscribe a GPU
+        # (the request-sharded configs can); report instead of failing the launcher
+        if rank == 0 or local == torch.cuda.device_count():
+            emit({"metric": METRIC, "config": {"workload": "qwen7b_c5_vocab_sharded"}, "n_gpus": ws,
+                  "unavailable": f"c5 needs one GPU per rank (NCCL): {ws} ranks, "
+                                 f"{torch.cuda.device_count()} GPU(s) visible"})
+        return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -938,6 +956,14 @@ def bench_greedy(args, ws, rank, local):
     from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
+    if local >= torch.cuda.device_count():
+        # NCCL needs one device per rank: the vocab-sharded step cannot oversubscribe a GPU
+        # (the request-sharded configs can); report instead of failing the launcher
+        if rank == 0 or local == torch.cuda.device_count():
+            emit({"metric": METRIC, "config": {"workload": "qwen7b_c5_vocab_sharded"}, "n_gpus": ws,
+                  "unavailable": f"c5 needs one GPU per rank (NCCL): {ws} ranks, "
+                                 f"{torch.cuda.device_count()} GPU(s) visible"})
+        return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
