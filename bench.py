@@ -664,10 +664,10 @@ def bench_c5(args, ws, rank, local):
     from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
-    if local >= torch.cuda.device_count():
+    if ws > torch.cuda.device_count():
         # NCCL needs one device per rank: the vocab-sharded step cannot oversubscribe a GPU
-        # (the request-sharded configs can); report instead of failing the launcher
-        if rank == 0 or local == torch.cuda.device_count():
+        # (the request-sharded configs can); every rank stops, rank 0 reports
+        if rank == 0:
             emit({"metric": METRIC, "config": {"workload": "qwen7b_c5_vocab_sharded"}, "n_gpus": ws,
                   "unavailable": f"c5 needs one GPU per rank (NCCL): {ws} ranks, "
                                  f"{torch.cuda.device_count()} GPU(s) visible"})
@@ -816,10 +816,10 @@ def bench_propose(args, ws, rank, local):
     from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
-    if local >= torch.cuda.device_count():
+    if ws > torch.cuda.device_count():
         # NCCL needs one device per rank: the vocab-sharded step cannot oversubscribe a GPU
-        # (the request-sharded configs can); report instead of failing the launcher
-        if rank == 0 or local == torch.cuda.device_count():
+        # (the request-sharded configs can); every rank stops, rank 0 reports
+        if rank == 0:
             emit({"metric": METRIC, "config": {"workload": "qwen7b_c5_vocab_sharded"}, "n_gpus": ws,
                   "unavailable": f"c5 needs one GPU per rank (NCCL): {ws} ranks, "
                                  f"{torch.cuda.device_count()} GPU(s) visible"})
@@ -956,10 +956,10 @@ def bench_greedy(args, ws, rank, local):
     from paper_2512_22420_b200 import dist as njdist
     from synth.inputs import make_batch, make_weight
 
-    if local >= torch.cuda.device_count():
+    if ws > torch.cuda.device_count():
         # NCCL needs one device per rank: the vocab-sharded step cannot oversubscribe a GPU
-        # (the request-sharded configs can); report instead of failing the launcher
-        if rank == 0 or local == torch.cuda.device_count():
+        # (the request-sharded configs can); every rank stops, rank 0 reports
+        if rank == 0:
             emit({"metric": METRIC, "config": {"workload": "qwen7b_c5_vocab_sharded"}, "n_gpus": ws,
                   "unavailable": f"c5 needs one GPU per rank (NCCL): {ws} ranks, "
                                  f"{torch.cuda.device_count()} GPU(s) visible"})
