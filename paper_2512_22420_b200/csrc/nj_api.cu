@@ -105,7 +105,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -146,8 +146,9 @@ Knobs read_knobs() {
     k.small = env_int("NJ_SMALL", 1);
     k.small_pdl = env_int("NJ_SMALL_PDL", 1);
     k.small_cl16 = env_int("NJ_SMALL_CL16", 1);
-    k.small_pf = env_int("NJ_SMALL_PF", 0);
-    k.lm_sleep = env_int("NJ_LM_SLEEP", 0);   // measured slower (C2 204.7 vs 200.5 us)
+    k.small_pf = env_int("NJ_SMALL_PF", 0);          // measured slower (C2 204.7 vs 200.5 us)
+    k.lm_sleep = env_int("NJ_LM_SLEEP", 0);
+    k.small_bmax = env_int("NJ_SMALL_BMAX", 12);   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
@@ -358,18 +359,26 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
 
 // k_sample_small (nj_sampler.cuh) takes the unsharded staged path's sampler when
 // one cluster of kSmallCl CTAs per request fits the SMs
-// cluster size: 16 CTAs per request for B <= 8 (one cluster per GPC at a time), else 8
-int small_sampler_cl(const nj_ctx* c, int B) { return (B <= 8 && c->kn.small_cl16) ? 16 : kSmallCl; }
-size_t small_sampler_smem(const nj_ctx* c, int B) {   // the CTA's chunks, logits + q
+// cluster size: 16 CTAs per request for B <= 8 (one cluster per GPC at a time), 8 up to
+// B = 12 (16 clusters of 8 did not all fit at once), then 4 / 2 while B * cluster <= SMs
+int small_sampler_cl(const nj_ctx* c, int B) {
+    if (B <= 8 && c->kn.small_cl16) return 16;
+    if (B <= 12) return kSmallCl;
+    return B * 4 <= c->num_sms ? 4 : 2;
+}
+int small_sampler_pb(const nj_ctx* c, int B) {   // chunks per staged batch (two buffers)
     const int cl = small_sampler_cl(c, B);
-    return (size_t)((c->nchunks + cl - 1) / cl) * 2 * kChunk * sizeof(float);
+    const int nmine = (c->nchunks + cl - 1) / cl;
+    return std::max(1, std::min(3, nmine));
+}
+size_t small_sampler_smem(const nj_ctx* c, int B) {   // two batch buffers of logits + q chunks
+    return (size_t)2 * small_sampler_pb(c, B) * 2 * kChunk * sizeof(float);
 }
 bool small_sampler_ok(const nj_ctx* c, const Plan& pl) {
-    // (B <= 12: 16 clusters of 8 did not all fit at once -- B = 16 was slower than the 5 launches)
     const int cl = small_sampler_cl(c, pl.B);
-    return c->kn.small && pl.path == NJ_PATH_STAGED && !c->sharded() && pl.B <= 12 && pl.B * cl <= c->num_sms &&
-           c->nchunks <= kSmallMaxChunks && c->nchunks <= kSmallMaxPerCta * cl &&
-           c->cfg.gamma_max + 1 <= kSmallMaxRows && small_sampler_smem(c, pl.B) <= 200 * 1024;
+    return c->kn.small && pl.path == NJ_PATH_STAGED && !c->sharded() && pl.B <= c->kn.small_bmax &&
+           pl.B * cl <= c->num_sms && c->nchunks <= kSmallMaxChunks && c->cfg.gamma_max + 1 <= kSmallMaxRows &&
+           small_sampler_smem(c, pl.B) <= 200 * 1024;
 }
 
 ReqMeta make_meta(const Plan& pl) {
@@ -1418,6 +1427,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
             mp.dbg_lse = dbg ? dbg->lse : nullptr;
             mp.certify = certify; mp.eps_draw = c->eps_draw;
+            mp.small_pb = small_sampler_pb(c, pl.B);
             mp.pf_rows = c->kn.small_pf && !c->q_remote && (ldq & 3) == 0 && (c->V_local & 3) == 0 &&
                          (reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0;
             cudaLaunchConfig_t cfg = {};

@@ -235,6 +235,7 @@ struct MassParams {
     int32_t pld2;          // part2 row stride (>= grid2)
     int32_t part2_by_row;  // 1: part2 row of request b is s_row[b] (vocab-sharded staged step)
     int32_t pf_rows;       // k_sample_small: L2-prefetch the candidate rows while testing
+    int32_t small_pb;      // k_sample_small: chunks per staged batch
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
 // decisions, masses and draws); only the launches and the global round trips
 // between them are gone (~20 us of a ~205 us step at C2).
 constexpr int kSmallCl = 8;         // CTAs per request (16 when B <= 8: one cluster per GPC)
-constexpr int kSmallMaxPerCta = 8;  // chunks per CTA (nchunks <= 8 * cluster size)
+constexpr int kSmallMaxPerCta = 4;  // chunks per staged batch (two batch buffers of <= 3 x 32 KB)
 constexpr int kSmallMaxChunks = 64;
 constexpr int kSmallMaxRows = 16;   // gamma_max <= 15
 __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParams ap, const MassParams p,
@@ -558,54 +559,69 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     const float* qrow = resid ? p.q + (int64_t)(g0 + n) * p.ldq + p.v_begin : nullptr;
     const double lse = s_lrow[n];
     const float lsef = (float)lse, corr = lse_corr(lse);
-    // (3) this CTA's chunk masses (k_mass's weights and reduction order); all of its
-    //     chunks (logits, and q for a residual row) staged with cp.async at once
-    extern __shared__ __align__(16) float stage[];   // [chunks of this CTA][2][kChunk]
-    {
-        int k = 0;
-        for (int c = rank; c < p.nchunks; c += CL, ++k) {
-            const int x0 = c * kChunk, nn = min(kChunk, p.V_local - x0);
-            mass_copy_chunk(stage + (size_t)k * 2 * kChunk, lrow + x0, nn);
-            if (resid) mass_copy_chunk(stage + (size_t)k * 2 * kChunk + kChunk, qrow + x0, nn);
-        }
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncthreads();
-    }
-    // every chunk's 16 sub-tile warp totals first (no barrier between chunks), then
-    // all sub-tile sums in parallel and each chunk total (k_mass's fp64 orders)
+    // (3) this CTA's chunk masses (k_mass's weights and reduction order): its chunks
+    //     c = rank, rank + CL, ... (logits, and q for a residual row) staged with cp.async
+    //     in batches of PB chunks, double-buffered; per batch every chunk's 16 sub-tile
+    //     warp totals first, then the sub-tile sums in parallel and each chunk total
+    extern __shared__ __align__(16) float stage[];   // [2 buffers][PB][2][kChunk]
     __shared__ float wtc[kSmallMaxPerCta][kSubTiles][8];
     __shared__ double sstc[kSmallMaxPerCta][kSubTiles];
-    int kk = 0;
-    for (int c = rank; c < p.nchunks; c += CL, ++kk) {
-        const float* sl = stage + (size_t)kk * 2 * kChunk;
-        const float* sq = sl + kChunk;
-        const int x0 = c * kChunk + (int)threadIdx.x;
-        float v[kSubTiles];
-#pragma unroll
-        for (int s2 = 0; s2 < kSubTiles; ++s2) {
-            const int o = s2 * kSampThreads + (int)threadIdx.x;
-            const bool in = x0 + s2 * kSampThreads < p.V_local;
-            const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
-            v[s2] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
+    const int PB = p.small_pb;
+    const int nmine = rank < p.nchunks ? (p.nchunks - rank + CL - 1) / CL : 0;
+    const int nbat = (nmine + PB - 1) / PB;
+    auto stage_batch = [&](int bi) {
+        float* buf = stage + (size_t)(bi & 1) * PB * 2 * kChunk;
+        for (int k = 0; k < PB; ++k) {
+            const int j = bi * PB + k;
+            if (j >= nmine) break;
+            const int x0 = (rank + j * CL) * kChunk, nn = min(kChunk, p.V_local - x0);
+            mass_copy_chunk(buf + (size_t)k * 2 * kChunk, lrow + x0, nn);
+            if (resid) mass_copy_chunk(buf + (size_t)k * 2 * kChunk + kChunk, qrow + x0, nn);
         }
-        warp_totals16(v, wtc[kk]);
-    }
-    const int nmine = kk;
-    __syncthreads();
-    for (int t = threadIdx.x; t < nmine * kSubTiles; t += kSampThreads) {
-        const int k2 = t / kSubTiles, s2 = t - k2 * kSubTiles;
-        double st = 0.0;
+        cp_async_commit();
+    };
+    if (nbat > 0) stage_batch(0);
+    for (int bi = 0; bi < nbat; ++bi) {
+        if (bi + 1 < nbat) {
+            stage_batch(bi + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float* buf = stage + (size_t)(bi & 1) * PB * 2 * kChunk;
+        const int nk = min(PB, nmine - bi * PB);
+        for (int k = 0; k < nk; ++k) {
+            const int c = rank + (bi * PB + k) * CL;
+            const float* sl = buf + (size_t)k * 2 * kChunk;
+            const float* sq = sl + kChunk;
+            const int x0 = c * kChunk + (int)threadIdx.x;
+            float v[kSubTiles];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) st = st + (double)wtc[k2][s2][k];
-        sstc[k2][s2] = st;
-    }
-    __syncthreads();
-    for (int k2 = threadIdx.x; k2 < nmine; k2 += kSampThreads) {
-        double acc = 0.0;
+            for (int s2 = 0; s2 < kSubTiles; ++s2) {
+                const int o = s2 * kSampThreads + (int)threadIdx.x;
+                const bool in = x0 + s2 * kSampThreads < p.V_local;
+                const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
+                v[s2] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
+            }
+            warp_totals16(v, wtc[k]);
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nk * kSubTiles; t += kSampThreads) {
+            const int k2 = t / kSubTiles, s2 = t - k2 * kSubTiles;
+            double st = 0.0;
 #pragma unroll
-        for (int s2 = 0; s2 < kSubTiles; ++s2) acc = acc + sstc[k2][s2];
-        cml[rank + k2 * CL] = acc;
+            for (int k = 0; k < 8; ++k) st = st + (double)wtc[k2][s2][k];
+            sstc[k2][s2] = st;
+        }
+        __syncthreads();
+        for (int k2 = threadIdx.x; k2 < nk; k2 += kSampThreads) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s2 = 0; s2 < kSubTiles; ++s2) acc = acc + sstc[k2][s2];
+            cml[rank + (bi * PB + k2) * CL] = acc;
+        }
+        __syncthreads();   // wtc / sstc / this buffer are reused two batches on
     }
     // (4) every chunk mass from the CTA that owns it (distributed shared memory); the
     //     second cluster barrier keeps each CTA's cml alive until all have read it
@@ -651,18 +667,9 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     if (c % CL != rank) return;
     const double tp = sh_tp;
     float w[kSubTiles], v[kSubTiles];
-    {   // the located chunk's weights again, from this CTA's staged copy (same expression)
-        const float* sl = stage + (size_t)(c / CL) * 2 * kChunk;
-        const float* sq = sl + kChunk;
-        const int x0 = c * kChunk + (int)threadIdx.x;
+    // the located chunk's weights again (k_locate's chunk_weight: same expression)
 #pragma unroll
-        for (int s2 = 0; s2 < kSubTiles; ++s2) {
-            const int o = s2 * kSampThreads + (int)threadIdx.x;
-            const bool in = x0 + s2 * kSampThreads < p.V_local;
-            const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
-            v[s2] = w[s2] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
-        }
-    }
+    for (int s2 = 0; s2 < kSubTiles; ++s2) v[s2] = w[s2] = chunk_weight(p, lrow, c, s2, lsef, corr, resid, qrow);
     warp_totals16(v, wt);
     __syncthreads();
     if (threadIdx.x < kSubTiles) {
