@@ -294,11 +294,13 @@ def test_staged_small(B, g, V, d):
 
 
 @pytest.mark.parametrize("B,g", [(16, 3), (32, 3), (64, 3), (256, 0), (50, "mixed:5"), (96, 2), (33, 3),
-                                 (128, 3), (170, 5)])
+                                 (128, 3), (170, 5), (12, 3), (10, "mixed:5"), (7, 4)])
 def test_staged_full_size(B, g):
     """C3 points at the Qwen shape from the memory-bound band through the ridge
     to the tensor-bound band (one k_lmhead pass: CTA or CTA-pair tiles, 1-6
-    token chunks, ragged last chunk), every request vs the oracle."""
+    token chunks, ragged last chunk; B <= 12: k_sample_small with clusters of
+    8 (two staged chunk batches per CTA) or 16 CTAs), every request vs the
+    oracle."""
     b = make_batch(B, g, V=QV, d=QD, seed=B + 17, device=DEV, W=w_full())
     acc, nxt, dd, v = run(b)
     assert v.plan(b.gamma)[0] == (NJ_PATH_FUSED if b.N <= 24 else NJ_PATH_STAGED)   # kFusedAutoMaxN
