@@ -2,7 +2,8 @@
 (M=128, N=n) and CTA pair (cta_group::2, M=256, each SM 128 x n), operands
 resident in shared memory.  Modes: 0 commit at the end, 2 commit per group (the
 ring's), 1 commit + wait per group, 4 / 5 the whole warp convergent with elect-predicated
-issue (per MMA / four MMAs under one elect), commit per group.  Tensor floor per SM: 4 * 128 * n / 256 cycles."""
+issue (per MMA / four MMAs under one elect), commit per group; pair mode 3 rotates the
+operands over 4 shared-memory stages (as a ring does).  Tensor floor per SM: 4 * 128 * n / 256 cycles."""
 import sys
 
 import torch
@@ -13,7 +14,7 @@ from scripts.probes import _probe  # noqa: E402
 dev = torch.device("cuda:0")
 out = torch.zeros(148, dtype=torch.int64, device=dev)
 for cg, fn, ns, modes in ((1, _probe.mma_probe, (32, 64, 128, 192, 240, 256), (0, 2, 1, 4, 5, 6, 7)),
-                          (2, _probe.mma_probe_cg2, (64, 128, 192, 224, 256), (0, 2, 1))):
+                          (2, _probe.mma_probe_cg2, (64, 128, 176, 192, 208, 224, 240, 256), (0, 2, 1, 3))):
     for mode in modes:
         for n in ns:
             out.zero_()

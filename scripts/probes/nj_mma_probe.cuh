@@ -82,12 +82,12 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe(int n, int iters, int mode
 // commit is multicast to both CTAs.  Reports the leader's cycles per group.
 __global__ void __launch_bounds__(128, 1) k_mma_probe_cg2(int n, int iters, int mode, long long* out) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sA = smem;                       // 16 KB
+    uint8_t* sA = smem;                       // 16 KB (mode 3: 4 stages of A 16 KB | B 16 KB)
     uint8_t* sB = smem + kTileBytesA;         // (n / 2) x 128 B
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sB + 128 * 128);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 4 * (kTileBytesA + 128 * 128));
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
     const bool leader = cluster_ctarank() == 0;
-    for (int i = threadIdx.x; i < (kTileBytesA + 128 * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+    for (int i = threadIdx.x; i < 4 * (kTileBytesA + 128 * 128) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
     if (threadIdx.x == 0) { mbar_init(bar, 1); fence_barrier_init(); }
     if (warp_id() == 0) tmem_alloc_cg2(slot, 256);
     fence_proxy_async();
@@ -97,10 +97,12 @@ __global__ void __launch_bounds__(128, 1) k_mma_probe_cg2(int n, int iters, int 
     const uint32_t tbase = *slot;
     if (leader && threadIdx.x == 32) {
         const uint32_t idesc = idesc_bf16_f32(256, (uint32_t)n);
-        const uint64_t ad = sdesc_sw128(sA), bd = sdesc_sw128(sB);
         uint32_t ph = 0;
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
+            const int stg = mode == 3 ? (it & 3) : 0;
+            const uint64_t ad = sdesc_sw128(sA + stg * (kTileBytesA + 128 * 128));
+            const uint64_t bd = sdesc_sw128(sB + stg * (kTileBytesA + 128 * 128));
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma_bf16_cg2(tbase, ad + 2 * k, bd + 2 * k, idesc, (it | k) != 0);
             if (mode == 1) {

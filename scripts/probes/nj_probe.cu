@@ -118,8 +118,8 @@ int njp_mma_probe(void* stream, int32_t n, int32_t iters, int32_t mode, int64_t*
 }
 
 int njp_mma_probe_cg2(void* stream, int32_t n, int32_t iters, int32_t mode, int64_t* cycles_out) {
-    if (!cycles_out || n < 32 || n > 256 || n % 32 || iters < 1) return 1;
-    const size_t smem = kTileBytesA + 128 * 128 + 64;
+    if (!cycles_out || n < 32 || n > 256 || n % 16 || iters < 1) return 1;
+    const size_t smem = 4 * (kTileBytesA + 128 * 128) + 64;
     if (cudaFuncSetAttribute(k_mma_probe_cg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return 3;
     cudaLaunchConfig_t cfg = {};
