@@ -105,7 +105,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -148,7 +148,8 @@ Knobs read_knobs() {
     k.small_cl16 = env_int("NJ_SMALL_CL16", 1);
     k.small_pf = env_int("NJ_SMALL_PF", 0);          // measured slower (C2 204.7 vs 200.5 us)
     k.lm_sleep = env_int("NJ_LM_SLEEP", 0);
-    k.small_bmax = env_int("NJ_SMALL_BMAX", 12);   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
+    k.small_bmax = env_int("NJ_SMALL_BMAX", 12);
+    k.inline_lse = env_int("NJ_INLINE_LSE", kInlineLseRows);   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
@@ -1315,7 +1316,7 @@ nj_status nj_plan(nj_ctx* c, const int32_t* gamma, int32_t B, int32_t* path_out,
     }
     if (pl.path == NJ_PATH_FUSED) n = 1;
     else if (pl.path == NJ_PATH_STAGED)   // GEMM, [row lse,] accept, mass, locate | GEMM, k_sample_small
-        n = small_sampler_ok(c, pl) ? 2 : pl.N > kInlineLseRows ? 5 : 4;
+        n = small_sampler_ok(c, pl) ? 2 : pl.N > c->kn.inline_lse ? 5 : 4;
     else n = (pl.G > 0 ? 2 * ((pl.G + kMaxStatRows - 1) / kMaxStatRows) + 1 : 0) + 4;   // gather+KA, row lse, KB, KC, KD1, KD2
     n += 1;   // k_fb (every call; exits at once on an empty queue)
     if (path_out) *path_out = pl.path;
@@ -1450,7 +1451,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             goto fallback;
         }
         // small batches: k_accept merges its rows' statistics itself (one launch fewer)
-        if (pl.N > kInlineLseRows) {
+        if (pl.N > c->kn.inline_lse) {
             k_lse_rows<<<(pl.N + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.N, c->row_lse);
             NJ_LAUNCHED(c, "k_lse_rows", st);
             ap.pre_lse = c->row_lse;
