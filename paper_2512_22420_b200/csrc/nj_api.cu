@@ -105,7 +105,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -149,7 +149,8 @@ Knobs read_knobs() {
     k.small_pf = env_int("NJ_SMALL_PF", 0);          // measured slower (C2 204.7 vs 200.5 us)
     k.lm_sleep = env_int("NJ_LM_SLEEP", 0);
     k.small_bmax = env_int("NJ_SMALL_BMAX", 12);
-    k.inline_lse = env_int("NJ_INLINE_LSE", kInlineLseRows);   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
+    k.inline_lse = env_int("NJ_INLINE_LSE", kInlineLseRows);
+    k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
     return k;
@@ -1429,6 +1430,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             mp.dbg_lse = dbg ? dbg->lse : nullptr;
             mp.certify = certify; mp.eps_draw = c->eps_draw;
             mp.small_pb = small_sampler_pb(c, pl.B);
+            mp.pdl_trigger = c->kn.small_trig;
             mp.pf_rows = c->kn.small_pf && !c->q_remote && (ldq & 3) == 0 && (c->V_local & 3) == 0 &&
                          (reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0;
             cudaLaunchConfig_t cfg = {};

@@ -236,6 +236,7 @@ struct MassParams {
     int32_t part2_by_row;  // 1: part2 row of request b is s_row[b] (vocab-sharded staged step)
     int32_t pf_rows;       // k_sample_small: L2-prefetch the candidate rows while testing
     int32_t small_pb;      // k_sample_small: chunks per staged batch
+    int32_t pdl_trigger;   // k_sample_small: trigger the fallback kernel's launch at the start
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -487,6 +488,9 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     // launched with programmatic dependent launch: the CTAs start on SMs the GEMM's
     // finished CTAs free, then wait here for the whole GEMM grid and its writes
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // let the fp64 fallback kernel (launched next with programmatic serialization) be
+    // scheduled now: it waits in its own griddepcontrol.wait for this grid to finish
+    if (p.pdl_trigger && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int b = (int)cluster_id_x();
     const int rank = (int)cluster_ctarank();
     const int CL = (int)cluster_nctarank();   // 8 or 16 CTAs per request
