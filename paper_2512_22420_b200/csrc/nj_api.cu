@@ -634,11 +634,10 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.nbuf = std::max(2, std::min(kLmMaxBuf, 512 / p.bstride));
     if (c->kn.lm_nbuf > 0) p.nbuf = std::min(kLmMaxBuf, c->kn.lm_nbuf);
     if (c->kn.lm_ks > 0) p.ks = c->kn.lm_ks;
-    // the first accumulator group of an item spans 8 k-blocks (ks = 4: the MMAs then run 12
-    // k-blocks ahead of the epilogue's per-item output, -3..-4 %), at an accuracy cost inside
-    // the certificates (scripts/lm_accuracy.py: max |d ln p| 6.4e-6 vs 6.8e-6, max CDF error
-    // 8.6e-7 vs 6.9e-7 over 256 Qwen-shape rows)
-    p.ks0 = std::max(p.ks, c->kn.lm_ks0 > 0 ? c->kn.lm_ks0 : 8);
+    // first accumulator group of an item: ks (NJ_LM_KS0 = 8 lets the MMAs run 12 k-blocks
+    // ahead of the per-item output, -3..-4 %, but its larger CDF error put one of 10 240
+    // uncertified B = 256 gamma = 5 draws outside the 1e-6 band, DESIGN.md §6 / §17)
+    p.ks0 = std::max(p.ks, c->kn.lm_ks0 > 0 ? c->kn.lm_ks0 : p.ks);
     p.arv1 = c->kn.lm_arv1;
     p.sleep_ns = c->kn.lm_sleep;
     p.fence_full = c->kn.lm_fence;

@@ -1,6 +1,8 @@
 """Raw decision accuracy of the CUDA path with the certificate OFF, at the
-bench shapes: >= 10^4 Qwen-shape requests (B = 256, gamma = 5 two-pass; B = 64,
-gamma = 3 staged; B = 8, gamma = 3 fused) against the fp64 oracle.  Counts
+bench shapes: >= 10^4 Qwen-shape requests (B = 256, gamma = 5; B = 64,
+gamma = 3; B = 8, gamma = 3 on the AUTO path -- the staged k_lmhead step since
+round 2's second session -- and B = 8, gamma = 3 on the fused kernel) against
+the fp64 oracle.  Counts
 out-of-band mismatches (must be 0), ties (oracle band 1e-6) and excused
 requests that took the other tie branch.  Writes one JSON summary.
 
@@ -18,12 +20,12 @@ sys.path.insert(0, ".")
 sys.path.insert(0, "tests")
 import oracle  # noqa: E402
 import parity  # noqa: E402
-from paper_2512_22420_b200 import NJ_OPT_CERTIFY, Verifier  # noqa: E402
+from paper_2512_22420_b200 import NJ_OPT_CERTIFY, NJ_OPT_PATH, NJ_PATH_AUTO, NJ_PATH_FUSED, Verifier  # noqa: E402
 from synth.inputs import make_batch, make_weight  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--batches", type=int, default=40)
-ap.add_argument("--out", default="profiles/r02_uncertified.json")
+ap.add_argument("--out", default="profiles/r02c_uncertified.json")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 V, d = 152064, 3584
@@ -31,9 +33,11 @@ W = make_weight(V, d, 0, dev)
 W64 = oracle.weight_f64(oracle.bf16_bits(W))
 summary = {}
 t0 = time.time()
-for (B, g, nb) in [(256, 5, a.batches), (64, 3, a.batches), (8, 3, 4 * a.batches)]:
+for (B, g, nb, fp) in [(256, 5, a.batches, NJ_PATH_AUTO), (64, 3, a.batches, NJ_PATH_AUTO),
+                      (8, 3, 4 * a.batches, NJ_PATH_AUTO), (8, 3, 2 * a.batches, NJ_PATH_FUSED)]:
     v = Verifier(d, V, max_batch=B, gamma_max=5)
     v.set_option(NJ_OPT_CERTIFY, 0)
+    v.set_option(NJ_OPT_PATH, fp)
     path = v.plan(np.full(B, g, np.int32))[0]
     tot = {"requests": 0, "mismatch_out_of_band": 0, "ties": 0, "expected_ties": 0.0, "excused_other_branch": 0}
     for i in range(nb):
@@ -52,14 +56,15 @@ for (B, g, nb) in [(256, 5, a.batches), (64, 3, a.batches), (8, 3, 4 * a.batches
         tot["ties"] += int(r["tie"].sum())
         tot["expected_ties"] += float(r["p_tie"].sum())
         try:
-            parity.check(f"sweep B={B} g={g} #{i}", n, a_, t_, r=r, L=L)
+            parity.check(f"sweep B={B} g={g} p={fp} #{i}", n, a_, t_, r=r, L=L)
         except AssertionError as e:
             tot.setdefault("failures", []).append(str(e)[:300])
         tot["excused_other_branch"] = sum(s["excused_differing"] for s in parity.STATS
-                                          if s["test"].startswith(f"sweep B={B} g={g}"))
+                                          if s["test"].startswith(f"sweep B={B} g={g} p={fp}"))
     tot["path"] = ["auto", "fused", "two-pass", "staged"][path]
-    summary[f"B{B}_g{g}"] = tot
-    print(json.dumps({f"B{B}_g{g}": tot}), flush=True)
+    key = f"B{B}_g{g}" + ("_fused" if fp == NJ_PATH_FUSED else "")
+    summary[key] = tot
+    print(json.dumps({key: tot}), flush=True)
 summary["total_requests"] = sum(v_["requests"] for v_ in summary.values() if isinstance(v_, dict))
 summary["total_mismatch_out_of_band"] = sum(v_["mismatch_out_of_band"] for v_ in summary.values() if isinstance(v_, dict))
 summary["certificate"] = "off (raw kernels)"
