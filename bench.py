@@ -71,6 +71,17 @@ def load_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
 
 
+def tensor_roof(name, flops, kern_ms, tf_burst, tf_sust):
+    """Roofline entry of a tensor-bound GEMM.  The kernel is timed inside the repeated
+    step loop (K back-to-back steps, the SM clock under sw_power_cap: see `clocks`), so
+    its peak is MEASURED_PEAKS' sustained bf16 figure (cuBLAS back to back for 4 s);
+    the burst figure (a kernel timed alone) is kept beside it."""
+    a = flops / (kern_ms / 1e3) / 1e12
+    return {"kernel": name, "bound": "tensor", "achieved": a, "peak": tf_sust, "unit": "TFLOP/s",
+            "frac": a / tf_sust, "peak_kind": "sustained (kernel timed inside the back-to-back step loop)",
+            "peak_burst": tf_burst, "frac_burst": a / tf_burst, "algorithmic_flops_per_launch": flops}
+
+
 class ClockSampler:
     """NVML SM clock + throttle reasons sampled during the timed region."""
     NAMES = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
@@ -424,10 +435,8 @@ def bench_nj(args, ws, rank, local):
             roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "algorithmic_bytes_per_launch": byts, "rows": R}
         else:
-            flops = 2.0 * R * V_Q * D_Q
-            achieved = flops / (kern_ms / 1e3) / 1e12
-            roof = {"kernel": name, "bound": "tensor", "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
-                    "frac": achieved / tf_burst, "algorithmic_flops_per_launch": flops, "rows": R}
+            roof = tensor_roof(name, 2.0 * R * V_Q * D_Q, kern_ms, tf_burst, tf_sust)
+            roof["rows"] = R
     roof["peak_source"] = peak_src
     roof["kernel_ms_avg"] = kern_ms
     # share of the step in the SAME (eager, event-bracketed) pass the kernel was timed in
@@ -742,16 +751,14 @@ def bench_c5(args, ws, rank, local):
             print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
     t_max = njdist.max_over_ranks(ms, dev)
     toks = int((acc + 1).sum().item())
-    hbm, tf_burst, _, peak_src = load_peaks()
+    hbm, tf_burst, tf_sust, peak_src = load_peaks()
     kern_ms = kms / max(kn, 1)
     staged = v.plan(b.gamma)[0] == NJ_PATH_STAGED   # the staged sharded step: k_lmhead over all N rows
     flops = 2.0 * (b.N if staged else b.G) * (ve - vb) * D_Q
-    roof = {"kernel": ("k_lmhead<logits,stats,capture> (all N rows, this rank's shard)" if staged else
-                       "k_gemm_big<stats> (K-A, draft rows, this rank's shard)"), "bound": "tensor",
-            "achieved": flops / (kern_ms / 1e3) / 1e12, "peak": tf_burst, "unit": "TFLOP/s",
-            "frac": flops / (kern_ms / 1e3) / 1e12 / tf_burst, "algorithmic_flops_per_launch": flops,
-            "peak_source": peak_src, "kernel_ms_avg": kern_ms, "kernel_share_of_step": kms / ms_eager,
-            "traffic": None}
+    roof = tensor_roof("k_lmhead<logits,stats,capture> (all N rows, this rank's shard)" if staged else
+                       "k_gemm_big<stats> (K-A, draft rows, this rank's shard)", flops, kern_ms, tf_burst, tf_sust)
+    roof.update({"peak_source": peak_src, "kernel_ms_avg": kern_ms, "kernel_share_of_step": kms / ms_eager,
+                 "traffic": None})
     # end to end through nj_verify_host (pinned host inputs, copies inside the timed region)
     pin = lambda t: t.cpu().pin_memory()
     hh, th, qh, uh = pin(b.hidden), pin(b.draft_tokens), pin(b.draft_probs), pin(b.uniforms)
@@ -1023,7 +1030,7 @@ def bench_greedy(args, ws, rank, local):
         except Exception as e:
             print(f"[bench] CUDA graph timing skipped: {e}", file=sys.stderr)
     t_max = njdist.max_over_ranks(ms, dev) if ws > 1 else ms
-    hbm, tf_burst, _, peak_src = load_peaks()
+    hbm, tf_burst, tf_sust, peak_src = load_peaks()
     kern_ms = kms / max(kn, 1)
     R = b.N / nblk
     ridge = tf_burst * 1e12 / (hbm * 1e9)
@@ -1033,10 +1040,7 @@ def bench_greedy(args, ws, rank, local):
                 "peak": hbm, "unit": "GB/s", "frac": byts / (kern_ms / 1e3) / 1e9 / hbm,
                 "algorithmic_bytes_per_launch": byts}
     else:
-        fl = 2.0 * R * V_Q * D_Q
-        roof = {"kernel": "k_lmhead<argmax> (all rows)", "bound": "tensor",
-                "achieved": fl / (kern_ms / 1e3) / 1e12, "peak": tf_burst, "unit": "TFLOP/s",
-                "frac": fl / (kern_ms / 1e3) / 1e12 / tf_burst, "algorithmic_flops_per_launch": fl}
+        roof = tensor_roof("k_lmhead<argmax> (all rows)", 2.0 * R * V_Q * D_Q, kern_ms, tf_burst, tf_sust)
     roof.update({"peak_source": peak_src, "kernel_ms_avg": kern_ms,
                  "kernel_share_of_step": kms / ms_eager if ms_eager > 0 else None, "traffic": None, "rows": R})
     # end to end: pinned host hidden + draft tokens in, accept_len / next_token out
@@ -1108,7 +1112,7 @@ def bench_sweep(args, ws, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     W = make_weight(V_Q, D_Q, args.seed, dev)
-    hbm, tf_burst, _, _ = load_peaks()
+    hbm, tf_burst, tf_sust, _ = load_peaks()
     Bs = [int(x) for x in args.sweep_B.split(",")]
     Gs = [x if x.startswith("mixed") else int(x) for x in args.sweep_gamma.split(",")]
     for g in Gs:
@@ -1139,10 +1143,13 @@ def bench_sweep(args, ws, rank, local):
             toks = int((acc + 1).sum().item())
             N = b.N
             t_star = max(2.0 * N * V_Q * D_Q / (tf_burst * 1e12), (2.0 * V_Q * D_Q + 2 * N * D_Q) / (hbm * 1e9))
+            t_sus = max(2.0 * N * V_Q * D_Q / (tf_sust * 1e12), (2.0 * V_Q * D_Q + 2 * N * D_Q) / (hbm * 1e9))
             emit({"config": f"B{B}_g{g}", "B": B, "gamma": g, "N": N, "path": PATH_NAMES[path],
                               "us_per_step": ms * 1e3, "positions_per_s": N / (ms / 1e3),
                               "accepted_tokens_per_s": toks / (ms / 1e3), "roofline_us": t_star * 1e6,
-                              "frac_of_roofline": t_star / (ms / 1e3), "dominant_kernel_us": kms / max(kn, 1) * 1e3,
+                              "frac_of_roofline": t_star / (ms / 1e3), "roofline_us_sustained": t_sus * 1e6,
+                              "frac_of_roofline_sustained": t_sus / (ms / 1e3),
+                              "dominant_kernel_us": kms / max(kn, 1) * 1e3,
                               "launches": launches})
             del v
 

@@ -673,9 +673,12 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     size_t tail = (p.tma_out ? (size_t)kLmEpiWarps * p.ost_n * 2048 : 0) + (STATE ? 4 * nloc * 8 : 0) + (CAP ? nloc * 8 : 0);
     tail = align_up(tail, 8) + (2 * 8 + 2 * kLmMaxBuf) * 8 + 8;
     const size_t kb_bytes = (size_t)p.hbox * 128 + (size_t)p.wbox * 128;
-    // CTA pair, one token chunk (R <= 256): 2-k-block ring stages (W streamed once; -7 % at R = 256);
-    // several: 1-k-block stages, the MMA warp taking two per operand wait (equal or better there)
-    p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : (pl.nchunks == 1 && CG == 2 ? 2 : 1);
+    // CTA pairs: 2-k-block ring stages.  Every ring stage costs one tcgen05.commit, and
+    // each commit stalls the tensor pipe: with no loads at all, 1-k-block stages run
+    // 1.26x slower than no ring, 2-k-block stages as fast (R = 1536, interleaved A/B:
+    // full kernel -7 % at R = 1536, -4 % at 768, -7 % at R = 256).
+    // Single CTAs: 1-k-block stages (a 2-k-block stage of 92 KB leaves 2 stages; equal)
+    p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : (CG == 2 ? 2 : 1);
     while (p.gk > 1 && (kSmemLimit - tail - 1024) / ((size_t)p.gk * kb_bytes) < 2) --p.gk;
     const size_t stage = (size_t)p.gk * kb_bytes;
     int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
