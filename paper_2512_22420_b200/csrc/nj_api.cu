@@ -79,6 +79,7 @@ constexpr int kStagedMaxN = kBigMaxRowG;   // staged path on k_gemm_big (NJ_LM=0
 constexpr int kFusedAutoMaxN = 24;          // AUTO takes the fused kernel up to this many rows
 constexpr int kInlineLseRows = 64;          // staged path: N up to which k_accept merges row statistics inline
 constexpr int kStagedMaxRows = 2048;        // staged path on k_lmhead: rows of one GEMM pass (logits_st rows)
+constexpr int kPhaseTsN = 20 * 1024;     // debug timeline entries (NJ_PHASE_TS; k_lmhead uses [16K, 18K) for accumulator waits)
 
 inline int round16(int x) { return (x + 15) & ~15; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -456,7 +457,7 @@ nj_status launch_fused(nj_ctx* c, cudaStream_t st, const Plan& pl, const CUtenso
     fp.eps_acc = (kspan == 1 ? c->eps_acc_fused : kspan == 2 ? 2.0f * c->eps_acc_fused : c->eps_acc) *
                  (float)std::max(1.0, c->inv_t);
     if (c->kn.phase_ts) {
-        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
+        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, kPhaseTsN * sizeof(unsigned long long)));
         fp.phase_ts = c->phase_ts;
     }
     const size_t smem = (size_t)S * stage2 + fused_tail(NPAD, S);
@@ -556,7 +557,7 @@ nj_status launch_lmhead(nj_ctx* c, cudaStream_t st, const uint16_t* h, int R, co
     gp.sleep_ns = c->kn.sleep_ns;
     gp.ts = nullptr;
     if (c->kn.phase_ts) {
-        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
+        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, kPhaseTsN * sizeof(unsigned long long)));
         gp.ts = c->phase_ts;
     }
     CUtensorMap tmH;
@@ -645,8 +646,8 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.dbg = c->kn.lm_dbg;
     p.ts = nullptr;
     if (c->kn.phase_ts) {
-        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, 16 * 1024 * sizeof(unsigned long long)));
-        NJ_CUDA(c, cudaMemsetAsync(c->phase_ts, 0, 16 * 1024 * sizeof(unsigned long long), st));
+        if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, kPhaseTsN * sizeof(unsigned long long)));
+        NJ_CUDA(c, cudaMemsetAsync(c->phase_ts, 0, kPhaseTsN * sizeof(unsigned long long), st));
         p.ts = c->phase_ts;
     }
     // one chunk: W is streamed once (evict_first); several: the other chunks of a
@@ -1278,7 +1279,7 @@ nj_status nj_set_temperature(nj_ctx* c, double temperature) {
 
 nj_status nj_debug_phase_times(nj_ctx* c, unsigned long long* host_out, int32_t n) {
     if (!c || !c->phase_ts) return NJ_EINVAL;
-    NJ_CUDA(c, cudaMemcpy(host_out, c->phase_ts, sizeof(unsigned long long) * std::min(n, 16 * 1024), cudaMemcpyDeviceToHost));
+    NJ_CUDA(c, cudaMemcpy(host_out, c->phase_ts, sizeof(unsigned long long) * std::min(n, kPhaseTsN), cudaMemcpyDeviceToHost));
     return NJ_OK;
 }
 

@@ -283,7 +283,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
             // consumes p.mb ring stages per iteration (one operand wait + fence per mb x GK
             // k-blocks: the issuing warp is paced by the tensor pipe, so its per-iteration
             // overhead is exposed)
-            int s = 0, abuf = 0;
+            int s = 0, abuf = 0, gall = 0;
             uint32_t ph = 0, aph = 0;
             const int MB = p.mb;
             for (int it = 0; it < nitems; ++it) {
@@ -315,7 +315,11 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                         uint8_t* st = ring + (size_t)(s % SM_) * stageBytes;
                         for (int g = 0; g < ng; ++g) {
                             if (kin == 0) {
+                                const int gw = gall++;   // accumulator groups issued so far (timeline index)
+                                const bool tsa = p.ts != nullptr && blockIdx.x == 0 && lane == 0 && gw < 1000;
+                                if (tsa) p.ts[16384 + 2 * gw] = globaltimer();
                                 mbar_wait_w(&aempty[abuf], aph ^ 1);
+                                if (tsa) p.ts[16384 + 2 * gw + 1] = globaltimer();
                                 tc_fence_after();
                                 dt = tbase + (uint32_t)(abuf * p.bstride);
                             }

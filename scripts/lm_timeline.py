@@ -31,8 +31,8 @@ for dbg in sys.argv[2].split(","):
     for _ in range(3):
         v.lmhead_logits(h, W, rows, out)
     torch.cuda.synchronize()
-    ts = np.zeros(16 * 1024, np.uint64)
-    lib.nj_debug_phase_times(v._h, ts.ctypes.data, 16 * 1024)
+    ts = np.zeros(20 * 1024, np.uint64)
+    lib.nj_debug_phase_times(v._h, ts.ctypes.data, 20 * 1024)
     t = ts.astype(np.int64)
     P = t[:4000].reshape(2000, 2)
     M = t[4096:4096 + 3 * 1300].reshape(1300, 3)
@@ -69,6 +69,18 @@ for dbg in sys.argv[2].split(","):
         print(f"   epilogue warp0 groups {ng}: afull wait median {np.median(wait):.0f} ns mean {wait.mean():.0f}; "
               f"drain (wait end -> arrive) median {np.median(drain):.0f} ns mean {drain.mean():.0f}; group period "
               f"{np.median(np.diff(Gs[:, 1])):.0f} ns")
+    AE = t[16384:16384 + 2000].reshape(1000, 2)
+    na = int((AE[:, 0] > 0).sum())
+    if na > 2:
+        AE = AE[:na]
+        aw = AE[:, 1] - AE[:, 0]
+        ngi = int(os.environ.get("NGROUPS", "14"))
+        first = aw[0::ngi]
+        rest = np.delete(aw, np.s_[0::ngi])
+        span_a = AE[-1, 1] - AE[0, 0]
+        print(f"   MMA aempty waits {na}: total {aw.sum() / span_a * 100:.1f} % of span; first group of an item "
+              f"median {np.median(first):.0f} ns mean {first.mean():.0f}; other groups median {np.median(rest):.0f} "
+              f"mean {rest.mean():.0f} ns; sum first {first.sum() / span_a * 100:.1f} %, rest {rest.sum() / span_a * 100:.1f} %")
     # first 12 stages raw (relative ns)
     print("   MMA  ", [(int(a - t0), int(b - t0), int(c - t0)) for a, b, c in M[20:28]])
     print("   prod ", [(int(a - t0), int(b - t0)) for a, b in P[20:28]])
