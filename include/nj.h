@@ -218,8 +218,8 @@ nj_status nj_plan(nj_ctx* ctx, const int32_t* gamma_per_req, int32_t B,
  * fp32, row-major with pitch ld_out (>= V_local).  rows: device int32
  * [n_rows], 1 <= n_rows <= min(max_batch·gamma_max, 1536).  ks: k-blocks (64
  * deep) per TMEM accumulator restart; 0 = the sample-row GEMM's
- * default (4; k_lmhead's first group of an item spans max(ks, 8)), 8 = the
- * two-pass draft-row GEMM's.  Test-only (element-wise
+ * default (4, every group of k_lmhead included), 8 = the two-pass draft-row
+ * GEMM's.  Test-only (element-wise
  * parity of the GEMM against the fp64 oracle). */
 nj_status nj_lmhead_logits(nj_ctx* ctx, void* stream,
                            const uint16_t* hidden, const uint16_t* W_lm,

@@ -221,6 +221,7 @@ struct nj_ctx {
     unsigned long long* amax = nullptr;   // nj_verify_greedy: per-row argmax keys [Nmax]
     int mass_nst = 2;                 // k_mass cp.async ring stages (NJ_MASS_NST: 2..4; 2 = 3 CTAs / SM)
     int mass_occ = 1;                 // resident k_mass CTAs per SM at mass_nst
+    int small_maxcl[17] = {};         // k_sample_small: co-resident clusters of 2 / 4 / 8 / 16 CTAs (0: unknown)
     int32_t* scratch_i = nullptr;  // [MB]
     int32_t* s_row = nullptr;      // [MB] staged path: sample row of each request
     int32_t* g2row = nullptr;      // [Gmax] staged sharded step: packed row of each draft row
@@ -364,16 +365,20 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
 // one cluster of kSmallCl CTAs per request fits the SMs
 // cluster size: 16 CTAs per request for B <= 8 (one cluster per GPC at a time), 8 up to
 // B = 12 (16 clusters of 8 did not all fit at once), then 4 / 2 while B * cluster <= SMs
+// -- but only a size of which all B clusters are co-resident on this device (the
+// driver's cudaOccupancyMaxActiveClusters at nj_create): the GPCs' SM counts differ
+// between B200 parts, and a request whose cluster waits for a second wave doubles the
+// sampler's time (measured 20 -> 34 us at B = 8 on a box where 16-CTA clusters did
+// not all fit); a smaller cluster then takes over in one wave
 int small_sampler_cl(const nj_ctx* c, int B) {
-    if (B <= 8 && c->kn.small_cl16) return 16;
-    if (B <= 12) return kSmallCl;
-    return B * 4 <= c->num_sms ? 4 : 2;
+    int cl = (B <= 8 && c->kn.small_cl16) ? 16 : B <= 12 ? kSmallCl : (B * 4 <= c->num_sms ? 4 : 2);
+    while (cl > 2 && c->small_maxcl[cl] > 0 && c->small_maxcl[cl] < B) cl >>= 1;
+    return cl;
 }
-int small_sampler_pb(const nj_ctx* c, int B) {   // chunks per staged batch (two buffers)
-    const int cl = small_sampler_cl(c, B);
-    const int nmine = (c->nchunks + cl - 1) / cl;
-    return std::max(1, std::min(3, nmine));
+int small_pb_for(int nchunks, int cl) {   // chunks per staged batch (two buffers)
+    return std::max(1, std::min(3, (nchunks + cl - 1) / cl));
 }
+int small_sampler_pb(const nj_ctx* c, int B) { return small_pb_for(c->nchunks, small_sampler_cl(c, B)); }
 size_t small_sampler_smem(const nj_ctx* c, int B) {   // two batch buffers of logits + q chunks
     return (size_t)2 * small_sampler_pb(c, B) * 2 * kChunk * sizeof(float);
 }
@@ -1225,6 +1230,25 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 1>);
     e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int cl = 2; cl <= 16 && !e; cl <<= 1) {
+        cudaLaunchConfig_t oc = {};
+        oc.gridDim = dim3(cl);
+        oc.blockDim = dim3(kSampThreads);
+        oc.dynamicSmemBytes = (size_t)2 * small_pb_for(c->nchunks, cl) * 2 * kChunk * sizeof(float);
+        cudaLaunchAttribute oa[1];
+        oa[0].id = cudaLaunchAttributeClusterDimension;
+        oa[0].val.clusterDim.x = cl;
+        oa[0].val.clusterDim.y = 1;
+        oa[0].val.clusterDim.z = 1;
+        oc.attrs = oa;
+        oc.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_sample_small, &oc) == cudaSuccess) c->small_maxcl[cl] = n;
+        else (void)cudaGetLastError();   // unknown: keep the measured default size
+    }
+    if (getenv("NJ_SMALL_INFO"))
+        fprintf(stderr, "[nj] k_sample_small co-resident clusters: 2:%d 4:%d 8:%d 16:%d\n", c->small_maxcl[2],
+                c->small_maxcl[4], c->small_maxcl[8], c->small_maxcl[16]);
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 2>);
     if (const char* ev = getenv("NJ_MASS_NST")) c->mass_nst = std::min(4, std::max(2, atoi(ev)));
     e = e ? e : cudaFuncSetAttribute(k_mass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(2, c->cfg.max_batch));
