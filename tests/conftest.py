@@ -43,13 +43,17 @@ def pytest_terminal_summary(terminalreporter, exitstatus, config):
     tr = terminalreporter
     tr.write_sep("-", "parity tie counts (oracle band 1e-6)")
     tot = {"B": 0, "ties": 0, "excused": 0, "excused_differing": 0, "fallback": 0}
-    exp = 0.0
+    exp, n_unknown = 0.0, 0
     for s in stats:
         tr.write_line(f"{s['test']:<60} B={s['B']:<5} N={s['N']:<5} ties={s['ties']} (acc {s['accept_ties']}, "
                       f"draw {s['draw_ties']}) expected={s['expected_ties']} excused={s['excused']} "
                       f"other-branch={s['excused_differing']} fallback={s['fallback']}")
         for k in tot:
             tot[k] += s[k]
-        exp += s["expected_ties"]
-    tr.write_line(f"TOTAL requests={tot['B']} ties={tot['ties']} expected={exp:.2f} excused={tot['excused']} "
+        if s["expected_ties"] == s["expected_ties"]:   # the stage-isolated tests carry no tie probability (NaN)
+            exp += s["expected_ties"]
+        else:
+            n_unknown += s["B"]
+    tr.write_line(f"TOTAL requests={tot['B']} ties={tot['ties']} expected={exp:.2f} (over the "
+                  f"{tot['B'] - n_unknown} requests with a tie probability) excused={tot['excused']} "
                   f"other-branch={tot['excused_differing']} fallback={tot['fallback']}")
