@@ -272,8 +272,56 @@ bool trace_on() {
     if (on < 0) { const char* e = getenv("NJ_TRACE"); on = (e && *e == '1') ? 1 : 0; }
     return on == 1;
 }
+// NJ_LAUNCH_TIMES=1 (measurement): an event after every launch; at exit, per kernel
+// name the mean GPU time between its event and the previous launch's event on the same
+// stream (the kernel's duration in an eager back-to-back pipeline, no profiler attached),
+// printed to stderr.  Production runs leave it off (one getenv at first launch).
+struct LaunchTimes {
+    struct Rec { const char* name; cudaStream_t st; cudaEvent_t ev; };
+    std::vector<Rec> recs;
+    std::mutex mu;
+    ~LaunchTimes() {
+        if (recs.empty()) return;
+        cudaDeviceSynchronize();
+        std::unordered_map<std::string, std::pair<double, int64_t>> agg;
+        std::vector<std::string> order;
+        std::unordered_map<cudaStream_t, cudaEvent_t> last;
+        for (auto& r : recs) {
+            auto it = last.find(r.st);
+            if (it != last.end()) {
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, it->second, r.ev) == cudaSuccess) {
+                    auto& a = agg[r.name];
+                    if (a.second == 0) order.push_back(r.name);
+                    a.first += ms;
+                    a.second += 1;
+                }
+            }
+            last[r.st] = r.ev;
+        }
+        for (auto& n : order)
+            fprintf(stderr, "[nj-launch-times] %s n=%lld mean_us=%.2f\n", n.c_str(), (long long)agg[n].second,
+                    agg[n].first * 1e3 / agg[n].second);
+    }
+};
+LaunchTimes& launch_times() { static LaunchTimes lt; return lt; }
+bool launch_times_on() {
+    static int on = -1;
+    if (on < 0) { const char* e = getenv("NJ_LAUNCH_TIMES"); on = (e && *e == '1') ? 1 : 0; }
+    return on == 1;
+}
 cudaError_t trace(const char* what, cudaStream_t st) {
     cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && launch_times_on()) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) {
+            cudaEvent_t ev;
+            if (cudaEventCreate(&ev) == cudaSuccess) {
+                std::lock_guard<std::mutex> g(launch_times().mu);
+                if (cudaEventRecord(ev, st) == cudaSuccess) launch_times().recs.push_back({what, st, ev});
+            }
+        }
+    }
     if (!trace_on() || e != cudaSuccess) return e;
     e = cudaStreamSynchronize(st);
     fprintf(stderr, "[nj] %s -> %s\n", what, cudaGetErrorString(e));
