@@ -79,7 +79,7 @@ constexpr int kStagedMaxN = kBigMaxRowG;   // staged path on k_gemm_big (NJ_LM=0
 constexpr int kFusedAutoMaxN = 24;          // AUTO takes the fused kernel up to this many rows
 constexpr int kInlineLseRows = 64;          // staged path: N up to which k_accept merges row statistics inline
 constexpr int kStagedMaxRows = 2048;        // staged path on k_lmhead: rows of one GEMM pass (logits_st rows)
-constexpr int kPhaseTsN = 20 * 1024;     // debug timeline entries (NJ_PHASE_TS; k_lmhead uses [16K, 18K) for accumulator waits)
+constexpr int kPhaseTsN = 24 * 1024;     // debug timeline entries (NJ_PHASE_TS): k_lmhead [0, 18K) CTA 0 + [20K, 20.5K) per-CTA end, k_sample_small [18K, 20K)
 
 inline int round16(int x) { return (x + 15) & ~15; }
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -151,6 +151,10 @@ Knobs read_knobs() {
     k.lm_sleep = env_int("NJ_LM_SLEEP", 0);
     k.small_bmax = env_int("NJ_SMALL_BMAX", 12);
     k.inline_lse = env_int("NJ_INLINE_LSE", kInlineLseRows);
+    k.lm_pdl = env_int("NJ_LM_PDL", 0);             // k_lmhead triggers its dependents' launch at its start:
+                                                    // k_sample_small still starts ~4 us after the last GEMM CTA (no gain)
+    k.small_cl12 = env_int("NJ_SMALL_CL12", 1);     // 12-CTA clusters between 16 and 8
+    k.small_reuse = env_int("NJ_SMALL_REUSE", 1);   // owner CTA reads the located chunk from its staging buffer
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
@@ -221,7 +225,7 @@ struct nj_ctx {
     unsigned long long* amax = nullptr;   // nj_verify_greedy: per-row argmax keys [Nmax]
     int mass_nst = 2;                 // k_mass cp.async ring stages (NJ_MASS_NST: 2..4; 2 = 3 CTAs / SM)
     int mass_occ = 1;                 // resident k_mass CTAs per SM at mass_nst
-    int small_maxcl[17] = {};         // k_sample_small: co-resident clusters of 2 / 4 / 8 / 16 CTAs (0: unknown)
+    int small_maxcl[17] = {};         // k_sample_small: co-resident clusters of 2 / 4 / 8 / 12 / 16 CTAs (0: unknown)
     int32_t* scratch_i = nullptr;  // [MB]
     int32_t* s_row = nullptr;      // [MB] staged path: sample row of each request
     int32_t* g2row = nullptr;      // [Gmax] staged sharded step: packed row of each draft row
@@ -420,7 +424,9 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
 // not all fit); a smaller cluster then takes over in one wave
 int small_sampler_cl(const nj_ctx* c, int B) {
     int cl = (B <= 8 && c->kn.small_cl16) ? 16 : B <= 12 ? kSmallCl : (B * 4 <= c->num_sms ? 4 : 2);
-    while (cl > 2 && c->small_maxcl[cl] > 0 && c->small_maxcl[cl] < B) cl >>= 1;
+    auto fits = [&](int n) { return c->small_maxcl[n] == 0 || c->small_maxcl[n] >= B; };
+    if (cl == 16 && !fits(16) && c->kn.small_cl12 && fits(12)) return 12;
+    while (cl > 2 && !fits(cl)) cl >>= 1;
     return cl;
 }
 int small_pb_for(int nchunks, int cl) {   // chunks per staged batch (two buffers)
@@ -696,6 +702,7 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.sleep_ns = c->kn.lm_sleep;
     p.fence_full = c->kn.lm_fence;
     p.mma4 = c->kn.lm_mma4;
+    p.pdl = c->kn.lm_pdl;
     p.dbg = c->kn.lm_dbg;
     p.ts = nullptr;
     if (c->kn.phase_ts) {
@@ -1280,7 +1287,8 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 1>);
     e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    for (int cl = 2; cl <= 16 && !e; cl <<= 1) {
+    for (int cl : {2, 4, 8, 12, 16}) {
+        if (e) break;
         cudaLaunchConfig_t oc = {};
         oc.gridDim = dim3(cl);
         oc.blockDim = dim3(kSampThreads);
@@ -1297,8 +1305,8 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
         else (void)cudaGetLastError();   // unknown: keep the measured default size
     }
     if (getenv("NJ_SMALL_INFO"))
-        fprintf(stderr, "[nj] k_sample_small co-resident clusters: 2:%d 4:%d 8:%d 16:%d\n", c->small_maxcl[2],
-                c->small_maxcl[4], c->small_maxcl[8], c->small_maxcl[16]);
+        fprintf(stderr, "[nj] k_sample_small co-resident clusters: 2:%d 4:%d 8:%d 12:%d 16:%d\n", c->small_maxcl[2],
+                c->small_maxcl[4], c->small_maxcl[8], c->small_maxcl[12], c->small_maxcl[16]);
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 2>);
     if (const char* ev = getenv("NJ_MASS_NST")) c->mass_nst = std::min(4, std::max(2, atoi(ev)));
     e = e ? e : cudaFuncSetAttribute(k_mass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mass_smem(2, c->cfg.max_batch));
@@ -1507,7 +1515,14 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             mp.dbg_lse = dbg ? dbg->lse : nullptr;
             mp.certify = certify; mp.eps_draw = c->eps_draw;
             mp.small_pb = small_sampler_pb(c, pl.B);
+            mp.ts = nullptr;
+            if (c->kn.phase_ts) {
+                if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, kPhaseTsN * sizeof(unsigned long long)));
+                NJ_CUDA(c, cudaMemsetAsync(c->phase_ts + 18432, 0, 2048 * sizeof(unsigned long long), st));
+                mp.ts = c->phase_ts;
+            }
             mp.pdl_trigger = c->kn.small_trig;
+            mp.small_reuse = c->kn.small_reuse;
             mp.pf_rows = c->kn.small_pf && !c->q_remote && (ldq & 3) == 0 && (c->V_local & 3) == 0 &&
                          (reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0;
             cudaLaunchConfig_t cfg = {};

@@ -57,6 +57,8 @@ struct LmheadParams {
     int32_t arv1;                // 1: one accumulator-release arrival per CTA (named barrier first)
     int32_t fence_full;          // probe: tcgen05.fence::after_thread_sync after every operand wait
     int32_t mma4;                // 1: a k-block's four MMAs issued from one asm block under one elect
+    int32_t pdl;                 // 1: trigger the dependent grid's launch at the start (k_sample_small's
+                                 //    CTAs take the SMs this grid's CTAs free; they wait for its writes)
     int32_t nbuf, bstride;       // TMEM accumulator buffers and their column stride
     int32_t tile_w;              // vocab tile width (multiple of 16, <= 256; the last tile of a range is ragged)
     int32_t wbox;                // W box rows per CTA (tile_w / CG)
@@ -155,6 +157,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     const int nitems = rg.ntile;   // item it: tile it of the range, chunk cfix
     const int ngk = (p.num_kb + GK - 1) / GK;
 
+    if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmW);
         tma_prefetch_desc(&tmH);
@@ -556,6 +559,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     }
     if (WRITE && p.tma_out && warp < kLmEpiWarps && lane == 0) bulk_wait<0>();   // stores complete before exit
     __syncthreads();
+    if (p.ts != nullptr && threadIdx.x == 0 && blockIdx.x < 512) p.ts[20480 + blockIdx.x] = globaltimer();
     if (STATS || ARGMAX) {
         // merge the 4 column slices of every row of this CTA into its group's partial
         for (int i = threadIdx.x; i < nloc; i += kLmThreads) {

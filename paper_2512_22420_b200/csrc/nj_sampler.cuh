@@ -237,6 +237,7 @@ struct MassParams {
     int32_t pf_rows;       // k_sample_small: L2-prefetch the candidate rows while testing
     int32_t small_pb;      // k_sample_small: chunks per staged batch
     int32_t pdl_trigger;   // k_sample_small: trigger the fallback kernel's launch at the start
+    int32_t small_reuse;   // k_sample_small: the owner CTA reads the located chunk from its staging buffer
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -262,6 +263,7 @@ struct MassParams {
     // nj_propose: k_mass writes each bonus row's weights exp(l - lse) over its
     // logits in place (the q rows), and k_locate then reads them as weights
     int32_t w_inplace;
+    unsigned long long* ts;   // debug (NJ_PHASE_TS): k_sample_small phase stamps at [18432 + 16 CTA + k], CTA < 128
     int32_t probe;         // k_mass timing probes (NJ_MASS_PROBE; 0 in normal runs): 1 no copies, 2 no scans, 4 no totals
 };
 
@@ -487,7 +489,10 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
                                                                const ReqMeta m) {
     // launched with programmatic dependent launch: the CTAs start on SMs the GEMM's
     // finished CTAs free, then wait here for the whole GEMM grid and its writes
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 0] = globaltimer();
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 1] = globaltimer();
+
     // let the fp64 fallback kernel (launched next with programmatic serialization) be
     // scheduled now: it waits in its own griddepcontrol.wait for this grid to finish
     if (p.pdl_trigger && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -523,6 +528,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
         if (lane_id() == 0) s_lrow[i] = l;
     }
     __syncthreads();
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 2] = globaltimer();
     // (2) acceptance and first rejection: lane i of warp 0 tests draft i (k_accept's
     //     expressions), the first failing lane is the rejection; a near-tie flag counts
     //     only for tests up to it (k_accept stops there).  Every CTA of the cluster
@@ -557,6 +563,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
         if (lane == 0) s_n = n;
     }
     __syncthreads();
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 3] = globaltimer();
     const int n = s_n;
     const bool resid = n < gam;
     const float* lrow = p.logits + (int64_t)(ro + n) * p.ld;
@@ -629,11 +636,15 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     }
     // (4) every chunk mass from the CTA that owns it (distributed shared memory); the
     //     second cluster barrier keeps each CTA's cml alive until all have read it
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 4] = globaltimer();
     cluster_sync_all();
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 5] = globaltimer();
+
     for (int c = threadIdx.x; c < p.nchunks; c += kSampThreads)
         cm[c] = ld_shared_cluster_f64(mapa_shared(&cml[c], (uint32_t)(c % CL)));
     __syncthreads();
     cluster_sync_all();
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 6] = globaltimer();
     // (5) the draw: k_locate's unsharded arithmetic; the CTA owning the located chunk finishes
     if (threadIdx.x == 0) {
         double W = 0.0;
@@ -668,12 +679,28 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
         return;
     }
     const int c = sh_c;
+    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 7] = globaltimer();
     if (c % CL != rank) return;
     const double tp = sh_tp;
     float w[kSubTiles], v[kSubTiles];
-    // the located chunk's weights again (k_locate's chunk_weight: same expression)
+    // the located chunk's weights again (k_locate's chunk_weight: same expression), from
+    // this CTA's staging buffer when no later batch reused it (<= 2 batches), else global
+    if (p.small_reuse && nbat <= 2) {
+        const int j = (c - rank) / CL;
+        const float* sl = stage + (size_t)((j / PB) & 1) * PB * 2 * kChunk + (size_t)(j % PB) * 2 * kChunk;
+        const float* sq = sl + kChunk;
+        const int x0 = c * kChunk + (int)threadIdx.x;
 #pragma unroll
-    for (int s2 = 0; s2 < kSubTiles; ++s2) v[s2] = w[s2] = chunk_weight(p, lrow, c, s2, lsef, corr, resid, qrow);
+        for (int s2 = 0; s2 < kSubTiles; ++s2) {
+            const int o = s2 * kSampThreads + (int)threadIdx.x;
+            const bool in = x0 + s2 * kSampThreads < p.V_local;
+            const float e = in ? p_weight(sl[o], lsef, corr) : 0.f;
+            v[s2] = w[s2] = resid ? resid_weight(e, in ? sq[o] : 0.f) : e;
+        }
+    } else {
+#pragma unroll
+        for (int s2 = 0; s2 < kSubTiles; ++s2) v[s2] = w[s2] = chunk_weight(p, lrow, c, s2, lsef, corr, resid, qrow);
+    }
     warp_totals16(v, wt);
     __syncthreads();
     if (threadIdx.x < kSubTiles) {
@@ -734,6 +761,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
         if (p.dbg_flags) p.dbg_flags[b] = 0;
         const double margin = fmin(tp - lo, hi - tp);
         if (margin <= (double)p.eps_draw) flag_draw(p, b, 0);
+        if (p.ts && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 8] = globaltimer();
     }
 }
 
