@@ -2,11 +2,13 @@
 // 1-3) in ONE persistent cooperative kernel for N <= 48 rows (memory-bound
 // regime, BJ config 2).  Included from nj_gemm.cuh (namespace nj).
 //
-//   phase 1  GEMM over every row.  Accuracy (DESIGN.md "accuracy"): the MMA
-//            accumulator is restarted every k-block (4 MMAs, K = 64) in a
-//            scratch TMEM buffer and the epilogue sums the partials in fp64 —
-//            tcgen05 truncates (RZ) on every fp32 accumulate, which over
-//            K = 3584 biases logits by -3.3e-6*l; restarting cuts that 68x.
+//   phase 1  GEMM over every row.  Accuracy (DESIGN.md §6): the MMA
+//            accumulator is restarted every ring stage (GK = 4 k-blocks, 16
+//            MMAs; NJ_SACC=0: every k-block) in a scratch TMEM buffer and the
+//            epilogue sums the partials in fp64 — tcgen05 truncates (RZ) on
+//            every fp32 accumulate, which over K = 3584 biases logits by
+//            -3.3e-6*l; restarting cuts that ~14x (acceptance certificate
+//            eps_acc_fused x the stage span, nj_api.cu).
 //            The fp64 logits are captured for draft tokens and stored back to
 //            TMEM as fp32 (this CTA's logits stay resident: ntiles*NPAD +
 //            nbuf*NPAD <= 512 columns); softmax statistics follow from them.
@@ -23,8 +25,9 @@
 //            with boundaries E(x) = I(x-1) built from the same fp32 scans, so
 //            the intervals [E, I) tile [0, W) exactly (no gaps, no overlaps).
 // W is streamed from HBM exactly once; nothing of size V x N is written.
-// Every decision whose margin is inside the certificate is queued for the fp64
-// fallback (nj_sampler.cuh), which makes the output equal the fp64 definition.
+// Every acceptance test whose margin is inside the certificate, and every
+// zero-mass draw (R6), is queued for the fp64 fallback (nj_sampler.cuh); the
+// draws themselves are not certified (R16, include/nj.h accuracy contract).
 
 // NC consecutive TMEM columns, one wait (NC in {8, 16, 24, 32, 48})
 template <int NC>
