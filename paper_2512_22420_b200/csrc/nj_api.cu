@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -155,6 +155,7 @@ Knobs read_knobs() {
                                                     // k_sample_small still starts ~4 us after the last GEMM CTA (no gain)
     k.small_cl12 = env_int("NJ_SMALL_CL12", 1);     // 12-CTA clusters between 16 and 8
     k.small_reuse = env_int("NJ_SMALL_REUSE", 1);   // owner CTA reads the located chunk from its staging buffer
+    k.small_cl = env_int("NJ_SMALL_CL", 0);         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
@@ -423,6 +424,8 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
 // sampler's time (measured 20 -> 34 us at B = 8 on a box where 16-CTA clusters did
 // not all fit); a smaller cluster then takes over in one wave
 int small_sampler_cl(const nj_ctx* c, int B) {
+    const int f = c->kn.small_cl;
+    if ((f == 2 || f == 4 || f == 8 || f == 12 || f == 16) && B * f <= c->num_sms) return f;   // tests
     int cl = (B <= 8 && c->kn.small_cl16) ? 16 : B <= 12 ? kSmallCl : (B * 4 <= c->num_sms ? 4 : 2);
     auto fits = [&](int n) { return c->small_maxcl[n] == 0 || c->small_maxcl[n] >= B; };
     if (cl == 16 && !fits(16) && c->kn.small_cl12 && fits(12)) return 12;

@@ -62,6 +62,14 @@ os.environ.pop("NJ_LM_CG", None)
 b = make_batch(7, "mixed:5", V=40000, d=64, seed=13, device=dev)
 run(b, NJ_PATH_STAGED)
 print("staged small-batch sampler ok", flush=True)
+# forced cluster sizes: 12 / 2 CTAs per request, 25 chunks (2 CTAs: 5 staged batches, the owner
+# re-reads its chunk from global memory; 12: one batch, read from the staging buffer)
+for cl in ("12", "2"):
+    os.environ["NJ_SMALL_CL"] = cl
+    b = make_batch(5, "mixed:4", V=100000, d=64, seed=14, device=dev)
+    run(b, NJ_PATH_STAGED)
+    print("staged small-batch sampler cl" + cl, "ok", flush=True)
+os.environ.pop("NJ_SMALL_CL", None)
 b = make_batch(6, "mixed:4", V=2048, d=128, seed=5, device=dev)
 grp = ShardGroup(128, 2048, max_batch=6, gamma_max=5, nshards=4)
 acc = torch.empty(6, dtype=torch.int32, device=dev)
@@ -87,4 +95,6 @@ if "--c2" in sys.argv:
     b = make_batch(8, 3, V=152064, d=3584, seed=100, device=dev, W=W)
     run(b, NJ_PATH_FUSED)
     print("c2 fused ok", flush=True)
+    run(b, NJ_PATH_STAGED)   # k_lmhead (one CTA chunk, 2-k-block stages) + k_sample_small
+    print("c2 staged ok", flush=True)
 print("all cases ok")

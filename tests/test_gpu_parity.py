@@ -467,3 +467,30 @@ def test_strided_misaligned_draft_probs(path):
         assert b_strided.draft_probs.stride(0) == V + 3
         acc, nxt, dd, _ = run(b_strided, path)
         check(b, acc, nxt, dd)
+
+
+@pytest.mark.parametrize("B,g", [(8, 3), (12, "mixed:5")])
+def test_small_sampler_cluster_sizes(B, g, monkeypatch):
+    """k_sample_small with every cluster size (16 / 12 / 8 / 4 / 2 CTAs per request:
+    one to seven staged chunk batches per CTA) and with the owner CTA reading the
+    located chunk from its staging buffer or from global memory: bit-identical
+    decisions, masses and tokens (same expressions and reduction order as
+    k_accept / k_mass / k_locate), and the default launch vs the oracle."""
+    b = make_batch(B, g, V=QV, d=QD, seed=B + 71, device=DEV, W=w_full())
+    ref = None
+    for cl in (0, 16, 12, 8, 4, 2):
+        for reuse in (1, 0):
+            if B * max(cl, 1) > torch.cuda.get_device_properties(0).multi_processor_count:
+                continue
+            monkeypatch.setenv("NJ_SMALL_CL", str(cl))
+            monkeypatch.setenv("NJ_SMALL_REUSE", str(reuse))
+            acc, nxt, dd, v = run(b)
+            assert v.plan(b.gamma)[0] == NJ_PATH_STAGED
+            out = (acc, nxt, dd["mass"], dd["flags"])
+            if ref is None:
+                ref = out
+                check(b, acc, nxt, dd, lnp_tol=2e-5, lse_tol=2e-5)
+            else:
+                for x, y in zip(out, ref):
+                    np.testing.assert_array_equal(x, y, err_msg=f"cluster {cl} reuse {reuse}")
+            v.close()
