@@ -469,11 +469,23 @@ def bench_nj(args, ws, rank, local):
         # bytes that cross the host link per step: the copied hidden / tokens / uniforms,
         # plus the draft-probability bytes the kernels read in place (zero copy):
         # q_i(x_i) of every draft and the sample row of every rejected request
-        rej0 = per_batch[0][1]
-        h2d = (b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.N * 4 + b.G * 4 + rej0 * V_Q * 4)
+        # (+ the likely sample rows nj_verify_host staged over the copy stream during the
+        # GEMM, NJ_OPT_Q_STAGE_ROWS; a rejected request's row is read in place only when
+        # it was not staged).  Every e2e step verifies the same batch, so the last call's
+        # outputs and staged rows are every step's.
+        staged = set(int(r) for r in v.host_staged_rows())
+        gam = np.asarray(b.gamma)
+        g0 = np.concatenate([[0], np.cumsum(gam)[:-1]])
+        an = ah.numpy()
+        rej_rows = [int(g0[i] + an[i]) for i in range(Bl) if an[i] < gam[i]]
+        inplace_rows = sum(1 for r in rej_rows if r not in staged)
+        h2d = (b.hidden.numel() * 2 + b.draft_tokens.numel() * 4 + b.N * 4 + b.G * 4
+               + (len(staged) + inplace_rows) * V_Q * 4)
         e2e = {"value": N_global * k_e2e / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(2 * Bl * 4), "steps": k_e2e, "api": "nj_verify_host",
-               "q_rows": "read in place from pinned host memory (NJ_OPT_Q_ZERO_COPY)"}
+               "q_rows": (f"{len(staged)} likely sample rows staged to the device during the GEMM, "
+                          f"{inplace_rows} rejected rows read in place from pinned host memory"
+                          if staged else "read in place from pinned host memory (NJ_OPT_Q_ZERO_COPY)")}
     if ws > 1:
         dist.barrier()
     if rank != 0:

@@ -158,6 +158,12 @@ nj_status nj_verify_host(nj_ctx* ctx, void* stream,
                          const int32_t* gamma_per_req, const float* uniforms_h,
                          int32_t B, int32_t* accept_len_h, int32_t* next_token_h);
 
+/* The draft rows g the last nj_verify_host call staged to the device before the
+ * sampler (NJ_OPT_Q_STAGE_ROWS): *n_out = their count, the first max_rows of
+ * them written to rows_out (may be NULL when max_rows = 0).  For byte
+ * accounting of the host link (bench.py's e2e).  NJ_EINVAL on NULL ctx/n_out. */
+nj_status nj_host_staged_rows(nj_ctx* ctx, int32_t* rows_out, int32_t max_rows, int32_t* n_out);
+
 /* Execution path of nj_verify. */
 typedef enum {
     NJ_PATH_AUTO = 0,    /* pick by size            */
@@ -177,10 +183,18 @@ typedef enum {
     NJ_OPT_FORCE_FALLBACK = 3,/* 1: recompute EVERY request in fp64 (tests)      */
     NJ_OPT_PROFILE = 4,       /* 1: bracket the dominant kernel of every nj_verify */
                               /*    with CUDA events (see nj_kernel_time)           */
-    NJ_OPT_Q_ZERO_COPY = 5    /* nj_verify_host: 1 (default) read a pinned, mapped */
+    NJ_OPT_Q_ZERO_COPY = 5,   /* nj_verify_host: 1 (default) read a pinned, mapped */
                               /*    draft_probs_h in place over the host link (only */
                               /*    q_i(x_i) and rejected rows are touched); 0 copy */
                               /*    all G rows to the device first                  */
+    NJ_OPT_Q_STAGE_ROWS = 6   /* nj_verify_host with in-place q, when the small-   */
+                              /*    batch sampler runs (staged path, B <= 12): how  */
+                              /*    many likely sample rows (first-rejection        */
+                              /*    positions 0, 1, ... of every request) to copy   */
+                              /*    to the device on a second stream while the GEMM */
+                              /*    runs; -1 as many as the host link moves in the  */
+                              /*    GEMM's time, 0 (default) none, else <= 256.     */
+                              /*    Outputs are identical either way (same values). */
 } nj_option;
 
 nj_status nj_set_option(nj_ctx* ctx, nj_option opt, int64_t value);

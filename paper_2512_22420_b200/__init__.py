@@ -9,9 +9,9 @@ the C ABI + the C++ bandit), the ctypes binding (_lib.py), the build script
 (_build.py) and the multi-GPU driver (dist.py).  It never imports oracle/.
 """
 from ._lib import (NJ_FLAG_CLAMP, NJ_FLAG_FALLBACK, NJ_FLAG_ZERO_MASS, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK,
-                   NJ_OPT_PATH, NJ_OPT_PROFILE, NJ_OPT_Q_ZERO_COPY, NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_STAGED, NJ_PATH_TWOPASS, Bandit, NcclComm, NJError, ShardGroup, Verifier, load,
+                   NJ_OPT_PATH, NJ_OPT_PROFILE, NJ_OPT_Q_STAGE_ROWS, NJ_OPT_Q_ZERO_COPY, NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_STAGED, NJ_PATH_TWOPASS, Bandit, NcclComm, NJError, ShardGroup, Verifier, load,
                    nccl_unique_id, shard_range)
 
 __all__ = ["Verifier", "Bandit", "ShardGroup", "NcclComm", "nccl_unique_id", "shard_range", "NJError", "load", "NJ_PATH_AUTO", "NJ_PATH_FUSED", "NJ_PATH_TWOPASS", "NJ_PATH_STAGED",
-           "NJ_OPT_PATH", "NJ_OPT_PROFILE", "NJ_OPT_Q_ZERO_COPY", "NJ_OPT_CERTIFY", "NJ_OPT_FORCE_FALLBACK", "NJ_FLAG_FALLBACK", "NJ_FLAG_ZERO_MASS",
+           "NJ_OPT_PATH", "NJ_OPT_PROFILE", "NJ_OPT_Q_ZERO_COPY", "NJ_OPT_Q_STAGE_ROWS", "NJ_OPT_CERTIFY", "NJ_OPT_FORCE_FALLBACK", "NJ_FLAG_FALLBACK", "NJ_FLAG_ZERO_MASS",
            "NJ_FLAG_CLAMP"]

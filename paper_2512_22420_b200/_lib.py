@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libnj.so")
 
 NJ_OK, NJ_EINVAL, NJ_ESHAPE, NJ_ECUDA, NJ_ENCCL, NJ_ENOMEM, NJ_EUNSUPPORTED = range(7)
 NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_TWOPASS, NJ_PATH_STAGED = 0, 1, 2, 3
-NJ_OPT_PATH, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PROFILE, NJ_OPT_Q_ZERO_COPY = 1, 2, 3, 4, 5
+NJ_OPT_PATH, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PROFILE, NJ_OPT_Q_ZERO_COPY, NJ_OPT_Q_STAGE_ROWS = 1, 2, 3, 4, 5, 6
 NJ_FLAG_FALLBACK, NJ_FLAG_ZERO_MASS, NJ_FLAG_CLAMP = 1, 2, 4
 
 # every symbol include/nj.h declares (checked by tests/test_abi.py)
@@ -34,7 +34,7 @@ EXPORTS = [
     "nj_bandit_last_gamma", "nj_bandit_snapshot_json",
     "nj_shard_range", "nj_nccl_get_unique_id", "nj_nccl_comm_init", "nj_nccl_comm_destroy", "nj_group_create",
     "nj_group_destroy", "nj_group_member", "nj_group_last_error", "nj_group_verify",
-    "nj_propose", "nj_verify_greedy",
+    "nj_propose", "nj_verify_greedy", "nj_host_staged_rows",
 ]
 NJ_NCCL_ID_BYTES = 128
 
@@ -83,6 +83,7 @@ def load():
         "nj_last_error": ([P], ctypes.c_char_p),
         "nj_verify": ([P, P, P, P, P, P, I64, P, P, I32, P, P, P], I32),
         "nj_verify_host": ([P, P, P, P, P, P, I64, P, P, I32, P, P], I32),
+        "nj_host_staged_rows": ([P, P, I32, P], I32),
         "nj_set_option": ([P, I32, I64], I32),
         "nj_set_temperature": ([P, D], I32),
         "nj_plan": ([P, P, I32, P, P], I32),
@@ -259,6 +260,14 @@ class Verifier:
         self._check(self._lib.nj_verify_host(
             self._h, _stream(stream), _ptr(hidden_h), _ptr(W), _ptr(tok_h), _ptr(q_h), ldq, _ptr(g),
             _ptr(u_h), g.shape[0], _ptr(acc_h), _ptr(next_h)))
+
+    def host_staged_rows(self):
+        """nj_host_staged_rows: the draft rows the last verify_host staged to the device."""
+        n = ctypes.c_int32(0)
+        self._check(self._lib.nj_host_staged_rows(self._h, None, 0, ctypes.byref(n)))
+        rows = np.zeros(max(n.value, 1), np.int32)
+        self._check(self._lib.nj_host_staged_rows(self._h, rows.ctypes.data, n.value, ctypes.byref(n)))
+        return rows[:n.value]
 
     def lmhead_logits(self, hidden, W, rows, out, ks: int = 0, stream=None):
         """nj_lmhead_logits: fp32 logits of hidden[rows] through the production GEMM."""

@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -155,7 +155,8 @@ Knobs read_knobs() {
                                                     // k_sample_small still starts ~4 us after the last GEMM CTA (no gain)
     k.small_cl12 = env_int("NJ_SMALL_CL12", 1);     // 12-CTA clusters between 16 and 8
     k.small_reuse = env_int("NJ_SMALL_REUSE", 1);   // owner CTA reads the located chunk from its staging buffer
-    k.small_cl = env_int("NJ_SMALL_CL", 0);         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
+    k.small_cl = env_int("NJ_SMALL_CL", 0);
+    k.qstage_gbs = env_int("NJ_QSTAGE_GBS", 50);    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
@@ -246,6 +247,15 @@ struct nj_ctx {
     int64_t st_ldq = 0;
     int q_zero_copy = 1;   // nj_verify_host: read mapped pinned q in place (NJ_OPT_Q_ZERO_COPY)
     int q_remote = 0;      // the current call's q lives in host memory (no bulk q prefetch)
+    // nj_verify_host, zero-copy q: the likely sample rows staged into st_q over a copy
+    // stream while the GEMM runs (NJ_OPT_Q_STAGE_ROWS; -1 auto budget, 0 off = default)
+    int q_stage_opt = 0;   // off by default: on this pool's hosts a pinned 608-KB copy takes ~50 us
+                           // (12.6 GB/s; 40 GB/s for 8 MB), so staging gains <= 6 % of a C2 call, noisily
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_qstage = nullptr;
+    int qstage_active = 0;              // the current call staged rows (the sampler waits for ev_qstage)
+    uint64_t qstage_mask[4] = {};       // staged draft rows (bit g), G <= 256
+    std::vector<int32_t> qstage_rows;   // the last call's staged rows (nj_host_staged_rows)
     // W tensor-map cache
     const void* w_cached = nullptr;
     CUtensorMap tmW128{}, tmW16{};
@@ -404,7 +414,8 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
         // N = 4 fused 193 vs 203 us)
         // q read in place from host memory (nj_verify_host, zero-copy): the fused kernel's
         // all-in-flight async copies of the rejected rows beat the staged sampler's
-        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm || c->q_remote)) ? NJ_PATH_FUSED
+        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm || (c->q_remote && !c->qstage_active)))
+                   ? NJ_PATH_FUSED
                : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
         return set_err(c, NJ_EUNSUPPORTED, "fused path needs N <= %d and TMEM room (N=%d)", kFusedMaxN, pl.N);
@@ -1332,6 +1343,8 @@ void nj_destroy(nj_ctx* c) {
     if (!c) return;
     for (auto& e : c->ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
     for (auto& e : c->ev_free) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+    if (c->ev_qstage) cudaEventDestroy(c->ev_qstage);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     for (void* p : c->allocs) cudaFree(p);
     delete c;
 }
@@ -1349,6 +1362,7 @@ nj_status nj_set_option(nj_ctx* c, nj_option opt, int64_t v) {
         case NJ_OPT_FORCE_FALLBACK: c->force_fb = v != 0; return NJ_OK;
         case NJ_OPT_PROFILE: c->profile = v != 0; return NJ_OK;
         case NJ_OPT_Q_ZERO_COPY: c->q_zero_copy = v != 0; return NJ_OK;
+        case NJ_OPT_Q_STAGE_ROWS: c->q_stage_opt = (int)std::max<int64_t>(-1, std::min<int64_t>(v, 256)); return NJ_OK;
     }
     return set_err(c, NJ_EINVAL, "unknown option %d", (int)opt);
 }
@@ -1526,6 +1540,12 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             }
             mp.pdl_trigger = c->kn.small_trig;
             mp.small_reuse = c->kn.small_reuse;
+            if (c->qstage_active) {
+                // nj_verify_host staged the likely sample rows over the copy stream during the GEMM
+                NJ_CUDA(c, cudaStreamWaitEvent(st, c->ev_qstage, 0));
+                mp.q_loc = c->st_q;
+                for (int i = 0; i < 4; ++i) mp.q_loc_mask[i] = c->qstage_mask[i];
+            }
             mp.pf_rows = c->kn.small_pf && !c->q_remote && (ldq & 3) == 0 && (c->V_local & 3) == 0 &&
                          (reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0;
             cudaLaunchConfig_t cfg = {};
@@ -1681,6 +1701,9 @@ nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, cons
     // move ~G/R times the bytes the method reads.
     const float* qd = c->st_q;
     c->q_remote = 0;
+    c->qstage_active = 0;
+    c->qstage_rows.clear();
+    for (auto& w : c->qstage_mask) w = 0;
     if (pl.G > 0) {
         NJ_CUDA(c, cudaMemcpyAsync(c->st_tok, tok_h, (size_t)pl.G * 4, cudaMemcpyHostToDevice, st));
         cudaPointerAttributes at{};
@@ -1688,6 +1711,32 @@ nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, cons
             at.devicePointer) {
             qd = static_cast<const float*>(at.devicePointer);
             c->q_remote = 1;
+            // The kernels read only q_i(x_i) and each rejected request's row n_b, known after
+            // the GEMM.  When the one-launch small-batch sampler will run, the rows of the
+            // likely first-rejection positions (position 0 of every request, then 1, ...:
+            // P(n_b = i) falls geometrically with i) are copied to st_q over a second
+            // stream while the GEMM streams W, as many as the host link moves in the GEMM's
+            // time; the sampler waits for them and reads the rest in place.
+            if (c->q_stage_opt != 0 && pl.path == NJ_PATH_STAGED && small_sampler_ok(c, pl) && pl.G <= 256) {
+                const double rowb = (double)c->cfg.V * 4.0;
+                const double t_gemm = std::max(2.0 * c->cfg.V * c->cfg.d / 6.5e12, 2.0 * pl.N * c->cfg.V * c->cfg.d / 1.35e15);
+                int budget = c->q_stage_opt > 0 ? c->q_stage_opt : (int)(t_gemm * c->kn.qstage_gbs * 1e9 / rowb);
+                budget = std::min(budget, pl.G);
+                for (int pos = 0; (int)c->qstage_rows.size() < budget && pos < c->cfg.gamma_max; ++pos)
+                    for (int b = 0; b < pl.B && (int)c->qstage_rows.size() < budget; ++b)
+                        if (pos < pl.row_off[b + 1] - pl.row_off[b] - 1) c->qstage_rows.push_back(pl.row_off[b] - b + pos);
+                if (!c->qstage_rows.empty()) {
+                    if (!c->cstream) NJ_CUDA(c, cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+                    if (!c->ev_qstage) NJ_CUDA(c, cudaEventCreateWithFlags(&c->ev_qstage, cudaEventDisableTiming));
+                    for (int g : c->qstage_rows) {
+                        NJ_CUDA(c, cudaMemcpyAsync(c->st_q + (size_t)g * ldq, q_h + (size_t)g * ldq, (size_t)c->cfg.V * 4,
+                                                   cudaMemcpyHostToDevice, c->cstream));
+                        c->qstage_mask[g >> 6] |= 1ull << (g & 63);
+                    }
+                    NJ_CUDA(c, cudaEventRecord(c->ev_qstage, c->cstream));
+                    c->qstage_active = 1;
+                }
+            }
         } else {
             (void)cudaGetLastError();
             NJ_CUDA(c, cudaMemcpyAsync(c->st_q, q_h, (size_t)pl.G * ldq * 4, cudaMemcpyHostToDevice, st));
@@ -1696,10 +1745,18 @@ nj_status nj_verify_host(nj_ctx* c, void* stream, const uint16_t* hidden_h, cons
     s = nj_verify(c, stream, c->st_hidden, W_lm, c->st_tok, qd, ldq, gamma, c->st_u, B, c->st_acc,
                   c->st_next, nullptr);
     c->q_remote = 0;
+    c->qstage_active = 0;
     if (s != NJ_OK) return s;
     NJ_CUDA(c, cudaMemcpyAsync(acc_h, c->st_acc, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
     NJ_CUDA(c, cudaMemcpyAsync(next_h, c->st_next, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
     NJ_CUDA(c, cudaStreamSynchronize(st));
+    return NJ_OK;
+}
+
+nj_status nj_host_staged_rows(nj_ctx* c, int32_t* rows_out, int32_t max_rows, int32_t* n_out) {
+    if (!c || !n_out || (max_rows > 0 && !rows_out)) return NJ_EINVAL;
+    *n_out = (int32_t)c->qstage_rows.size();
+    for (int i = 0; i < std::min<int>(max_rows, (int)c->qstage_rows.size()); ++i) rows_out[i] = c->qstage_rows[i];
     return NJ_OK;
 }
 

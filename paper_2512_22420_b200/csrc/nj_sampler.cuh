@@ -238,6 +238,10 @@ struct MassParams {
     int32_t small_pb;      // k_sample_small: chunks per staged batch
     int32_t pdl_trigger;   // k_sample_small: trigger the fallback kernel's launch at the start
     int32_t small_reuse;   // k_sample_small: the owner CTA reads the located chunk from its staging buffer
+    // nj_verify_host with host-resident q: draft rows g with bit g set were staged into
+    // q_loc (same pitch ldq) while the GEMM ran; the others are read in place (q)
+    const float* q_loc;
+    uint64_t q_loc_mask[4];
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -485,6 +489,10 @@ constexpr int kSmallCl = 8;         // CTAs per request (16 when B <= 8: one clu
 constexpr int kSmallMaxPerCta = 4;  // chunks per staged batch (two batch buffers of <= 3 x 32 KB)
 constexpr int kSmallMaxChunks = 64;
 constexpr int kSmallMaxRows = 16;   // gamma_max <= 15
+__device__ __forceinline__ const float* small_q_row(const MassParams& p, int g) {
+    return (p.q_loc && ((p.q_loc_mask[g >> 6] >> (g & 63)) & 1ull)) ? p.q_loc + (int64_t)g * p.ldq
+                                                                      : p.q + (int64_t)g * p.ldq;
+}
 __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParams ap, const MassParams p,
                                                                const ReqMeta m) {
     // launched with programmatic dependent launch: the CTAs start on SMs the GEMM's
@@ -541,7 +549,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
             const int g = g0 + lane;
             const double lse = s_lrow[lane], dlv = __ldcg(&ap.dl[g]);
             pd = exp(dlv - lse);
-            const double qx = (double)ap.q[(int64_t)g * ap.ldq + ap.draft_tokens[g]];
+            const double qx = (double)small_q_row(p, g)[ap.draft_tokens[g]];
             const double uq = (double)ap.u[ro + lane] * qx;
             near = fabs(uq - pd) <= (double)ap.eps_acc * pd;
             fail = !(uq < pd);
@@ -567,7 +575,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     const int n = s_n;
     const bool resid = n < gam;
     const float* lrow = p.logits + (int64_t)(ro + n) * p.ld;
-    const float* qrow = resid ? p.q + (int64_t)(g0 + n) * p.ldq + p.v_begin : nullptr;
+    const float* qrow = resid ? small_q_row(p, g0 + n) + p.v_begin : nullptr;
     const double lse = s_lrow[n];
     const float lsef = (float)lse, corr = lse_corr(lse);
     // (3) this CTA's chunk masses (k_mass's weights and reduction order): its chunks

@@ -24,7 +24,7 @@ import torch
 import oracle
 import parity
 from oracle import bruteforce
-from paper_2512_22420_b200 import (NJ_FLAG_FALLBACK, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PATH,
+from paper_2512_22420_b200 import (NJ_FLAG_FALLBACK, NJ_OPT_CERTIFY, NJ_OPT_FORCE_FALLBACK, NJ_OPT_PATH, NJ_OPT_Q_STAGE_ROWS,
                                    NJ_PATH_AUTO, NJ_PATH_FUSED, NJ_PATH_STAGED, NJ_PATH_TWOPASS, NJError, Verifier)
 from synth.inputs import dyadic_rows, make_batch, make_sampler_case, make_weight
 
@@ -351,6 +351,37 @@ def test_verify_host_equals_device():
     nxt_h = torch.empty(8, dtype=torch.int32).pin_memory()
     v.verify_host(pin(b.hidden), b.W, pin(b.draft_tokens), pin(b.draft_probs), b.gamma, pin(b.uniforms), acc_h, nxt_h)
     assert (acc_h.numpy() == acc).all() and (nxt_h.numpy() == nxt).all()
+
+
+@pytest.mark.parametrize("B,g,V,d", [(8, 4, 4096, 128), (12, "mixed:5", 20000, 128), (8, 3, QV, QD)])
+def test_verify_host_staged_q_rows(B, g, V, d):
+    """nj_verify_host with in-place (zero-copy) q on the staged small-batch path:
+    the likely sample rows staged to the device over the copy stream
+    (NJ_OPT_Q_STAGE_ROWS none / some / all / auto) give outputs identical to
+    nj_verify on device buffers, the staged rows are the first-rejection
+    positions in ascending order, and the device outputs match the oracle."""
+    b = make_batch(B, g, V=V, d=d, seed=B + 5, device=DEV, W=w_full() if V == QV else None)
+    acc, nxt, dd, v = run(b)
+    assert v.plan(b.gamma)[0] == NJ_PATH_STAGED
+    check(b, acc, nxt, dd, lnp_tol=2e-5 if V == QV else 2e-3, lse_tol=2e-5 if V == QV else None)
+    pin = lambda t: t.cpu().pin_memory()
+    hh, th, qh, uh = pin(b.hidden), pin(b.draft_tokens), pin(b.draft_probs), pin(b.uniforms)
+    gam = np.asarray(b.gamma)
+    g0 = np.concatenate([[0], np.cumsum(gam)[:-1]])
+    order = [g0[r] + pos for pos in range(int(gam.max())) for r in range(B) if pos < gam[r]]
+    for nst in (0, 3, 256, -1):
+        v.set_option(NJ_OPT_Q_STAGE_ROWS, nst)
+        acc_h = torch.full((B,), -7, dtype=torch.int32).pin_memory()
+        nxt_h = torch.full((B,), -7, dtype=torch.int32).pin_memory()
+        v.verify_host(hh, b.W, th, qh, b.gamma, uh, acc_h, nxt_h)
+        assert (acc_h.numpy() == acc).all() and (nxt_h.numpy() == nxt).all(), nst
+        rows = v.host_staged_rows()
+        want = order[:len(rows)]
+        assert list(rows) == want, (nst, list(rows), want)
+        if nst >= 0:
+            assert len(rows) == min(nst, b.G), (nst, len(rows))
+        elif V == QV:
+            assert len(rows) > 0   # the Qwen-shape GEMM time covers several rows
 
 
 def test_invalid_arguments():
