@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -156,7 +156,9 @@ Knobs read_knobs() {
     k.small_cl12 = env_int("NJ_SMALL_CL12", 1);     // 12-CTA clusters between 16 and 8
     k.small_reuse = env_int("NJ_SMALL_REUSE", 1);   // owner CTA reads the located chunk from its staging buffer
     k.small_cl = env_int("NJ_SMALL_CL", 0);
-    k.qstage_gbs = env_int("NJ_QSTAGE_GBS", 50);    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
+    k.qstage_gbs = env_int("NJ_QSTAGE_GBS", 50);
+    k.pdl_chain = env_int("NJ_PDL_CHAIN", 0);       // staged multi-kernel sampler as a PDL chain (no gain measured:
+                                                    // B = 16 / 64 / 256 equal within the box's noise)    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
     k.qpf = env_int("NJ_QPF", 0);   // measured slower (the prefetch competes with the W stream)
     k.lm_ost = std::min(2, std::max(1, env_int("NJ_LM_OST", 1)));
@@ -793,9 +795,38 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     return NJ_OK;
 }
 
+template <typename K, typename... Args>
+cudaError_t launch_pdl_smem(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <typename K, typename... Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // K-D: [k_sample_lse when some sample-row lse is still NaN] + k_mass over a
 // grid of num_sms x resident CTAs taking (request, chunk) items round-robin.
-nj_status launch_mass(nj_ctx* c, cudaStream_t st, const MassParams& mp, int B, bool need_lse) {
+nj_status launch_mass(nj_ctx* c, cudaStream_t st, const MassParams& mp, int B, bool need_lse, bool pdl = false) {
     if (B <= 0) return NJ_OK;
     if (need_lse) {
         k_sample_lse<<<(B + 7) / 8, 256, 0, st>>>(mp, B, const_cast<double*>(mp.s_lse));   // ctx-owned s_lse
@@ -805,7 +836,10 @@ nj_status launch_mass(nj_ctx* c, cudaStream_t st, const MassParams& mp, int B, b
     const int grid = std::max(1, std::min(total, c->num_sms * c->mass_occ));
     const_cast<MassParams&>(mp).probe = c->kn.mass_probe;
     const size_t sm = mass_smem(c->mass_nst, B);
-    if (c->mass_nst == 2) k_mass<2><<<grid, kSampThreads, sm, st>>>(mp, B);
+    if (pdl) {
+        auto km = c->mass_nst == 2 ? k_mass<2> : c->mass_nst == 4 ? k_mass<4> : k_mass<3>;
+        NJ_CUDA(c, launch_pdl_smem(km, dim3(grid), dim3(kSampThreads), sm, st, mp, B));
+    } else if (c->mass_nst == 2) k_mass<2><<<grid, kSampThreads, sm, st>>>(mp, B);
     else if (c->mass_nst == 4) k_mass<4><<<grid, kSampThreads, sm, st>>>(mp, B);
     else k_mass<3><<<grid, kSampThreads, sm, st>>>(mp, B);
     NJ_LAUNCHED(c, "k_mass", st);
@@ -839,21 +873,6 @@ FbParams fb_params(nj_ctx* c, const uint16_t* hidden, const uint16_t* W, const i
 
 // launch with programmatic stream serialization (PDL): the kernel may start
 // before its predecessor finishes and waits in-kernel (griddepcontrol.wait)
-template <typename K, typename... Args>
-cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t st, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, args...);
-}
-
 nj_status launch_fallback(nj_ctx* c, cudaStream_t st, const FbParams& f, const ReqMeta& m) {
     NJ_CUDA(c, launch_pdl(k_fb, dim3(c->num_sms * 2), dim3(256), st, f, m));
     NJ_LAUNCHED(c, "k_fb", st);
@@ -1568,12 +1587,17 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             goto fallback;
         }
         // small batches: k_accept merges its rows' statistics itself (one launch fewer)
+        // (NJ_PDL_CHAIN: the sampler kernels launched as programmatic dependents, pdl_enter)
+        const bool pdl = c->kn.pdl_chain != 0;
         if (pl.N > c->kn.inline_lse) {
-            k_lse_rows<<<(pl.N + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.N, c->row_lse);
+            if (pdl) NJ_CUDA(c, launch_pdl(k_lse_rows, dim3((pl.N + 7) / 8), dim3(256), st, (const float*)c->part_m,
+                                           (const float*)c->part_s, c->pld, gridA, pl.N, c->row_lse));
+            else k_lse_rows<<<(pl.N + 7) / 8, 256, 0, st>>>(c->part_m, c->part_s, c->pld, gridA, pl.N, c->row_lse);
             NJ_LAUNCHED(c, "k_lse_rows", st);
             ap.pre_lse = c->row_lse;
         }
-        k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
+        if (pdl) NJ_CUDA(c, launch_pdl(k_accept, dim3((pl.B + 7) / 8), dim3(256), st, ap, meta));
+        else k_accept<<<(pl.B + 7) / 8, 256, 0, st>>>(ap, meta);
         NJ_LAUNCHED(c, "k_accept", st);
         MassParams mp{};
         mp.logits = c->logits_st; mp.ld = c->V_local; mp.s_row = c->s_row;
@@ -1586,8 +1610,9 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
         mp.dbg_mass = dbg ? dbg->mass : nullptr; mp.dbg_flags = dbg ? dbg->flags : nullptr;
         mp.dbg_lse = dbg ? dbg->lse : nullptr;
         mp.certify = certify; mp.eps_draw = c->eps_draw;
-        if ((s = launch_mass(c, st, mp, pl.B, false)) != NJ_OK) return s;
-        k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
+        if ((s = launch_mass(c, st, mp, pl.B, false, pdl)) != NJ_OK) return s;
+        if (pdl) NJ_CUDA(c, launch_pdl(k_locate, dim3(pl.B), dim3(kSampThreads), st, mp, meta));
+        else k_locate<<<pl.B, kSampThreads, 0, st>>>(mp, meta);
         NJ_LAUNCHED(c, "k_locate", st);
     } else {
         NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));

@@ -45,6 +45,17 @@ __device__ __forceinline__ void copy_row(uint16_t* dst, const uint16_t* src, int
 }
 
 // gather the draft rows of hidden into a contiguous [G, d] buffer (block per row)
+// Programmatic dependent launch: every sampler kernel first waits for its
+// predecessor grid (a no-op unless launched with the PDL attribute), then lets
+// its own successor be scheduled, which waits in turn -- so each launch's ramp
+// overlaps the previous kernel instead of following its drain.  The wait comes
+// before any global access in EVERY CTA, so a grid never completes before its
+// predecessor (the chain stays transitive).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void k_gather_drafts(const uint16_t* __restrict__ hidden, int d, const ReqMeta m,
                                 uint16_t* __restrict__ out) {
     const int g = blockIdx.x;
@@ -126,6 +137,7 @@ __device__ __forceinline__ double xmerge_lse(const double* xr, int nranks, int l
 // K-B: warp per request — lse of its draft rows, acceptance tests, first
 // rejection, sample-row bookkeeping, and the copy of the sample hidden row.
 __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
+    pdl_enter();
     const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     if (b >= m.B) return;
     const int lane = (int)lane_id();
@@ -186,6 +198,7 @@ __global__ void k_accept(const AcceptParams p, const ReqMeta m) {
 
 __global__ void k_lse_rows(const float* __restrict__ pm, const float* __restrict__ ps, int pld, int grid, int n,
                            double* __restrict__ out) {
+    pdl_enter();
     const int r = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     if (r >= n) return;
     const double l = warp_lse(pm, ps, pld, r, grid);
@@ -326,6 +339,7 @@ __device__ __forceinline__ float chunk_weight(const MassParams& p, const float* 
 // two-pass path's K-C statistics), merged once per request so that k_mass's
 // items and k_locate read one value.  Warp per request.
 __global__ void k_sample_lse(const MassParams p, int B, double* s_lse) {   // s_lse == p.s_lse
+    pdl_enter();
     const int b = blockIdx.x * (blockDim.x / 32) + (int)warp_id();
     if (b >= B) return;
     if (!isnan(__ldcg(&p.s_lse[b]))) return;
@@ -386,6 +400,7 @@ __device__ __forceinline__ void mass_copy_chunk(float* dst, const float* src, in
 
 template <int NST>
 __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B) {
+    pdl_enter();
     extern __shared__ __align__(16) float ring[];   // NST x {logits[kChunk], q[kChunk]}, then the request table
     __shared__ float wt[kSubTiles][8];
     __shared__ double sst[kSubTiles];
@@ -872,6 +887,7 @@ __global__ void k_greedy_decide(const ReqMeta m, const int32_t* __restrict__ dra
 // ranks see it identically after X2 and draw from p_n instead: the masses are
 // exp(lse_r(n) - M), and the owner recomputes its p_n chunk masses here.
 __global__ void __launch_bounds__(kSampThreads) k_locate(const MassParams p, const ReqMeta m) {
+    pdl_enter();
     const int b = blockIdx.x;
     const double lse = sample_lse(p, b);
     const bool resid0 = p.s_resid[b] != 0;
