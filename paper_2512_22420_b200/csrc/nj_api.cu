@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -157,6 +157,7 @@ Knobs read_knobs() {
     k.small_reuse = env_int("NJ_SMALL_REUSE", 1);   // owner CTA reads the located chunk from its staging buffer
     k.small_cl = env_int("NJ_SMALL_CL", 0);
     k.qstage_gbs = env_int("NJ_QSTAGE_GBS", 50);
+    k.small_flat = env_int("NJ_SMALL_FLAT", 1);     // k_sample_small<FLAT> (no cluster, PDL dependent of k_lmhead)
     k.pdl_chain = env_int("NJ_PDL_CHAIN", 0);       // staged multi-kernel sampler as a PDL chain (no gain measured:
                                                     // B = 16 / 64 / 256 equal within the box's noise)    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
@@ -223,7 +224,7 @@ struct nj_ctx {
     float* logits_s = nullptr;
     float* logits_st = nullptr;    // staged path: [staged_rows][V_local]
     int32_t *s_resid = nullptr, *s_qrow = nullptr;
-    int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags
+    int32_t* fb_block = nullptr;   // [0] count, [1..MB] list, [1+MB..] req_flags, [1+2MB..] k_sample_small<FLAT> arrivals
     uint32_t* bar = nullptr;       // count, gen
     int32_t* fb_done = nullptr;    // k_fb completion counter
     unsigned long long* amax = nullptr;   // nj_verify_greedy: per-row argmax keys [Nmax]
@@ -269,6 +270,7 @@ struct nj_ctx {
     int32_t* fb_count() { return fb_block; }
     int32_t* fb_list() { return fb_block + 1; }
     int32_t* req_flags() { return fb_block + 1 + cfg.max_batch; }
+    int32_t* small_cnt() { return fb_block + 1 + 2 * cfg.max_batch; }
 };
 
 namespace {
@@ -448,12 +450,19 @@ int small_sampler_cl(const nj_ctx* c, int B) {
 int small_pb_for(int nchunks, int cl) {   // chunks per staged batch (two buffers)
     return std::max(1, std::min(3, (nchunks + cl - 1) / cl));
 }
-int small_sampler_pb(const nj_ctx* c, int B) { return small_pb_for(c->nchunks, small_sampler_cl(c, B)); }
+// NJ_SMALL_FLAT: k_sample_small<FLAT> -- no cluster, num_sms / B CTAs per request (<= 32),
+// chunk masses exchanged through global memory, the request's last CTA draws; launched as
+// a programmatic dependent of k_lmhead (which then triggers at its start), so its CTAs
+// take the SMs the GEMM's CTAs free during the GEMM's tail
+int small_flat_cpr(const nj_ctx* c, int B) { return std::max(1, std::min(32, c->num_sms / std::max(B, 1))); }
+bool small_flat_on(const nj_ctx* c) { return c->kn.small_flat && c->kn.small_cl == 0; }   // NJ_SMALL_CL: clusters
+int small_sampler_ctas(const nj_ctx* c, int B) { return small_flat_on(c) ? small_flat_cpr(c, B) : small_sampler_cl(c, B); }
+int small_sampler_pb(const nj_ctx* c, int B) { return small_pb_for(c->nchunks, small_sampler_ctas(c, B)); }
 size_t small_sampler_smem(const nj_ctx* c, int B) {   // two batch buffers of logits + q chunks
     return (size_t)2 * small_sampler_pb(c, B) * 2 * kChunk * sizeof(float);
 }
 bool small_sampler_ok(const nj_ctx* c, const Plan& pl) {
-    const int cl = small_sampler_cl(c, pl.B);
+    const int cl = small_sampler_ctas(c, pl.B);
     return c->kn.small && pl.path == NJ_PATH_STAGED && !c->sharded() && pl.B <= c->kn.small_bmax &&
            pl.B * cl <= c->num_sms && c->nchunks <= kSmallMaxChunks && c->cfg.gamma_max + 1 <= kSmallMaxRows &&
            small_sampler_smem(c, pl.B) <= 200 * 1024;
@@ -718,7 +727,7 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.sleep_ns = c->kn.lm_sleep;
     p.fence_full = c->kn.lm_fence;
     p.mma4 = c->kn.lm_mma4;
-    p.pdl = c->kn.lm_pdl;
+    p.pdl = (c->kn.lm_pdl || p.pdl) ? 1 : 0;   // the caller asks for it when a PDL dependent follows
     p.dbg = c->kn.lm_dbg;
     p.ts = nullptr;
     if (c->kn.phase_ts) {
@@ -1026,6 +1035,7 @@ nj_status shard_phase(nj_ctx* c, cudaStream_t st, ShardCall& a, int ph) {
             lp.part_m = c->part_m; lp.part_s = c->part_s;
             lp.tok = a.tok; lp.dl = c->dl;
             lp.cap_staged = 1;
+            lp.pdl = (small_flat_on(c) && small_sampler_ok(c, pl)) ? 1 : 0;   // k_sample_small<FLAT> follows
             lp.B = pl.B;
             for (int b = 0; b <= pl.B; ++b) lp.row_off[b] = pl.row_off[b];
             std::pair<cudaEvent_t, cudaEvent_t> ev;
@@ -1289,7 +1299,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     A(logits_st, (size_t)c->staged_rows * c->V_local);
     A(s_resid, (size_t)MB);
     A(s_qrow, (size_t)MB);
-    A(fb_block, (size_t)1 + 2 * MB);
+    A(fb_block, (size_t)1 + 3 * MB);
     A(bar, 2);
     A(fb_done, 1);
     A(scratch_i, (size_t)MB);
@@ -1299,7 +1309,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
 #undef A
     if (c->ncomm && (s = alloc_shard_ws(c)) != NJ_OK) { nj_destroy(c); return s; }
     if (cudaMemset(c->bar, 0, 2 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(c->fb_done, 0, sizeof(int32_t)) != cudaSuccess ||
-        cudaMemset(c->fb_block, 0, (1 + 2 * MB) * sizeof(int32_t)) != cudaSuccess) {
+        cudaMemset(c->fb_block, 0, (1 + 3 * MB) * sizeof(int32_t)) != cudaSuccess) {
         nj_destroy(c);
         return set_err(nullptr, NJ_ECUDA, "cudaMemset failed");
     }
@@ -1318,8 +1328,9 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 1>);
     e = e ? e : set_smem_attr(k_lmhead<LM_WRITE | LM_STATS, 2>);
     e = e ? e : set_smem_attr(k_lmhead<LM_ARGMAX, 1>);
-    e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    e = e ? e : cudaFuncSetAttribute(k_sample_small, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = e ? e : cudaFuncSetAttribute(k_sample_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    e = e ? e : cudaFuncSetAttribute(k_sample_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    e = e ? e : cudaFuncSetAttribute(k_sample_small<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     for (int cl : {2, 4, 8, 12, 16}) {
         if (e) break;
         cudaLaunchConfig_t oc = {};
@@ -1334,7 +1345,7 @@ nj_status nj_create(const nj_config* cfg, nj_ctx** out) {
         oc.attrs = oa;
         oc.numAttrs = 1;
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k_sample_small, &oc) == cudaSuccess) c->small_maxcl[cl] = n;
+        if (cudaOccupancyMaxActiveClusters(&n, k_sample_small<false>, &oc) == cudaSuccess) c->small_maxcl[cl] = n;
         else (void)cudaGetLastError();   // unknown: keep the measured default size
     }
     if (getenv("NJ_SMALL_INFO"))
@@ -1495,7 +1506,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
     } else if (pl.path == NJ_PATH_STAGED) {
         // one GEMM pass over all N rows: per-row stats, draft-logit capture, and every
         // row's fp32 logits stored with an L2 evict_last policy (W streams evict_first)
-        NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 2 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
+        NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 3 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
         if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
         GemmBigParams gp{};
         gp.logits = c->logits_st; gp.ld_out = c->V_local;
@@ -1517,6 +1528,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             lp.part_m = c->part_m; lp.part_s = c->part_s;
             lp.tok = draft_tokens; lp.dl = c->dl;
             lp.cap_staged = 1;
+            lp.pdl = (small_flat_on(c) && small_sampler_ok(c, pl)) ? 1 : 0;   // k_sample_small<FLAT> follows
             lp.B = pl.B;
             for (int b = 0; b <= pl.B; ++b) lp.row_off[b] = pl.row_off[b];
             // small batches: the q rows into L2 during the GEMM (the sampler reads the rejected
@@ -1551,12 +1563,8 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             mp.dbg_lse = dbg ? dbg->lse : nullptr;
             mp.certify = certify; mp.eps_draw = c->eps_draw;
             mp.small_pb = small_sampler_pb(c, pl.B);
-            mp.ts = nullptr;
-            if (c->kn.phase_ts) {
-                if (!c->phase_ts) NJ_CUDA(c, cudaMalloc(&c->phase_ts, kPhaseTsN * sizeof(unsigned long long)));
-                NJ_CUDA(c, cudaMemsetAsync(c->phase_ts + 18432, 0, 2048 * sizeof(unsigned long long), st));
-                mp.ts = c->phase_ts;
-            }
+            mp.ts = c->kn.phase_ts ? c->phase_ts : nullptr;   // cleared with k_lmhead's stamps (a memset
+                                                                  // here would break the PDL edge)
             mp.pdl_trigger = c->kn.small_trig;
             mp.small_reuse = c->kn.small_reuse;
             if (c->qstage_active) {
@@ -1565,8 +1573,19 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
                 mp.q_loc = c->st_q;
                 for (int i = 0; i < 4; ++i) mp.q_loc_mask[i] = c->qstage_mask[i];
             }
-            mp.pf_rows = c->kn.small_pf && !c->q_remote && (ldq & 3) == 0 && (c->V_local & 3) == 0 &&
-                         (reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0;
+            // NJ_SMALL_PF: 1 candidate logits + q rows into L2 after the wait, 2 (flat sampler) the
+            // candidate q rows before it (device-resident q of a 16-byte-aligned pitch only)
+            mp.pf_rows = (!c->q_remote && (ldq & 3) == 0 && (c->V_local & 3) == 0 &&
+                          (reinterpret_cast<uintptr_t>(draft_probs) & 15) == 0) ? c->kn.small_pf : 0;
+            if (small_flat_on(c)) {
+                mp.flat_cpr = small_flat_cpr(c, pl.B);
+                mp.cm_glob = c->cmass;
+                mp.cm_cnt = c->small_cnt();
+                NJ_CUDA(c, launch_pdl_smem(k_sample_small<true>, dim3(pl.B * mp.flat_cpr), dim3(kSampThreads),
+                                           small_sampler_smem(c, pl.B), st, ap, mp, meta));
+                NJ_LAUNCHED(c, "k_sample_small", st);
+                goto fallback;
+            }
             cudaLaunchConfig_t cfg = {};
             const int cl = small_sampler_cl(c, pl.B);
             cfg.gridDim = dim3(pl.B * cl);
@@ -1582,7 +1601,7 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             at[1].val.programmaticStreamSerializationAllowed = c->kn.small_pdl ? 1 : 0;
             cfg.attrs = at;
             cfg.numAttrs = 2;
-            NJ_CUDA(c, cudaLaunchKernelEx(&cfg, k_sample_small, ap, mp, meta));
+            NJ_CUDA(c, cudaLaunchKernelEx(&cfg, k_sample_small<false>, ap, mp, meta));
             NJ_LAUNCHED(c, "k_sample_small", st);
             goto fallback;
         }

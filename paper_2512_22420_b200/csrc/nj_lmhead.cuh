@@ -157,7 +157,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     const int nitems = rg.ntile;   // item it: tile it of the range, chunk cfix
     const int ngk = (p.num_kb + GK - 1) / GK;
 
-    if (p.pdl && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // every thread
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmW);
         tma_prefetch_desc(&tmH);

@@ -255,6 +255,12 @@ struct MassParams {
     // q_loc (same pitch ldq) while the GEMM ran; the others are read in place (q)
     const float* q_loc;
     uint64_t q_loc_mask[4];
+    // k_sample_small<FLAT = true>: CTAs per request (no cluster); chunk masses go through
+    // global memory (cm_glob[b][nchunks]) and a per-request arrival barrier (cm_cnt[b],
+    // zeroed before every call)
+    int32_t flat_cpr;
+    double* cm_glob;
+    int32_t* cm_cnt;
     const float* q;
     int64_t ldq;
     const float* u;        // final-draw uniform of request b at u[row_off[b]+gamma_b] (or u[b] in stage mode)
@@ -493,13 +499,17 @@ __global__ void __launch_bounds__(kSampThreads) k_mass(const MassParams p, int B
     }
     cp_async_wait_all();
 }
-// Small-batch staged sampler (unsharded staged path, B * kSmallCl <= SMs): the
-// acceptance tests (K-B), the chunk masses (K-D1) and the draw (K-D2) of request
-// b in ONE launch by a cluster of kSmallCl CTAs -- the request's chunks dealt over
-// the cluster, chunk masses exchanged through distributed shared memory.  The
-// arithmetic and its order are k_accept's, k_mass's and k_locate's (bit-identical
-// decisions, masses and draws); only the launches and the global round trips
-// between them are gone (~20 us of a ~205 us step at C2).
+// Small-batch staged sampler (unsharded staged path, B * CTAs per request <= SMs):
+// the acceptance tests (K-B), the chunk masses (K-D1) and the draw (K-D2) of
+// request b in ONE launch by CL CTAs -- the request's chunks dealt over them.
+// FLAT (default): num_sms / B CTAs per request, no cluster, chunk masses through
+// global memory and a per-request arrival barrier; launched as a programmatic
+// dependent of k_lmhead, so its CTAs take the SMs the GEMM's CTAs free during the
+// GEMM's tail and read the inputs the GEMM does not produce (q_i(x_i), u_i) before
+// griddepcontrol.wait (C2 208.3-209.3 -> 204.4-205.1 us/step).
+// !FLAT: a cluster of 16 / 12 / 8 / ... CTAs per request, chunk masses exchanged
+// through distributed shared memory.  The arithmetic and its order are k_accept's,
+// k_mass's and k_locate's (bit-identical decisions, masses and draws in both modes).
 constexpr int kSmallCl = 8;         // CTAs per request (16 when B <= 8: one cluster per GPC)
 constexpr int kSmallMaxPerCta = 4;  // chunks per staged batch (two batch buffers of <= 3 x 32 KB)
 constexpr int kSmallMaxChunks = 64;
@@ -508,26 +518,46 @@ __device__ __forceinline__ const float* small_q_row(const MassParams& p, int g) 
     return (p.q_loc && ((p.q_loc_mask[g >> 6] >> (g & 63)) & 1ull)) ? p.q_loc + (int64_t)g * p.ldq
                                                                       : p.q + (int64_t)g * p.ldq;
 }
+template <bool FLAT>
 __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParams ap, const MassParams p,
                                                                const ReqMeta m) {
     // launched with programmatic dependent launch: the CTAs start on SMs the GEMM's
     // finished CTAs free, then wait here for the whole GEMM grid and its writes
     if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 0] = globaltimer();
+    // FLAT: flat_cpr CTAs per request without a cluster (a PDL dependent can then be
+    // scheduled on the SMs the GEMM's CTAs free during its tail)
+    const int b = FLAT ? (int)blockIdx.x / p.flat_cpr : (int)cluster_id_x();
+    const int rank = FLAT ? (int)blockIdx.x - b * p.flat_cpr : (int)cluster_ctarank();
+    const int CL = FLAT ? p.flat_cpr : (int)cluster_nctarank();   // CTAs per request
+    const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
+    // inputs of the acceptance tests that the GEMM does not produce (q_i(x_i), u_i) are
+    // read before the wait, while the GEMM's tail still runs
+    double qx_pre = 0.0, u_pre = 0.0;
+    if (warp_id() == 0 && (int)lane_id() < gam) {
+        const int g = g0 + (int)lane_id();
+        qx_pre = (double)small_q_row(p, g)[ap.draft_tokens[g]];
+        u_pre = (double)ap.u[ro + (int)lane_id()];
+    }
+    // optional: this CTA's chunks of every candidate q row into L2 before the wait
+    if (FLAT && p.pf_rows == 2 && threadIdx.x < 32) {
+        const int c = rank + (int)(threadIdx.x >> 2) * CL;
+        if (c < p.nchunks) {
+            const int x0 = c * kChunk, nn = min(kChunk, p.V_local - x0) & ~3;
+            for (int i = (int)(threadIdx.x & 3); i < gam; i += 4)
+                bulk_prefetch_l2(small_q_row(p, g0 + i) + p.v_begin + x0, (uint32_t)nn * 4u);
+        }
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 1] = globaltimer();
 
     // let the fp64 fallback kernel (launched next with programmatic serialization) be
     // scheduled now: it waits in its own griddepcontrol.wait for this grid to finish
     if (p.pdl_trigger && threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int b = (int)cluster_id_x();
-    const int rank = (int)cluster_ctarank();
-    const int CL = (int)cluster_nctarank();   // 8 or 16 CTAs per request
-    const int ro = m.row_off[b], gam = m.row_off[b + 1] - ro - 1, g0 = ro - b;
     __shared__ double s_lrow[kSmallMaxRows];
     __shared__ int s_n;
     // every candidate sample row's (and its q row's) chunks of this CTA into L2 while
     // the acceptance tests run; the staging after them then hits L2
-    if (p.pf_rows && threadIdx.x < 32) {
+    if (p.pf_rows == 1 && threadIdx.x < 32) {
         const int c = rank + (int)(threadIdx.x >> 2) * CL;   // lanes: (chunk slot, 4 rows each)
         if (c < p.nchunks) {
             const int x0 = c * kChunk, nn = min(kChunk, p.V_local - x0) & ~3;
@@ -564,8 +594,7 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
             const int g = g0 + lane;
             const double lse = s_lrow[lane], dlv = __ldcg(&ap.dl[g]);
             pd = exp(dlv - lse);
-            const double qx = (double)small_q_row(p, g)[ap.draft_tokens[g]];
-            const double uq = (double)ap.u[ro + lane] * qx;
+            const double uq = u_pre * qx_pre;   // u_i * q_i(x_i), read before the wait
             near = fabs(uq - pd) <= (double)ap.eps_acc * pd;
             fail = !(uq < pd);
         }
@@ -660,13 +689,37 @@ __global__ void __launch_bounds__(kSampThreads) k_sample_small(const AcceptParam
     // (4) every chunk mass from the CTA that owns it (distributed shared memory); the
     //     second cluster barrier keeps each CTA's cml alive until all have read it
     if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 4] = globaltimer();
-    cluster_sync_all();
-    if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 5] = globaltimer();
-
-    for (int c = threadIdx.x; c < p.nchunks; c += kSampThreads)
-        cm[c] = ld_shared_cluster_f64(mapa_shared(&cml[c], (uint32_t)(c % CL)));
-    __syncthreads();
-    cluster_sync_all();
+    if constexpr (FLAT) {
+        // this CTA's chunk masses to global memory, then a barrier over the request's
+        // CTAs (arrival counter, zeroed by the call's fb_block memset; all B x CL CTAs are
+        // co-resident once the GEMM's CTAs have exited, B x CL <= SMs), then every CTA
+        // reads all masses, so the owner of the located chunk draws from its staging buffer
+        for (int j = threadIdx.x; j < nmine; j += kSampThreads) {
+            const int c = rank + j * CL;
+            p.cm_glob[(int64_t)b * p.nchunks + c] = cml[c];
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            atomicAdd(&p.cm_cnt[b], 1);
+            const long long t0 = clock64();
+            while ((int)ld_acquire_gpu(reinterpret_cast<const uint32_t*>(&p.cm_cnt[b])) < CL) {
+                __nanosleep(20);
+                watchdog(t0);
+            }
+        }
+        __syncthreads();
+        if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 5] = globaltimer();
+        for (int c = threadIdx.x; c < p.nchunks; c += kSampThreads) cm[c] = __ldcg(&p.cm_glob[(int64_t)b * p.nchunks + c]);
+        __syncthreads();
+    } else {
+        cluster_sync_all();
+        if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 5] = globaltimer();
+        for (int c = threadIdx.x; c < p.nchunks; c += kSampThreads)
+            cm[c] = ld_shared_cluster_f64(mapa_shared(&cml[c], (uint32_t)(c % CL)));
+        __syncthreads();
+        cluster_sync_all();
+    }
     if (p.ts && threadIdx.x == 0 && blockIdx.x < 128) p.ts[18432 + blockIdx.x * 16 + 6] = globaltimer();
     // (5) the draw: k_locate's unsharded arithmetic; the CTA owning the located chunk finishes
     if (threadIdx.x == 0) {
