@@ -149,7 +149,11 @@ Knobs read_knobs() {
     k.small_cl16 = env_int("NJ_SMALL_CL16", 1);
     k.small_pf = env_int("NJ_SMALL_PF", 0);          // measured slower (C2 204.7 vs 200.5 us)
     k.lm_sleep = env_int("NJ_LM_SLEEP", 0);
-    k.small_bmax = env_int("NJ_SMALL_BMAX", 12);
+    k.small_flat = env_int("NJ_SMALL_FLAT", 1);     // k_sample_small<FLAT> (no cluster, PDL dependent of k_lmhead)
+    // batch limit of the one-launch sampler: flat mode beats the multi-kernel sampler up to
+    // B = 32 (sweep at gamma 2 / 3: -2..-4 % at B = 16-24, -1 % at 32, +1 % at 40-48), the
+    // cluster mode up to 12
+    k.small_bmax = env_int("NJ_SMALL_BMAX", k.small_flat ? 32 : 12);
     k.inline_lse = env_int("NJ_INLINE_LSE", kInlineLseRows);
     k.lm_pdl = env_int("NJ_LM_PDL", 0);             // k_lmhead triggers its dependents' launch at its start:
                                                     // k_sample_small still starts ~4 us after the last GEMM CTA (no gain)
@@ -157,7 +161,6 @@ Knobs read_knobs() {
     k.small_reuse = env_int("NJ_SMALL_REUSE", 1);   // owner CTA reads the located chunk from its staging buffer
     k.small_cl = env_int("NJ_SMALL_CL", 0);
     k.qstage_gbs = env_int("NJ_QSTAGE_GBS", 50);
-    k.small_flat = env_int("NJ_SMALL_FLAT", 1);     // k_sample_small<FLAT> (no cluster, PDL dependent of k_lmhead)
     k.pdl_chain = env_int("NJ_PDL_CHAIN", 0);       // staged multi-kernel sampler as a PDL chain (no gain measured:
                                                     // B = 16 / 64 / 256 equal within the box's noise)    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches

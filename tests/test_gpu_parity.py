@@ -500,13 +500,14 @@ def test_strided_misaligned_draft_probs(path):
         check(b, acc, nxt, dd)
 
 
-@pytest.mark.parametrize("B,g", [(8, 3), (12, "mixed:5")])
+@pytest.mark.parametrize("B,g", [(8, 3), (12, "mixed:5"), (32, 2)])
 def test_small_sampler_cluster_sizes(B, g, monkeypatch):
-    """k_sample_small with every cluster size (16 / 12 / 8 / 4 / 2 CTAs per request:
-    one to seven staged chunk batches per CTA) and with the owner CTA reading the
-    located chunk from its staging buffer or from global memory: bit-identical
-    decisions, masses and tokens (same expressions and reduction order as
-    k_accept / k_mass / k_locate), and the default launch vs the oracle."""
+    """k_sample_small in its default flat mode (num_sms / B CTAs per request, no
+    cluster) and with every cluster size (16 / 12 / 8 / 4 / 2 CTAs per request: one
+    to seven staged chunk batches per CTA), the owner CTA reading the located chunk
+    from its staging buffer or from global memory: bit-identical decisions, masses
+    and tokens (same expressions and reduction order as k_accept / k_mass /
+    k_locate), and the default launch vs the oracle."""
     b = make_batch(B, g, V=QV, d=QD, seed=B + 71, device=DEV, W=w_full())
     ref = None
     for cl in (0, 16, 12, 8, 4, 2):
