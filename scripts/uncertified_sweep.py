@@ -1,7 +1,8 @@
 """Raw decision accuracy of the CUDA path with the certificate OFF, at the
 bench shapes: >= 10^4 Qwen-shape requests (B = 256, gamma = 5; B = 64,
-gamma = 3; B = 8, gamma = 3 on the AUTO path -- the staged k_lmhead step since
-round 2's second session -- and B = 8, gamma = 3 on the fused kernel) against
+gamma = 3; B = 24, gamma = 3 and B = 8, gamma = 3 on the AUTO path -- the staged
+k_lmhead step with the flat one-launch sampler -- and B = 8, gamma = 3 on the
+fused kernel) against
 the fp64 oracle.  Counts
 out-of-band mismatches (must be 0), ties (oracle band 1e-6) and excused
 requests that took the other tie branch.  Writes one JSON summary.
@@ -34,6 +35,7 @@ W64 = oracle.weight_f64(oracle.bf16_bits(W))
 summary = {}
 t0 = time.time()
 for (B, g, nb, fp) in [(256, 5, a.batches, NJ_PATH_AUTO), (64, 3, a.batches, NJ_PATH_AUTO),
+                      (24, 3, 2 * a.batches, NJ_PATH_AUTO),   # the flat one-launch sampler's range
                       (8, 3, 4 * a.batches, NJ_PATH_AUTO), (8, 3, 2 * a.batches, NJ_PATH_FUSED)]:
     v = Verifier(d, V, max_batch=B, gamma_max=5)
     v.set_option(NJ_OPT_CERTIFY, 0)
