@@ -1152,6 +1152,32 @@ def bench_sweep(args, ws, rank, local):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.steps
             kms, kn = v.kernel_time(True)
+            v.set_option(NJ_OPT_PROFILE, 0)
+            # the same step replayed from a CUDA graph (the bench lines' launch mode)
+            ms_graph = None
+            if not args.no_graph:
+                try:
+                    cap = torch.cuda.Stream()
+                    cap.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(cap):
+                        v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+                        cap.synchronize()
+                        gr = torch.cuda.CUDAGraph()
+                        with torch.cuda.graph(gr, stream=cap):
+                            v.verify(b.hidden, W, b.draft_tokens, b.draft_probs, b.gamma, b.uniforms, acc, nxt)
+                    torch.cuda.current_stream().wait_stream(cap)
+                    for _ in range(3):
+                        gr.replay()
+                    torch.cuda.synchronize()
+                    e0.record()
+                    for _ in range(args.steps):
+                        gr.replay()
+                    e1.record()
+                    torch.cuda.synchronize()
+                    ms_graph = e0.elapsed_time(e1) / args.steps
+                    del gr
+                except Exception as e:   # noqa: BLE001
+                    print(f"[bench] sweep graph timing skipped: {e}", file=sys.stderr)
             toks = int((acc + 1).sum().item())
             N = b.N
             t_star = max(2.0 * N * V_Q * D_Q / (tf_burst * 1e12), (2.0 * V_Q * D_Q + 2 * N * D_Q) / (hbm * 1e9))
@@ -1161,6 +1187,9 @@ def bench_sweep(args, ws, rank, local):
                               "accepted_tokens_per_s": toks / (ms / 1e3), "roofline_us": t_star * 1e6,
                               "frac_of_roofline": t_star / (ms / 1e3), "roofline_us_sustained": t_sus * 1e6,
                               "frac_of_roofline_sustained": t_sus / (ms / 1e3),
+                              "us_per_step_graph": ms_graph * 1e3 if ms_graph else None,
+                              "frac_of_roofline_graph": t_star / (ms_graph / 1e3) if ms_graph else None,
+                              "frac_of_roofline_sustained_graph": t_sus / (ms_graph / 1e3) if ms_graph else None,
                               "dominant_kernel_us": kms / max(kn, 1) * 1e3,
                               "launches": launches})
             del v
