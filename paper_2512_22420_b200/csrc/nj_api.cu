@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1, hostq_fused = 0;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -161,6 +161,11 @@ Knobs read_knobs() {
     k.small_reuse = env_int("NJ_SMALL_REUSE", 1);   // owner CTA reads the located chunk from its staging buffer
     k.small_cl = env_int("NJ_SMALL_CL", 0);
     k.qstage_gbs = env_int("NJ_QSTAGE_GBS", 50);
+    // host-resident q (nj_verify_host): 1 = the fused kernel up to 48 rows; 0 (default) = the
+    // device-q rule -- the staged step above 24 rows, whose flat sampler reads q_i(x_i) during
+    // the GEMM's tail and the rejected rows' chunks from ~144 CTAs at once (e2e +13..19 % at
+    // B = 8-16, scripts/e2e_path.py)
+    k.hostq_fused = env_int("NJ_HOSTQ_FUSED", 0);
     k.pdl_chain = env_int("NJ_PDL_CHAIN", 0);       // staged multi-kernel sampler as a PDL chain (no gain measured:
                                                     // B = 16 / 64 / 256 equal within the box's noise)    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
@@ -421,7 +426,8 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
         // N = 4 fused 193 vs 203 us)
         // q read in place from host memory (nj_verify_host, zero-copy): the fused kernel's
         // all-in-flight async copies of the rejected rows beat the staged sampler's
-        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm || (c->q_remote && !c->qstage_active)))
+        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm ||
+                             (c->q_remote && !c->qstage_active && c->kn.hostq_fused)))
                    ? NJ_PATH_FUSED
                : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
