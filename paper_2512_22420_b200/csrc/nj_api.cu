@@ -424,10 +424,14 @@ nj_status make_plan(nj_ctx* c, const int32_t* gamma, int32_t B, Plan& pl) {
         // fused for the smallest batches only: above kFusedAutoMaxN rows k_lmhead + the sampler
         // kernels are faster (B200: N = 32 203-208 vs 207-210 us, N = 48 210-215 vs 240-248 us;
         // N = 4 fused 193 vs 203 us)
-        // q read in place from host memory (nj_verify_host, zero-copy): the fused kernel's
-        // all-in-flight async copies of the rejected rows beat the staged sampler's
-        path = (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm ||
-                             (c->q_remote && !c->qstage_active && c->kn.hostq_fused)))
+        // q read in place from host memory (nj_verify_host, zero-copy): the staged step at
+        // every size (its flat sampler reads q_i(x_i) during the GEMM's tail and a rejected
+        // row's chunks from ~144 CTAs at once: N = 4 / 16 / 24 / 32 266 / 296 / 309 / 314 us
+        // per call vs the fused kernel's 278 / 335 / 351 / 354, scripts/e2e_*path.py);
+        // NJ_HOSTQ_FUSED=1: the fused kernel up to 48 rows (round-2 second session's rule)
+        path = (c->q_remote && !c->kn.hostq_fused && staged_ok && c->kn.lm) ? NJ_PATH_STAGED
+               : (fused_ok && (pl.N <= kFusedAutoMaxN || !staged_ok || !c->kn.lm ||
+                               (c->q_remote && !c->qstage_active && c->kn.hostq_fused)))
                    ? NJ_PATH_FUSED
                : (staged_ok && staged_pays) ? NJ_PATH_STAGED : NJ_PATH_TWOPASS;
     if (path == NJ_PATH_FUSED && !fused_ok)
