@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1, hostq_fused = 0;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1, hostq_fused = 0, small_coop = 1;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -166,6 +166,7 @@ Knobs read_knobs() {
     // the GEMM's tail and the rejected rows' chunks from ~144 CTAs at once (e2e +13..19 % at
     // B = 8-16, scripts/e2e_path.py)
     k.hostq_fused = env_int("NJ_HOSTQ_FUSED", 0);
+    k.small_coop = env_int("NJ_SMALL_COOP", 1);     // flat sampler launched cooperatively (co-residency guaranteed)
     k.pdl_chain = env_int("NJ_PDL_CHAIN", 0);       // staged multi-kernel sampler as a PDL chain (no gain measured:
                                                     // B = 16 / 64 / 256 equal within the box's noise)    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
     k.small_trig = env_int("NJ_SMALL_TRIG", 0);   // early PDL trigger of the fallback launch (no gain measured)   // larger B: 2-4 CTA clusters measured slower than the 4-5 launches
@@ -1594,8 +1595,26 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
                 mp.flat_cpr = small_flat_cpr(c, pl.B);
                 mp.cm_glob = c->cmass;
                 mp.cm_cnt = c->small_cnt();
-                NJ_CUDA(c, launch_pdl_smem(k_sample_small<true>, dim3(pl.B * mp.flat_cpr), dim3(kSampThreads),
-                                           small_sampler_smem(c, pl.B), st, ap, mp, meta));
+                if (c->kn.small_coop) {
+                    // cooperative: the runtime guarantees the B x CL CTAs are co-resident (the
+                    // per-request barrier of the flat mode relies on it); PDL as above
+                    cudaLaunchConfig_t cfg = {};
+                    cfg.gridDim = dim3(pl.B * mp.flat_cpr);
+                    cfg.blockDim = dim3(kSampThreads);
+                    cfg.dynamicSmemBytes = small_sampler_smem(c, pl.B);
+                    cfg.stream = st;
+                    cudaLaunchAttribute at[2];
+                    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                    at[0].val.programmaticStreamSerializationAllowed = 1;
+                    at[1].id = cudaLaunchAttributeCooperative;
+                    at[1].val.cooperative = 1;
+                    cfg.attrs = at;
+                    cfg.numAttrs = 2;
+                    NJ_CUDA(c, cudaLaunchKernelEx(&cfg, k_sample_small<true>, ap, mp, meta));
+                } else {
+                    NJ_CUDA(c, launch_pdl_smem(k_sample_small<true>, dim3(pl.B * mp.flat_cpr), dim3(kSampThreads),
+                                               small_sampler_smem(c, pl.B), st, ap, mp, meta));
+                }
                 NJ_LAUNCHED(c, "k_sample_small", st);
                 goto fallback;
             }
