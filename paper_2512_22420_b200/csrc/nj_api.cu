@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1, hostq_fused = 0, small_coop = 1;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1, hostq_fused = 0, small_coop = 1, lm_out_keep = 0;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -166,6 +166,7 @@ Knobs read_knobs() {
     // the GEMM's tail and the rejected rows' chunks from ~144 CTAs at once (e2e +13..19 % at
     // B = 8-16, scripts/e2e_path.py)
     k.hostq_fused = env_int("NJ_HOSTQ_FUSED", 0);
+    k.lm_out_keep = env_int("NJ_LM_OUT_KEEP", 0);   // evict_last hint on small staged logits stores
     k.small_coop = env_int("NJ_SMALL_COOP", 1);     // flat sampler launched cooperatively (co-residency guaranteed)
     k.pdl_chain = env_int("NJ_PDL_CHAIN", 0);       // staged multi-kernel sampler as a PDL chain (no gain measured:
                                                     // B = 16 / 64 / 256 equal within the box's noise)    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
@@ -742,6 +743,9 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     p.fence_full = c->kn.lm_fence;
     p.mma4 = c->kn.lm_mma4;
     p.pdl = (c->kn.lm_pdl || p.pdl) ? 1 : 0;   // the caller asks for it when a PDL dependent follows
+    // NJ_LM_OUT_KEEP: the staged logits of a one-chunk launch (R <= 128 rows, <= 78 MB) stored with
+    // an L2 evict_last hint so that the sampler's re-read hits L2
+    p.out_keep = (c->kn.lm_out_keep && pl.nchunks == 1 && CG == 1) ? 1 : 0;
     p.dbg = c->kn.lm_dbg;
     p.ts = nullptr;
     if (c->kn.phase_ts) {

@@ -57,6 +57,8 @@ struct LmheadParams {
     int32_t arv1;                // 1: one accumulator-release arrival per CTA (named barrier first)
     int32_t fence_full;          // probe: tcgen05.fence::after_thread_sync after every operand wait
     int32_t mma4;                // 1: a k-block's four MMAs issued from one asm block under one elect
+    int32_t out_keep;            // 1: TMA logits stores with an L2 evict_last hint (small R: the sampler
+                                 //    re-reads them right after; W streams evict_first)
     int32_t pdl;                 // 1: trigger the dependent grid's launch at the start (k_sample_small's
                                  //    CTAs take the SMs this grid's CTAs free; they wait for its writes)
     int32_t nbuf, bstride;       // TMEM accumulator buffers and their column stride
@@ -369,6 +371,7 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
         const bool quad_empty = cfix * kLmTok * CG + crank * kLmTok + q * 32 >= p.R;
         const int ngroups = p.num_kb <= p.ks0 ? 1 : 1 + (p.num_kb - p.ks0 + p.ks - 1) / p.ks;
         const uint64_t pol_out = policy_evict_first();   // logits: do not push W / H out of L2
+        const uint64_t pol_keep = policy_evict_last();   // out_keep: small staged logits stay for the sampler
         const bool vec_ok = (p.ld_out & 3) == 0 && (reinterpret_cast<uintptr_t>(p.logits) & 15) == 0;
         uint8_t* my_ost = ostage + (size_t)warp * p.ost_n * 2048;   // this warp's staging boxes
         int osb = 0;                                          // next staging box
@@ -487,7 +490,8 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
                     fence_proxy_async();   // generic-proxy smem writes -> visible to the TMA (async proxy)
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&tmL, box, v0t + (e + 4 * j) * 16, row - lane);
+                        if (p.out_keep) tma_store_2d_hint(&tmL, box, v0t + (e + 4 * j) * 16, row - lane, pol_keep);
+                        else tma_store_2d(&tmL, box, v0t + (e + 4 * j) * 16, row - lane);
                         bulk_commit();
                     }
                     if (p.ost_n == 2) osb ^= 1;
