@@ -384,6 +384,23 @@ def test_verify_host_staged_q_rows(B, g, V, d):
             assert len(rows) > 0   # the Qwen-shape GEMM time covers several rows
 
 
+@pytest.mark.parametrize("B,g", [(1, 3), (2, 3), (6, 3)])
+def test_verify_host_small_batches_vs_oracle(B, g):
+    """nj_verify_host with host-resident q takes the staged step even where the
+    device-buffer AUTO rule picks the fused kernel (N <= 24): decisions against
+    the oracle, exact outside the tie band (band-aware check of tests/parity.py)."""
+    b = make_batch(B, g, V=4096, d=128, seed=40 + B, device=DEV)
+    v = Verifier(128, 4096, max_batch=B, gamma_max=5)
+    pin = lambda t: t.cpu().pin_memory()
+    acc_h = torch.full((B,), -7, dtype=torch.int32).pin_memory()
+    nxt_h = torch.full((B,), -7, dtype=torch.int32).pin_memory()
+    v.verify_host(pin(b.hidden), b.W, pin(b.draft_tokens), pin(b.draft_probs), b.gamma, pin(b.uniforms),
+                  acc_h, nxt_h)
+    n = b.to_numpy()
+    parity.check(f"verify_host small B={B}", n, acc_h.numpy(), nxt_h.numpy(),
+                 L=oracle.logits(n["hidden_bits"], n["W_bits"]), certified=True)
+
+
 def test_invalid_arguments():
     b = make_batch(2, 3, V=256, d=32, seed=1, device=DEV)
     v = Verifier(32, 256, max_batch=2, gamma_max=2)
