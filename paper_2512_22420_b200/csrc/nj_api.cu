@@ -783,8 +783,9 @@ nj_status launch_lm(nj_ctx* c, cudaStream_t st, const uint16_t* h, const uint16_
     // full kernel -7 % at R = 1536, -4 % at 768, -7 % at R = 256).
     // Single CTAs, one chunk (R <= 128, HBM-bound: C2): 2-k-block stages as well (fewer,
     // larger stages stream W faster: C2 214.1 -> 210.4 us/step, same-box
-    // A/B); several single-CTA chunks: 1-k-block stages (a 92-KB stage leaves 2; equal)
-    p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : ((CG == 2 || pl.nchunks == 1) ? 2 : 1);
+    // A/B); several single-CTA chunks too, although two 92-KB stages are all that fit
+    // (interleaved A/B: R = 160 / 192 / 288 / 320 / 384 -8 / -6 / -9 / -7 / -7 %)
+    p.gk = c->kn.lm_gk > 0 ? c->kn.lm_gk : 2;
     while (p.gk > 1 && (kSmemLimit - tail - 1024) / ((size_t)p.gk * kb_bytes) < 2) --p.gk;
     const size_t stage = (size_t)p.gk * kb_bytes;
     int S = (int)std::min<size_t>(8, (kSmemLimit - tail - 1024) / stage);
