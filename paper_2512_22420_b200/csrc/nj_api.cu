@@ -106,7 +106,7 @@ struct Knobs {
     int fgroups = -1, kpd = -1, sacc = -1, kgroup = -1, phase_ts = 0;       // fused kernel
     int big_gk = -1, big_nbuf = -1, big_dbg = 0, spin = 0, stats = 1, sleep_ns = 0, big_s = -1;   // k_gemm_big
     int w_evict_first = -1, mass_probe = 0;
-    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1, hostq_fused = 0, small_coop = 1, lm_out_keep = 0;   // k_lmhead; k_sample_small
+    int lm = 1, lm_cg = 0, lm_tw = 256, lm_gk = 0, lm_s = 0, lm_dbg = 0, lm_nbuf = 0, lm_ks = 0, lm_tma_out = 1, lm_pf = -1, lm_mb = 0, lm_ost = 1, lm_ks0 = 0, lm_arv1 = 0, lm_w = 0, lm_fence = 0, lm_mma4 = 0, small = 1, small_pdl = 1, small_cl16 = 1, qpf = 0, small_pf = 0, lm_sleep = 0, small_bmax = 12, inline_lse = kInlineLseRows, small_trig = 0, lm_pdl = 0, small_cl12 = 1, small_reuse = 1, small_cl = 0, qstage_gbs = 50, pdl_chain = 0, small_flat = 1, hostq_fused = 0, small_coop = 1, lm_out_keep = 0, lm_zero = 1;   // k_lmhead; k_sample_small
 };
 int env_int(const char* name, int dflt) {
     const char* e = getenv(name);
@@ -166,7 +166,8 @@ Knobs read_knobs() {
     // the GEMM's tail and the rejected rows' chunks from ~144 CTAs at once (e2e +13..19 % at
     // B = 8-16, scripts/e2e_path.py)
     k.hostq_fused = env_int("NJ_HOSTQ_FUSED", 0);
-    k.lm_out_keep = env_int("NJ_LM_OUT_KEEP", 0);   // evict_last hint on small staged logits stores
+    k.lm_out_keep = env_int("NJ_LM_OUT_KEEP", 0);
+    k.lm_zero = env_int("NJ_LM_ZERO", 1);           // staged step: k_lmhead zeroes the fallback block   // evict_last hint on small staged logits stores
     k.small_coop = env_int("NJ_SMALL_COOP", 1);     // flat sampler launched cooperatively (co-residency guaranteed)
     k.pdl_chain = env_int("NJ_PDL_CHAIN", 0);       // staged multi-kernel sampler as a PDL chain (no gain measured:
                                                     // B = 16 / 64 / 256 equal within the box's noise)    // host-link GB/s assumed by the q-row staging budget         // tests: force the cluster size (2, 4, 8, 12, 16; 0 = auto)
@@ -1525,7 +1526,11 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
     } else if (pl.path == NJ_PATH_STAGED) {
         // one GEMM pass over all N rows: per-row stats, draft-logit capture, and every
         // row's fp32 logits stored with an L2 evict_last policy (W streams evict_first)
-        NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 3 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
+        // the fallback block (queue, flags, the flat sampler's arrival counters) is zeroed by
+        // k_lmhead's first CTA (NJ_LM_ZERO; no memset node in the step) or by a memset
+        const bool zero_in_lm = c->kn.lm && c->kn.lm_zero;
+        if (!zero_in_lm)
+            NJ_CUDA(c, cudaMemsetAsync(c->fb_block, 0, (1 + 3 * (size_t)c->cfg.max_batch) * sizeof(int32_t), st));
         if (dbg && dbg->lse) NJ_CUDA(c, cudaMemsetAsync(dbg->lse, 0xFF, (size_t)pl.N * sizeof(float), st));
         GemmBigParams gp{};
         gp.logits = c->logits_st; gp.ld_out = c->V_local;
@@ -1548,6 +1553,10 @@ nj_status nj_verify(nj_ctx* c, void* stream, const uint16_t* hidden, const uint1
             lp.tok = draft_tokens; lp.dl = c->dl;
             lp.cap_staged = 1;
             lp.pdl = (small_flat_on(c) && small_sampler_ok(c, pl)) ? 1 : 0;   // k_sample_small<FLAT> follows
+            if (zero_in_lm) {
+                lp.zero_ptr = c->fb_block;
+                lp.zero_n = 1 + 3 * c->cfg.max_batch;
+            }
             lp.B = pl.B;
             for (int b = 0; b <= pl.B; ++b) lp.row_off[b] = pl.row_off[b];
             // small batches: the q rows into L2 during the GEMM (the sampler reads the rejected

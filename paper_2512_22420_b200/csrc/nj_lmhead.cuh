@@ -57,6 +57,8 @@ struct LmheadParams {
     int32_t arv1;                // 1: one accumulator-release arrival per CTA (named barrier first)
     int32_t fence_full;          // probe: tcgen05.fence::after_thread_sync after every operand wait
     int32_t mma4;                // 1: a k-block's four MMAs issued from one asm block under one elect
+    int32_t* zero_ptr;           // staged step: CTA 0 zeroes zero_ptr[0, zero_n) (the fallback block the
+    int32_t zero_n;              //    sampler kernels read after this grid; replaces a memset node)
     int32_t out_keep;            // 1: TMA logits stores with an L2 evict_last hint (small R: the sampler
                                  //    re-reads them right after; W streams evict_first)
     int32_t pdl;                 // 1: trigger the dependent grid's launch at the start (k_sample_small's
@@ -160,6 +162,8 @@ k_lmhead(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtens
     const int ngk = (p.num_kb + GK - 1) / GK;
 
     if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // every thread
+    if (p.zero_ptr && blockIdx.x == 0)
+        for (int i = threadIdx.x; i < p.zero_n; i += kLmThreads) p.zero_ptr[i] = 0;
     if (threadIdx.x == 0) {
         tma_prefetch_desc(&tmW);
         tma_prefetch_desc(&tmH);
